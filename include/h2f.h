@@ -1,0 +1,168 @@
+/*
+ * h2f.h — C ABI of the B200 RS-S factorize/solve path (libh2f.so).
+ *
+ * The reference (h2factor, pure Python) has no FFI; its boundary is the Python
+ * API in /root/reference/pkg/src/h2factor/__init__.py:11-26.  Each entry point
+ * below is what a ctypes/cffi binding of that API binds:
+ *
+ *   h2f_matrix_create   H2Matrix as consumed by factorize()      h2core.py:97-125
+ *   h2f_matvec          matvec(h2, x)                             h2core.py:285-315
+ *   h2f_norm2           estimate_norm2(h2, iters, seed)           h2core.py:318-330
+ *   h2f_factorize       factorize(h2, eps_lu, threads, norm_est)  factorization.py:204-271
+ *   h2f_solve           solve(fac, b) / solve_multi(fac, B)       solve.py:29-60
+ *   h2f_refined_solve   refined_solve(h2, fac, b, steps)          solve.py:63-77
+ *   h2f_factor_*        H2Factorization / LevelRecord / ClusterFactor fields
+ *                                                                 factorization.py:130-193
+ *   h2f_greedy_coloring greedy_coloring + color_groups            structure.py:148-167
+ *
+ * Conventions: every function returns 0 on success and a nonzero H2F_E* code
+ * otherwise (never throws across the ABI); h2f_last_error() gives the message.
+ * Pointers are HOST pointers unless the name ends in _dev.  All matrices are
+ * row-major (C order, like NumPy).  Vectors are in tree order.  Calls are
+ * synchronous on return and run on the library's own CUDA stream
+ * (h2f_stream()).  One process = one device context.
+ */
+#ifndef H2F_H
+#define H2F_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    H2F_OK = 0,
+    H2F_E_ARG = 1,        /* invalid argument / shape (ValueError)               */
+    H2F_E_CUDA = 2,       /* CUDA runtime failure                                 */
+    H2F_E_NOMEM = 3,      /* device arena exhausted                               */
+    H2F_E_SINGULAR = 4,   /* FactorizationError: vanishing pivot                  */
+    H2F_E_INTERNAL = 5    /* broken bookkeeping invariant (AssertionError)        */
+};
+
+typedef struct h2f_matrix_s* h2f_matrix;
+typedef struct h2f_factor_s* h2f_factor;
+
+/* Cluster tree + block partition + block values.  Node ids are the
+ * reference's preorder ids (geometry.py:85-142).  Pair lists are canonical
+ * (s <= t) and sorted, one list per level (structure.py:42-85). */
+typedef struct {
+    int64_t n;               /* number of points                                 */
+    int32_t depth;           /* tree depth (leaves at this level)                */
+    int32_t top_level;       /* shallowest level with admissible blocks, -1 none */
+    int64_t num_nodes;
+    const int64_t* parent;   /* [num_nodes]                                      */
+    const int64_t* child_left, *child_right, *level, *begin, *end;
+    const int64_t* rank;     /* [num_nodes] basis rank, -1 where no basis        */
+    /* per-level pair lists: pairs[2*i], pairs[2*i+1]; level l owns
+     * [ptr[l], ptr[l+1]) */
+    const int64_t* adm_pairs;   const int64_t* adm_ptr;     /* admissible leaves   */
+    const int64_t* inner_pairs; const int64_t* inner_ptr;   /* inadmissible inner  */
+    const int64_t* dense_pairs; const int64_t* dense_ptr;   /* inadmissible leaves */
+    /* element offsets into vals (-1 = absent):
+     *   leaf_basis_off[node]  (m_c x rank_c)       transfer_off[node] (rank_c x rank_parent)
+     *   coupling_off[i]  for adm pair i  (rank_s x rank_t)
+     *   dense_off[i]     for dense pair i (m_s x m_t) */
+    const int64_t* leaf_basis_off;
+    const int64_t* transfer_off;
+    const int64_t* coupling_off;
+    const int64_t* dense_off;
+    int64_t nvals;
+} h2f_matrix_desc;
+
+/* status of a factorization: for H2F_E_SINGULAR, cluster/level name the
+ * cluster whose redundant block failed (cluster = -1: the final dense LU). */
+typedef struct {
+    int32_t code;
+    int32_t cluster;
+    int32_t level;
+} h2f_status;
+
+typedef struct {
+    int64_t n;
+    int32_t top_level;       /* -1 when there are no records                     */
+    int32_t num_records;
+    int64_t top_size;
+    double eps_lu, eps_fill, norm_estimate;
+    int64_t nbytes;          /* H2Factorization.nbytes() accounting              */
+    /* phase seconds: norm, extract, color, augment, project, partial_lu,
+     * transition, top */
+    double phase_seconds[8];
+} h2f_factor_info;
+
+typedef struct {
+    int32_t level;
+    int32_t num_clusters;
+    int32_t num_batches;
+    int32_t csp, ncolors, graph_degree, max_rank;
+    int64_t total_size;      /* length of the level vector                       */
+    int64_t up_size;         /* length of up_index                               */
+    int64_t batch_entries;   /* sum of batch lengths                             */
+    double time_s;
+} h2f_level_info;
+
+typedef struct {
+    int32_t cluster, level;
+    int32_t size;            /* s: q is s x s                                    */
+    int32_t r;               /* redundant count; lu is r x r, piv r             */
+    int32_t num_edges;
+    int64_t offset;          /* offset in the level vector                       */
+} h2f_cluster_info;
+
+/* ---- context ------------------------------------------------------------ */
+int h2f_init(int device, double arena_gb);   /* arena_gb <= 0: automatic      */
+const char* h2f_last_error(void);
+int h2f_stream(void** stream_out);           /* cudaStream_t of the library    */
+int h2f_device_count(int* count);
+int h2f_kernel_launches(int64_t* count);     /* kernels launched so far        */
+int h2f_memory_stats(int64_t* arena_bytes, int64_t* in_use, int64_t* peak);
+
+/* ---- H2 matrix ----------------------------------------------------------- */
+int h2f_matrix_create(const h2f_matrix_desc* desc, const double* vals, h2f_matrix* out);
+int h2f_matrix_destroy(h2f_matrix m);
+int h2f_matrix_nbytes(h2f_matrix m, int64_t* bytes);
+int h2f_matvec(h2f_matrix m, const double* x, double* y, int64_t nrhs);
+int h2f_matvec_dev(h2f_matrix m, const double* x_dev, double* y_dev, int64_t nrhs);
+int h2f_norm2(h2f_matrix m, const double* v0, int32_t iters, double* est);
+
+/* ---- factorization ------------------------------------------------------- */
+/* norm_estimate < 0: run h2f_norm2 with start vector v0 (n values, already
+ * normalised, e.g. Philox(20240901) as in h2core.py:320-322). */
+int h2f_factorize(h2f_matrix m, double eps_lu, double norm_estimate, const double* v0,
+                  h2f_factor* out, h2f_status* status);
+int h2f_factor_destroy(h2f_factor f);
+int h2f_solve(h2f_factor f, const double* b, double* x, int64_t nrhs);
+int h2f_solve_dev(h2f_factor f, const double* b_dev, double* x_dev, int64_t nrhs);
+int h2f_refined_solve(h2f_matrix m, h2f_factor f, const double* b, double* x, int32_t steps);
+int h2f_refined_solve_dev(h2f_matrix m, h2f_factor f, const double* b_dev, double* x_dev,
+                          int32_t steps);
+
+/* ---- factor introspection (lazy export to host) ---------------------------- */
+int h2f_factor_info_get(h2f_factor f, h2f_factor_info* info);
+int h2f_factor_level_info(h2f_factor f, int32_t rec, h2f_level_info* info);
+/* clusters/offsets/sizes [num_clusters]; batch_ptr [num_batches+1];
+ * batch_ids [batch_entries]; up_index [up_size]  (any may be NULL) */
+int h2f_factor_level_arrays(h2f_factor f, int32_t rec, int64_t* clusters, int64_t* offsets,
+                            int64_t* sizes, int64_t* batch_ptr, int64_t* batch_ids,
+                            int64_t* up_index);
+int h2f_factor_cluster_info(h2f_factor f, int32_t rec, int32_t cluster, h2f_cluster_info* ci);
+/* q: s*s row-major; lu: r*r row-major; piv: r (0-based LAPACK swaps);
+ * edge_other/kind [num_edges] (kind 0 self, 1 full, 2 skel), edge_width [num_edges] */
+int h2f_factor_cluster_arrays(h2f_factor f, int32_t rec, int32_t cluster, double* q,
+                              double* lu, int32_t* piv, int64_t* edge_other,
+                              int32_t* edge_kind, int64_t* edge_width);
+/* edge matrix e: r x edge_width[e] row-major */
+int h2f_factor_cluster_edge(h2f_factor f, int32_t rec, int32_t cluster, int32_t e, double* mat);
+int h2f_factor_top(h2f_factor f, double* top_lu, int32_t* top_piv);
+
+/* ---- scheduling primitives (exposed for parity tests) ---------------------- */
+/* greedy colouring in ascending id order of the graph given by canonical
+ * pairs over `clusters`; colors_out[i] = colour of clusters[i]. */
+int h2f_greedy_coloring(int64_t num_clusters, const int64_t* clusters, int64_t num_pairs,
+                        const int64_t* pairs, int32_t* colors_out, int32_t* num_colors,
+                        int32_t* max_degree);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2F_H */

@@ -1,0 +1,179 @@
+"""ctypes binding of libh2f.so (include/h2f.h).
+
+The library is required: there is no CPU fallback anywhere in the package.
+Importing works without a GPU (so the CPU test suite can check the exported
+symbols); the first compute call initialises the CUDA context and raises if
+no device or no library is available.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libh2f.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "h2f.h")
+
+H2F_OK, H2F_E_ARG, H2F_E_CUDA, H2F_E_NOMEM, H2F_E_SINGULAR, H2F_E_INTERNAL = range(6)
+
+i64p = C.POINTER(C.c_int64)
+i32p = C.POINTER(C.c_int32)
+f64p = C.POINTER(C.c_double)
+
+
+class MatrixDesc(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("depth", C.c_int32), ("top_level", C.c_int32), ("num_nodes", C.c_int64),
+        ("parent", i64p), ("child_left", i64p), ("child_right", i64p), ("level", i64p),
+        ("begin", i64p), ("end", i64p), ("rank", i64p),
+        ("adm_pairs", i64p), ("adm_ptr", i64p),
+        ("inner_pairs", i64p), ("inner_ptr", i64p),
+        ("dense_pairs", i64p), ("dense_ptr", i64p),
+        ("leaf_basis_off", i64p), ("transfer_off", i64p), ("coupling_off", i64p), ("dense_off", i64p),
+        ("nvals", C.c_int64),
+    ]
+
+
+class Status(C.Structure):
+    _fields_ = [("code", C.c_int32), ("cluster", C.c_int32), ("level", C.c_int32)]
+
+
+class FactorInfo(C.Structure):
+    _fields_ = [("n", C.c_int64), ("top_level", C.c_int32), ("num_records", C.c_int32),
+                ("top_size", C.c_int64), ("eps_lu", C.c_double), ("eps_fill", C.c_double),
+                ("norm_estimate", C.c_double), ("nbytes", C.c_int64),
+                ("phase_seconds", C.c_double * 8)]
+
+
+class LevelInfo(C.Structure):
+    _fields_ = [("level", C.c_int32), ("num_clusters", C.c_int32), ("num_batches", C.c_int32),
+                ("csp", C.c_int32), ("ncolors", C.c_int32), ("graph_degree", C.c_int32),
+                ("max_rank", C.c_int32), ("total_size", C.c_int64), ("up_size", C.c_int64),
+                ("batch_entries", C.c_int64), ("time_s", C.c_double)]
+
+
+class ClusterInfo(C.Structure):
+    _fields_ = [("cluster", C.c_int32), ("level", C.c_int32), ("size", C.c_int32), ("r", C.c_int32),
+                ("num_edges", C.c_int32), ("offset", C.c_int64)]
+
+
+_SIGS = {
+    "h2f_init": (C.c_int, [C.c_int, C.c_double]),
+    "h2f_last_error": (C.c_char_p, []),
+    "h2f_stream": (C.c_int, [C.POINTER(C.c_void_p)]),
+    "h2f_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "h2f_kernel_launches": (C.c_int, [i64p]),
+    "h2f_memory_stats": (C.c_int, [i64p, i64p, i64p]),
+    "h2f_matrix_create": (C.c_int, [C.POINTER(MatrixDesc), f64p, C.POINTER(C.c_void_p)]),
+    "h2f_matrix_destroy": (C.c_int, [C.c_void_p]),
+    "h2f_matrix_nbytes": (C.c_int, [C.c_void_p, i64p]),
+    "h2f_matvec": (C.c_int, [C.c_void_p, f64p, f64p, C.c_int64]),
+    "h2f_matvec_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
+    "h2f_norm2": (C.c_int, [C.c_void_p, f64p, C.c_int32, f64p]),
+    "h2f_factorize": (C.c_int, [C.c_void_p, C.c_double, C.c_double, f64p, C.POINTER(C.c_void_p),
+                                C.POINTER(Status)]),
+    "h2f_factor_destroy": (C.c_int, [C.c_void_p]),
+    "h2f_solve": (C.c_int, [C.c_void_p, f64p, f64p, C.c_int64]),
+    "h2f_solve_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
+    "h2f_refined_solve": (C.c_int, [C.c_void_p, C.c_void_p, f64p, f64p, C.c_int32]),
+    "h2f_refined_solve_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
+    "h2f_factor_info_get": (C.c_int, [C.c_void_p, C.POINTER(FactorInfo)]),
+    "h2f_factor_level_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(LevelInfo)]),
+    "h2f_factor_level_arrays": (C.c_int, [C.c_void_p, C.c_int32, i64p, i64p, i64p, i64p, i64p, i64p]),
+    "h2f_factor_cluster_info": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(ClusterInfo)]),
+    "h2f_factor_cluster_arrays": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f64p, f64p, i32p, i64p,
+                                            i32p, i64p]),
+    "h2f_factor_cluster_edge": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, f64p]),
+    "h2f_factor_top": (C.c_int, [C.c_void_p, f64p, i32p]),
+    "h2f_greedy_coloring": (C.c_int, [C.c_int64, i64p, C.c_int64, i64p, i32p, i32p, i32p]),
+}
+
+_lib = None
+_initialised = False
+
+
+class H2FError(RuntimeError):
+    """A failure reported by libh2f (CUDA error, arena exhausted, ...)."""
+
+
+def header_symbols():
+    """Function names declared in include/h2f.h."""
+    with open(HEADER) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"\b(h2f_[a-z0-9_]+)\s*\(", text)))
+
+
+def lib():
+    """The loaded library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2509_11152_b200.build` "
+                              "(there is no CPU fallback)")
+        handle = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def last_error():
+    msg = lib().h2f_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(code, what=""):
+    if code == H2F_OK:
+        return
+    msg = last_error()
+    if code == H2F_E_ARG:
+        raise ValueError(msg)
+    if code == H2F_E_INTERNAL:
+        raise AssertionError(msg)
+    raise H2FError(f"{what}: {msg}" if what else msg)
+
+
+def ensure_init(device=None):
+    """Create the library's CUDA context (once per process)."""
+    global _initialised
+    if not _initialised:
+        dev = int(os.environ.get("H2F_DEVICE", "0")) if device is None else device
+        arena = float(os.environ.get("H2F_ARENA_GB", "0"))
+        check(lib().h2f_init(dev, arena), "h2f_init")
+        _initialised = True
+    return lib()
+
+
+def ptr(a, typ=f64p):
+    return a.ctypes.data_as(typ)
+
+
+def as_f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def as_i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def kernel_launches():
+    v = C.c_int64()
+    lib().h2f_kernel_launches(C.byref(v))
+    return v.value
+
+
+def stream_handle():
+    s = C.c_void_p()
+    check(ensure_init().h2f_stream(C.byref(s)))
+    return s.value
+
+
+def memory_stats():
+    a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+    check(ensure_init().h2f_memory_stats(C.byref(a), C.byref(b), C.byref(c)))
+    return {"arena_bytes": a.value, "in_use": b.value, "peak": c.value}

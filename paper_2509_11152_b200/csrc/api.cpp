@@ -1,0 +1,359 @@
+// C ABI (include/h2f.h).  Never throws across the boundary: every entry point
+// converts h2f::Error / std::exception into a status code + h2f_last_error().
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "factor.h"
+
+using namespace h2f;
+
+struct h2f_matrix_s {
+    H2Mat* m;
+};
+struct h2f_factor_s {
+    Factorization* f;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class Fn> int guard(Fn&& fn) {
+    try {
+        fn();
+        return H2F_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return H2F_E_INTERNAL;
+    }
+}
+
+// device buffer borrowed from the arena for a host-pointer call
+struct DevBuf {
+    double* p = nullptr;
+    explicit DevBuf(size_t n) { p = static_cast<double*>(dalloc(sizeof(double) * std::max<size_t>(n, 1))); }
+    ~DevBuf() {
+        if (p) dfree(p);
+    }
+};
+
+const LevelRecord& rec_at(h2f_factor f, int32_t rec) {
+    if (!f || !f->f) throw Error(H2F_E_ARG, "null factor");
+    if (rec < 0 || rec >= int32_t(f->f->recs.size())) throw Error(H2F_E_ARG, "record index out of range");
+    return f->f->recs[rec];
+}
+
+const ClusterFactor& cf_at(h2f_factor f, int32_t rec, int32_t cluster) {
+    const LevelRecord& r = rec_at(f, rec);
+    auto it = r.pos.find(cluster);
+    if (it == r.pos.end()) throw Error(H2F_E_ARG, "cluster not in record");
+    return r.factors[it->second];
+}
+
+void d2h(void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    H2F_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx().stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+int h2f_init(int device, double arena_gb) {
+    return guard([&] { ctx_init(device, arena_gb); });
+}
+
+const char* h2f_last_error(void) { return g_err.c_str(); }
+
+int h2f_stream(void** stream_out) {
+    return guard([&] { *stream_out = reinterpret_cast<void*>(ctx().stream); });
+}
+
+int h2f_device_count(int* count) {
+    return guard([&] { H2F_CUDA(cudaGetDeviceCount(count)); });
+}
+
+int h2f_kernel_launches(int64_t* count) {
+    *count = kernel_launch_count();
+    return H2F_OK;
+}
+
+int h2f_memory_stats(int64_t* arena_bytes, int64_t* in_use, int64_t* peak) {
+    return guard([&] {
+        Context& X = ctx();
+        *arena_bytes = int64_t(X.arena.capacity());
+        *in_use = int64_t(X.arena.in_use());
+        *peak = int64_t(X.arena.peak());
+    });
+}
+
+int h2f_matrix_create(const h2f_matrix_desc* desc, const double* vals, h2f_matrix* out) {
+    return guard([&] {
+        if (!desc || !out) throw Error(H2F_E_ARG, "null argument");
+        H2Mat* m = h2mat_create(desc, vals);
+        *out = new h2f_matrix_s{m};
+    });
+}
+
+int h2f_matrix_destroy(h2f_matrix m) {
+    return guard([&] {
+        if (!m) return;
+        ctx().sync();
+        delete m->m;
+        delete m;
+    });
+}
+
+int h2f_matrix_nbytes(h2f_matrix m, int64_t* bytes) {
+    return guard([&] { *bytes = m->m->nvals * 8; });
+}
+
+int h2f_matvec_dev(h2f_matrix m, const double* x_dev, double* y_dev, int64_t nrhs) {
+    return guard([&] {
+        if (nrhs < 1) throw Error(H2F_E_ARG, "nrhs must be >= 1");
+        matvec_device(*m->m, x_dev, y_dev, int(nrhs));
+        ctx().sync();
+    });
+}
+
+int h2f_matvec(h2f_matrix m, const double* x, double* y, int64_t nrhs) {
+    return guard([&] {
+        if (nrhs < 1) throw Error(H2F_E_ARG, "nrhs must be >= 1");
+        const size_t n = size_t(m->m->n) * nrhs;
+        DevBuf dx(n), dy(n);
+        H2F_CUDA(cudaMemcpyAsync(dx.p, x, n * 8, cudaMemcpyHostToDevice, ctx().stream));
+        matvec_device(*m->m, dx.p, dy.p, int(nrhs));
+        d2h(y, dy.p, n * 8);
+        ctx().sync();
+    });
+}
+
+int h2f_norm2(h2f_matrix m, const double* v0, int32_t iters, double* est) {
+    return guard([&] { *est = norm2_estimate(*m->m, v0, iters); });
+}
+
+int h2f_factorize(h2f_matrix m, double eps_lu, double norm_estimate, const double* v0, h2f_factor* out,
+                  h2f_status* status) {
+    if (status) *status = {H2F_OK, -1, -1};
+    try {
+        Factorization* f = factorize(*m->m, eps_lu, norm_estimate, v0);
+        *out = new h2f_factor_s{f};
+        return H2F_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        if (status) *status = {e.code, e.cluster, e.level};
+        try {
+            ctx().sync();
+        } catch (...) {
+        }
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        if (status) *status = {H2F_E_INTERNAL, -1, -1};
+        return H2F_E_INTERNAL;
+    }
+}
+
+int h2f_factor_destroy(h2f_factor f) {
+    return guard([&] {
+        if (!f) return;
+        ctx().sync();
+        delete f->f;
+        delete f;
+    });
+}
+
+int h2f_solve_dev(h2f_factor f, const double* b_dev, double* x_dev, int64_t nrhs) {
+    return guard([&] {
+        if (nrhs < 1) throw Error(H2F_E_ARG, "nrhs must be >= 1");
+        solve_device(*f->f, b_dev, x_dev, int(nrhs));
+        ctx().sync();
+    });
+}
+
+int h2f_solve(h2f_factor f, const double* b, double* x, int64_t nrhs) {
+    return guard([&] {
+        if (nrhs < 1) throw Error(H2F_E_ARG, "nrhs must be >= 1");
+        const size_t n = size_t(f->f->n) * nrhs;
+        DevBuf db(n), dx(n);
+        H2F_CUDA(cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, ctx().stream));
+        solve_device(*f->f, db.p, dx.p, int(nrhs));
+        d2h(x, dx.p, n * 8);
+        ctx().sync();
+    });
+}
+
+int h2f_refined_solve_dev(h2f_matrix m, h2f_factor f, const double* b_dev, double* x_dev, int32_t steps) {
+    return guard([&] {
+        refined_solve_device(*m->m, *f->f, b_dev, x_dev, steps);
+        ctx().sync();
+    });
+}
+
+int h2f_refined_solve(h2f_matrix m, h2f_factor f, const double* b, double* x, int32_t steps) {
+    return guard([&] {
+        const size_t n = size_t(f->f->n);
+        DevBuf db(n), dx(n);
+        H2F_CUDA(cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, ctx().stream));
+        refined_solve_device(*m->m, *f->f, db.p, dx.p, steps);
+        d2h(x, dx.p, n * 8);
+        ctx().sync();
+    });
+}
+
+int h2f_factor_info_get(h2f_factor f, h2f_factor_info* info) {
+    return guard([&] {
+        const Factorization& F = *f->f;
+        info->n = F.n;
+        info->top_level = F.top_level;
+        info->num_records = int32_t(F.recs.size());
+        info->top_size = F.top_size;
+        info->eps_lu = F.eps_lu;
+        info->eps_fill = F.eps_fill;
+        info->norm_estimate = F.norm_estimate;
+        info->nbytes = F.nbytes;
+        for (int i = 0; i < 8; ++i) info->phase_seconds[i] = F.phase[i];
+    });
+}
+
+int h2f_factor_level_info(h2f_factor f, int32_t rec, h2f_level_info* info) {
+    return guard([&] {
+        const LevelRecord& r = rec_at(f, rec);
+        info->level = r.level;
+        info->num_clusters = int32_t(r.clusters.size());
+        info->num_batches = int32_t(r.batches.size());
+        info->csp = r.csp;
+        info->ncolors = r.ncolors;
+        info->graph_degree = r.graph_degree;
+        info->max_rank = r.max_rank;
+        info->total_size = r.total();
+        info->up_size = int64_t(r.up_index.size());
+        int64_t be = 0;
+        for (auto& b : r.batches) be += int64_t(b.size());
+        info->batch_entries = be;
+        info->time_s = r.time_s;
+    });
+}
+
+int h2f_factor_level_arrays(h2f_factor f, int32_t rec, int64_t* clusters, int64_t* offsets, int64_t* sizes,
+                            int64_t* batch_ptr, int64_t* batch_ids, int64_t* up_index) {
+    return guard([&] {
+        const LevelRecord& r = rec_at(f, rec);
+        for (size_t i = 0; i < r.clusters.size(); ++i) {
+            if (clusters) clusters[i] = r.clusters[i];
+            if (offsets) offsets[i] = r.offset[i];
+            if (sizes) sizes[i] = r.size[i];
+        }
+        int64_t k = 0;
+        if (batch_ptr) batch_ptr[0] = 0;
+        for (size_t b = 0; b < r.batches.size(); ++b) {
+            for (int c : r.batches[b]) {
+                if (batch_ids) batch_ids[k] = c;
+                ++k;
+            }
+            if (batch_ptr) batch_ptr[b + 1] = k;
+        }
+        if (up_index) std::copy(r.up_index.begin(), r.up_index.end(), up_index);
+    });
+}
+
+int h2f_factor_cluster_info(h2f_factor f, int32_t rec, int32_t cluster, h2f_cluster_info* ci) {
+    return guard([&] {
+        const ClusterFactor& c = cf_at(f, rec, cluster);
+        ci->cluster = c.cluster;
+        ci->level = rec_at(f, rec).level;
+        ci->size = c.s;
+        ci->r = c.r;
+        ci->num_edges = int32_t(c.edges.size());
+        ci->offset = c.offset;
+    });
+}
+
+int h2f_factor_cluster_arrays(h2f_factor f, int32_t rec, int32_t cluster, double* q, double* lu, int32_t* piv,
+                              int64_t* edge_other, int32_t* edge_kind, int64_t* edge_width) {
+    return guard([&] {
+        const ClusterFactor& c = cf_at(f, rec, cluster);
+        if (q) d2h(q, c.q, sizeof(double) * c.s * c.s);
+        if (lu && c.r) d2h(lu, c.lu, sizeof(double) * c.r * c.r);
+        if (piv && c.r) d2h(piv, c.piv, sizeof(int32_t) * c.r);
+        for (size_t e = 0; e < c.edges.size(); ++e) {
+            if (edge_other) edge_other[e] = c.edges[e].other;
+            if (edge_kind) edge_kind[e] = c.edges[e].kind;
+            if (edge_width) edge_width[e] = c.edges[e].w;
+        }
+        ctx().sync();
+    });
+}
+
+int h2f_factor_cluster_edge(h2f_factor f, int32_t rec, int32_t cluster, int32_t e, double* mat) {
+    return guard([&] {
+        const ClusterFactor& c = cf_at(f, rec, cluster);
+        if (e < 0 || e >= int32_t(c.edges.size())) throw Error(H2F_E_ARG, "edge index out of range");
+        const EdgeRec& E = c.edges[e];
+        if (c.r && E.w)
+            H2F_CUDA(cudaMemcpy2DAsync(mat, sizeof(double) * E.w, E.mat, sizeof(double) * E.ld,
+                                       sizeof(double) * E.w, c.r, cudaMemcpyDeviceToHost, ctx().stream));
+        ctx().sync();
+    });
+}
+
+int h2f_factor_top(h2f_factor f, double* top_lu, int32_t* top_piv) {
+    return guard([&] {
+        const Factorization& F = *f->f;
+        if (top_lu) d2h(top_lu, F.top_lu, sizeof(double) * F.top_size * F.top_size);
+        if (top_piv) d2h(top_piv, F.top_piv, sizeof(int32_t) * F.top_size);
+        ctx().sync();
+    });
+}
+
+int h2f_greedy_coloring(int64_t num_clusters, const int64_t* clusters, int64_t num_pairs, const int64_t* pairs,
+                        int32_t* colors_out, int32_t* num_colors, int32_t* max_degree) {
+    // structure.py:137-167 (same algorithm as the factorization's level colouring)
+    return guard([&] {
+        std::vector<int64_t> ids(clusters, clusters + num_clusters);
+        std::vector<size_t> order(ids.size());
+        for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+        std::sort(order.begin(), order.end(), [&](size_t a, size_t b) { return ids[a] < ids[b]; });
+        std::unordered_map<int64_t, size_t> pos;
+        for (size_t i = 0; i < ids.size(); ++i) pos[ids[i]] = i;
+        std::vector<std::vector<size_t>> adj(ids.size());
+        for (int64_t p = 0; p < num_pairs; ++p) {
+            const int64_t s = pairs[2 * p], t = pairs[2 * p + 1];
+            if (s == t) continue;
+            auto is = pos.find(s), it = pos.find(t);
+            if (is == pos.end() || it == pos.end()) throw Error(H2F_E_ARG, "pair references unknown cluster");
+            adj[is->second].push_back(it->second);
+            adj[it->second].push_back(is->second);
+        }
+        int deg = 0;
+        for (auto& a : adj) {
+            std::sort(a.begin(), a.end());
+            a.erase(std::unique(a.begin(), a.end()), a.end());
+            deg = std::max(deg, int(a.size()));
+        }
+        std::vector<int32_t> col(ids.size(), -1);
+        int ncol = 0;
+        for (size_t i : order) {
+            std::vector<char> used;
+            for (size_t j : adj[i])
+                if (col[j] >= 0) {
+                    if (size_t(col[j]) >= used.size()) used.resize(col[j] + 1, 0);
+                    used[col[j]] = 1;
+                }
+            int c = 0;
+            while (size_t(c) < used.size() && used[c]) ++c;
+            col[i] = c;
+            ncol = std::max(ncol, c + 1);
+        }
+        std::copy(col.begin(), col.end(), colors_out);
+        *num_colors = ncol;
+        *max_degree = deg;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,1018 @@
+// RS-S factorization driver (Alg. 1/2; factorization.py:204-615) for B200.
+//
+// The host keeps only integer structure: the level's block maps (dense D, fill
+// F), neighbour lists, the greedy colouring and the batch picker (all
+// bit-exact with the reference), and the offsets of every block in the
+// device arena.  Every floating-point operation of a batch runs as a handful
+// of batched kernel launches over all clusters of the batch:
+//
+//   augment     copy(F-row gather) -> gemm(V^T Y) -> gemm(Y -= V C) -> qr_r ->
+//               jacobi(svd, kept, vbar) -> complement(Q~)            [1 sync: kept]
+//   project     gemm(Q~^T B | B Q~) (out of place, new arena views)
+//   eliminate   copy(G panels) -> lu -> trsm(-W) -> gemm(Schur targets +=,
+//               fill-candidate norms) -> reduce             [1 sync: norms, status]
+//               -> gemm(create the surviving fill blocks, in reference order)
+//   slice       host-only view arithmetic (factorization.py:513-523)
+//
+// Level transition and the dense top are batched copy launches plus a blocked
+// partial-pivot LU whose trailing updates run on the DMMA tile GEMM.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <numeric>
+#include <set>
+
+#include "factor.h"
+
+namespace h2f {
+
+namespace {
+
+constexpr double PIVOT_RTOL = 1e-14;      // factorization.py:47
+constexpr double FILL_DROP_FACTOR = 1e-2; // factorization.py:55
+
+struct View {
+    double* p = nullptr;
+    int64_t ld = 0;
+    int rows = 0, cols = 0;
+};
+
+struct CouplingW {    // coupling block with logical zero padding (factorization.py:396-403)
+    const double* p = nullptr;
+    int64_t ld = 0;
+    int rows = 0, cols = 0;
+};
+
+struct TransferW {    // transfer with logical zero rows (factorization.py:404-407)
+    const double* p = nullptr;
+    int64_t ld = 0;
+    int rows = 0, cols = 0;
+    bool has = false;
+};
+
+struct Entry {
+    Key key;
+    bool dense;
+};
+
+struct Lvl {
+    int level = 0;
+    std::vector<int> clusters;
+    std::unordered_map<int, int> pos;
+    std::vector<int64_t> offset, size;
+    std::vector<int> live, red, k;
+    std::vector<char> done;
+    std::vector<View> basis;
+    std::map<Key, View> D, F;
+    std::vector<std::map<int, Entry>> touch;
+    std::unordered_map<Key, CouplingW> S;
+    std::vector<TransferW> T;
+    Region mem{size_t(256) << 20};
+    std::vector<std::vector<int>> batches;
+    std::vector<ClusterFactor> factors;
+
+    int at(int c) const { return pos.at(c); }
+    void link(Key key, bool dense) {
+        touch[at(key_a(key))][key_b(key)] = {key, dense};
+        touch[at(key_b(key))][key_a(key)] = {key, dense};
+    }
+    View& block(Key key, bool dense) { return dense ? D.at(key) : F.at(key); }
+    View* find(Key key) {
+        auto it = D.find(key);
+        if (it != D.end()) return &it->second;
+        auto jt = F.find(key);
+        return jt != F.end() ? &jt->second : nullptr;
+    }
+    void init_common(const std::vector<int>& cl) {
+        clusters = cl;
+        const size_t n = cl.size();
+        for (size_t i = 0; i < n; ++i) pos[cl[i]] = int(i);
+        live.assign(n, 0);
+        red.assign(n, 0);
+        k.assign(n, 0);
+        done.assign(n, 0);
+        basis.assign(n, {});
+        touch.assign(n, {});
+        T.assign(n, {});
+        factors.assign(n, {});
+    }
+    void build_touch() {
+        for (auto& kv : D)
+            if (key_a(kv.first) != key_b(kv.first)) link(kv.first, true);
+        for (auto& kv : F) link(kv.first, false);
+    }
+};
+
+// ---- launch builders -----------------------------------------------------------
+struct GemmBuild {
+    std::vector<GemmTask> tasks;
+    std::vector<GemmContrib> contribs;
+    std::vector<int64_t> tile_start{0};
+    int64_t norm_tiles = 0;
+
+    static int64_t tiles(int M, int N) { return cdiv(M, GEMM_TILE) * cdiv(N, GEMM_TILE); }
+    // returns the task's norm base (mode NORM) or -1
+    int64_t add(double* C, int64_t ldc, int M, int N, int mode, const GemmContrib* cs, size_t nc) {
+        if (M <= 0 || N <= 0) return -1;
+        GemmTask t{};
+        t.C = C;
+        t.ldc = ldc;
+        t.M = M;
+        t.N = N;
+        t.mode = mode;
+        t.tiles_n = int(cdiv(N, GEMM_TILE));
+        t.contrib_begin = int64_t(contribs.size());
+        contribs.insert(contribs.end(), cs, cs + nc);
+        t.contrib_end = int64_t(contribs.size());
+        t.norm_base = -1;
+        const int64_t nt = tiles(M, N);
+        if (mode == GEMM_NORM) {
+            t.norm_base = norm_tiles;
+            norm_tiles += nt;
+        }
+        tasks.push_back(t);
+        tile_start.push_back(tile_start.back() + nt);
+        return t.norm_base;
+    }
+    int64_t add1(double* C, int64_t ldc, int M, int N, int mode, const GemmContrib& c) {
+        return add(C, ldc, M, N, mode, &c, 1);
+    }
+    void launch(double* norms = nullptr) {
+        if (tasks.empty()) return;
+        Context& X = ctx();
+        auto* dt = X.up.put(tasks);
+        auto* dc = X.up.put(contribs);
+        auto* ds = X.up.put(tile_start);
+        X.up.flush(X.stream);
+        launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), tile_start.back(), norms, X.stream);
+    }
+};
+
+inline GemmContrib contrib(const double* A, int64_t lda, int transA, const double* B, int64_t ldb,
+                           int transB, int K, double alpha = 1.0) {
+    GemmContrib c{};
+    c.A = A;
+    c.lda = lda;
+    c.transA = transA;
+    c.B = B;
+    c.ldb = ldb;
+    c.transB = transB;
+    c.K = K;
+    c.alpha = alpha;
+    return c;
+}
+
+struct CopyBuild {
+    std::vector<CopyTask> tasks;
+    std::vector<int64_t> tile_start{0};
+    void add(double* dst, int64_t ldd, int rows, int cols, const double* src, int64_t lds, int trans,
+             int mode, double alpha = 1.0) {
+        if (rows <= 0 || cols <= 0) return;
+        CopyTask t{};
+        t.dst = dst;
+        t.ldd = ldd;
+        t.rows = rows;
+        t.cols = cols;
+        t.src = src;
+        t.lds = lds;
+        t.trans = trans;
+        t.mode = mode;
+        t.alpha = alpha;
+        tasks.push_back(t);
+        tile_start.push_back(tile_start.back() + cdiv(rows, COPY_TILE) * cdiv(cols, COPY_TILE));
+    }
+    void zero(double* dst, int64_t ldd, int rows, int cols) { add(dst, ldd, rows, cols, nullptr, 0, 0, COPY_ZERO); }
+    void launch() {
+        if (tasks.empty()) return;
+        Context& X = ctx();
+        auto* dt = X.up.put(tasks);
+        auto* ds = X.up.put(tile_start);
+        X.up.flush(X.stream);
+        launch_copy_tasks(dt, ds, int32_t(tasks.size()), tile_start.back(), X.stream);
+    }
+};
+
+template <class T> T* upload(const std::vector<T>& v) {
+    Context& X = ctx();
+    T* d = X.up.put(v);
+    X.up.flush(X.stream);
+    return d;
+}
+
+// phase accounting from CUDA events (sums to the device-side wall time)
+class PhaseClock {
+  public:
+    ~PhaseClock() {
+        for (auto& e : marks_) cudaEventDestroy(e.first);
+    }
+    void mark(int phase) {
+        cudaEvent_t e;
+        H2F_CUDA(cudaEventCreate(&e));
+        H2F_CUDA(cudaEventRecord(e, ctx().stream));
+        marks_.push_back({e, phase});
+    }
+    size_t size() const { return marks_.size(); }
+    // call after a stream sync; returns seconds between mark i and j
+    double between(size_t i, size_t j) const {
+        float ms = 0.f;
+        H2F_CUDA(cudaEventElapsedTime(&ms, marks_[i].first, marks_[j].first));
+        return ms * 1e-3;
+    }
+    void accumulate(double* out) const {
+        for (size_t i = 0; i + 1 < marks_.size(); ++i)
+            if (marks_[i].second >= 0) out[marks_[i].second] += between(i, i + 1);
+    }
+
+  private:
+    std::vector<std::pair<cudaEvent_t, int>> marks_;
+};
+
+class Factorizer {
+  public:
+    Factorizer(H2Mat& m, Factorization& f) : M(m), F(f) {}
+    void run(double norm_estimate, const double* v0);
+
+  private:
+    H2Mat& M;
+    Factorization& F;
+    double eps_fill = 0, drop = 0;
+    PhaseClock clock;
+    Region scratch[2] = {Region(size_t(64) << 20), Region(size_t(64) << 20)};
+    int batch_counter = 0;
+    std::vector<size_t> level_marks;
+    std::vector<int> mark_node;  // node-indexed batch membership stamp
+    int stamp = 0;
+
+    std::unique_ptr<Lvl> leaf_level(int level);
+    void attach_couplings(Lvl& L);
+    void process_batch(Lvl& L, const std::vector<int>& batch);
+    std::unique_ptr<Lvl> transition(Lvl& L);
+    void finish_top(Lvl& L);
+    void dense_only_top();
+    void top_factor(double* A, int64_t n);
+    std::vector<std::pair<int, int>> dense_pairs(int level) const;
+};
+
+std::vector<std::pair<int, int>> Factorizer::dense_pairs(int level) const {
+    std::vector<std::pair<int, int>> out(M.inner[level]);
+    out.insert(out.end(), M.dense[level].begin(), M.dense[level].end());
+    std::sort(out.begin(), out.end());
+    out.erase(std::unique(out.begin(), out.end()), out.end());
+    return out;
+}
+
+std::unique_ptr<Lvl> Factorizer::leaf_level(int level) {
+    // factorization.py:288-327 (leaf: copies of the dense blocks)
+    auto L = std::make_unique<Lvl>();
+    L->level = level;
+    L->init_common(M.levels[level]);
+    const size_t n = L->clusters.size();
+    L->offset.resize(n);
+    L->size.resize(n);
+    for (size_t i = 0; i < n; ++i) {
+        const int c = L->clusters[i];
+        L->offset[i] = M.begin[c];
+        L->size[i] = M.rows(c);
+        if (M.top >= 0 && M.leaf_basis_off[c] >= 0) {
+            L->basis[i] = View{const_cast<double*>(M.leaf_basis(c)), M.rank[c], int(L->size[i]), int(M.rank[c])};
+        } else {
+            L->basis[i] = View{nullptr, 0, int(L->size[i]), 0};
+        }
+        L->k[i] = L->basis[i].cols;
+    }
+    CopyBuild cp;
+    for (int l = 0; l <= M.depth; ++l)
+        for (auto& pr : M.dense[l]) {
+            if (M.level[pr.first] != level || M.level[pr.second] != level)
+                throw Error(H2F_E_INTERNAL, "assertion: dense leaf block away from the leaf level");
+            const int rs = int(M.rows(pr.first)), cs = int(M.rows(pr.second));
+            double* dst = L->mem.alloc_n<double>(int64_t(rs) * cs);
+            cp.add(dst, cs, rs, cs, M.vals + M.dense_off.at(mkkey(pr.first, pr.second)), cs, 0, COPY_SET);
+            L->D[mkkey(pr.first, pr.second)] = View{dst, cs, rs, cs};
+        }
+    cp.launch();
+    L->build_touch();
+    return L;
+}
+
+void Factorizer::attach_couplings(Lvl& L) {
+    for (auto& pr : M.adm[L.level]) {
+        const Key key = mkkey(pr.first, pr.second);
+        CouplingW w;
+        w.p = M.coupling(key);
+        w.rows = int(M.rank[pr.first]);
+        w.cols = int(M.rank[pr.second]);
+        w.ld = w.cols;
+        L.S[key] = w;
+    }
+    if (L.level > M.top)
+        for (size_t i = 0; i < L.clusters.size(); ++i) {
+            const int c = L.clusters[i];
+            const int p = int(M.parent[c]);
+            TransferW t;
+            t.has = M.transfer_off[c] >= 0;
+            if (t.has) {
+                t.p = M.transfer(c);
+                t.rows = int(M.rank[c]);
+                t.cols = int(M.rank[p]);
+                t.ld = t.cols;
+            }
+            L.T[i] = t;
+        }
+}
+
+void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
+    Context& X = ctx();
+    cudaStream_t st = X.stream;
+    Region& scr = scratch[batch_counter++ & 1];
+    scr.reset();
+    const int nb = int(batch.size());
+    ++stamp;
+    for (int c : batch) mark_node[c] = stamp;
+    auto in_batch = [&](int c) { return mark_node[c] == stamp; };
+
+    // ------------------------------------------------------------- augment
+    clock.mark(PH_AUGMENT);
+    std::vector<double*> Q(nb);
+    int* kept_d = scr.alloc_n<int>(nb);
+    {
+        CopyBuild gather;
+        GemmBuild g1, g2;
+        std::vector<QrTask> qr;
+        std::vector<SvdTask> svd;
+        std::vector<ComplementTask> cmp;
+        for (int bi = 0; bi < nb; ++bi) {
+            const int c = batch[bi], ci = L.at(c);
+            const int s = int(L.size[ci]);
+            const View V = L.basis[ci];
+            const int k = V.cols;
+            // fill row: F blocks in sorted key order (== sorted by partner id)
+            struct Part { View v; int trans; int w; };
+            std::vector<Part> parts;
+            int wf = 0;
+            for (auto& kv : L.touch[ci]) {
+                if (kv.second.dense) continue;
+                const View& B = L.F.at(kv.second.key);
+                const bool row = key_a(kv.second.key) == c;
+                parts.push_back({B, row ? 0 : 1, row ? B.cols : B.rows});
+                wf += parts.back().w;
+            }
+            const bool skip = (wf == 0 || k == s);
+            const int m = skip ? 0 : std::min(s, wf);
+            double* R = scr.alloc_n<double>(int64_t(std::max(m, 1)) * s);
+            double* BT = scr.alloc_n<double>(int64_t(s) * s);
+            double* Wc = scr.alloc_n<double>(int64_t(s) * s);
+            double* cs = scr.alloc_n<double>(int64_t(16) * s);
+            Q[bi] = F.store.alloc_n<double>(int64_t(s) * s);
+            if (!skip) {
+                double* Y = scr.alloc_n<double>(int64_t(s) * wf);
+                int off = 0;
+                for (auto& p : parts) {
+                    gather.add(Y + off, wf, s, p.w, p.v.p, p.v.ld, p.trans, COPY_SET);
+                    off += p.w;
+                }
+                if (k > 0) {
+                    double* Cb = scr.alloc_n<double>(int64_t(k) * wf);
+                    g1.add1(Cb, wf, k, wf, GEMM_STORE, contrib(V.p, V.ld, 1, Y, wf, 0, s));
+                    g2.add1(Y, wf, s, wf, GEMM_ADD, contrib(V.p, V.ld, 0, Cb, wf, 0, k, -1.0));
+                }
+                qr.push_back(QrTask{Y, R, wf, s, wf});
+            }
+            SvdTask sv{};
+            sv.R = R;
+            sv.V = V.p;
+            sv.BT = BT;
+            sv.ldv = V.ld;
+            sv.m = m;
+            sv.s = s;
+            sv.k = k;
+            sv.skip = skip ? 1 : 0;
+            sv.kept_out = kept_d + bi;
+            svd.push_back(sv);
+            ComplementTask ct{};
+            ct.BT = BT;
+            ct.W = Wc;
+            ct.Q = Q[bi];
+            ct.scratch = cs;
+            ct.kept = kept_d + bi;
+            ct.s = s;
+            ct.k = k;
+            cmp.push_back(ct);
+        }
+        gather.launch();
+        g1.launch();
+        g2.launch();
+        if (!qr.empty()) launch_qr_r(upload(qr), int32_t(qr.size()), st);
+        launch_jacobi(upload(svd), int32_t(svd.size()), drop, st);
+        launch_complement(upload(cmp), int32_t(cmp.size()), st);
+    }
+    int* kept_h = static_cast<int*>(X.pinned_buf(sizeof(int) * nb));
+    H2F_CUDA(cudaMemcpyAsync(kept_h, kept_d, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
+    X.sync();
+    std::vector<int> kept(kept_h, kept_h + nb);
+    for (int bi = 0; bi < nb; ++bi) {
+        const int c = batch[bi], ci = L.at(c);
+        const int kt = L.k[ci] + kept[bi];
+        if (kt > L.size[ci]) throw Error(H2F_E_INTERNAL, "assertion: augmented basis wider than the cluster");
+        L.red[ci] = int(L.size[ci]) - kt;
+        L.k[ci] = kt;
+        // zero padding of couplings / transfer is logical: S and T keep their
+        // stored extent and every consumer treats the added rows as zeros
+    }
+
+    // ------------------------------------------------------------- project
+    clock.mark(PH_PROJECT);
+    {
+        std::set<std::pair<bool, Key>> items;  // (is_fill, key), dense first like the reference
+        for (int c : batch) {
+            items.insert({false, mkkey(c, c)});
+            for (auto& kv : L.touch[L.at(c)]) items.insert({!kv.second.dense, kv.second.key});
+        }
+        GemmBuild p1, p2;
+        for (auto& it : items) {
+            View& B = L.block(it.second, !it.first);
+            const int a = key_a(it.second), b = key_b(it.second);
+            const bool ra = in_batch(a), rb = in_batch(b);
+            double* out = L.mem.alloc_n<double>(int64_t(B.rows) * B.cols);
+            if (ra && rb) {
+                double* tmp = scr.alloc_n<double>(int64_t(B.rows) * B.cols);
+                const int sa = B.rows, sb = B.cols;
+                double* qa = Q[std::find(batch.begin(), batch.end(), a) - batch.begin()];
+                double* qb = Q[std::find(batch.begin(), batch.end(), b) - batch.begin()];
+                p1.add1(tmp, B.cols, B.rows, B.cols, GEMM_STORE, contrib(qa, sa, 1, B.p, B.ld, 0, sa));
+                p2.add1(out, B.cols, B.rows, B.cols, GEMM_STORE, contrib(tmp, B.cols, 0, qb, sb, 0, sb));
+            } else if (ra) {
+                const int sa = B.rows;
+                double* qa = Q[std::find(batch.begin(), batch.end(), a) - batch.begin()];
+                p1.add1(out, B.cols, B.rows, B.cols, GEMM_STORE, contrib(qa, sa, 1, B.p, B.ld, 0, sa));
+            } else if (rb) {
+                const int sb = B.cols;
+                double* qb = Q[std::find(batch.begin(), batch.end(), b) - batch.begin()];
+                p1.add1(out, B.cols, B.rows, B.cols, GEMM_STORE, contrib(B.p, B.ld, 0, qb, sb, 0, sb));
+            } else {
+                throw Error(H2F_E_INTERNAL, "assertion: projected block touches no batch member");
+            }
+            B = View{out, B.cols, B.rows, B.cols};
+        }
+        p1.launch();
+        p2.launch();
+    }
+
+    // ------------------------------------------------------------- eliminate
+    clock.mark(PH_PARTIAL_LU);
+    struct Elim {
+        int c, ci, r, kt, np;
+        std::vector<int> ids, widths;
+        std::vector<int64_t> offs;
+        std::vector<Entry> ents;
+        double* G;
+        double* MW;
+        int64_t W;
+    };
+    std::vector<Elim> el;
+    int* status_d = scr.alloc_n<int>(nb);
+    {
+        CopyBuild panels;
+        std::vector<LuTask> lus;
+        std::vector<TrsmTask> trs;
+        H2F_CUDA(cudaMemsetAsync(status_d, 0, sizeof(int) * nb, st));
+        for (int bi = 0; bi < nb; ++bi) {
+            const int c = batch[bi], ci = L.at(c);
+            const int s = int(L.size[ci]), r = L.red[ci], kt = s - r;
+            ClusterFactor& cf = L.factors[ci];
+            cf.cluster = c;
+            cf.s = s;
+            cf.r = r;
+            cf.offset = L.offset[ci];
+            cf.q = Q[bi];
+            if (r == 0) continue;
+            Elim e;
+            e.c = c;
+            e.ci = ci;
+            e.r = r;
+            e.kt = kt;
+            e.ids.push_back(c);
+            e.widths.push_back(kt);
+            for (auto& kv : L.touch[ci]) {
+                e.ids.push_back(kv.first);
+                e.ents.push_back(kv.second);
+                const View& B = L.block(kv.second.key, kv.second.dense);
+                e.widths.push_back(key_a(kv.second.key) == c ? B.cols : B.rows);
+            }
+            e.np = int(e.ids.size());
+            e.offs.assign(e.np + 1, 0);
+            for (int i = 0; i < e.np; ++i) e.offs[i + 1] = e.offs[i] + e.widths[i];
+            e.W = e.offs[e.np];
+            e.G = scr.alloc_n<double>(int64_t(r) * e.W);
+            e.MW = F.store.alloc_n<double>(int64_t(r) * e.W);
+            cf.lu = F.store.alloc_n<double>(int64_t(r) * r);
+            cf.piv = F.store.alloc_n<int32_t>(r);
+            const View& Dcc = L.D.at(mkkey(c, c));
+            // panel 0: d_cc[:r, r:]
+            panels.add(e.G, e.W, r, kt, Dcc.p + r, Dcc.ld, 0, COPY_SET);
+            for (int i = 1; i < e.np; ++i) {
+                const Entry& en = e.ents[i - 1];
+                const View& B = L.block(en.key, en.dense);
+                if (key_a(en.key) == c)
+                    panels.add(e.G + e.offs[i], e.W, r, B.cols, B.p, B.ld, 0, COPY_SET);
+                else
+                    panels.add(e.G + e.offs[i], e.W, r, B.rows, B.p, B.ld, 1, COPY_SET);
+            }
+            LuTask lt{};
+            lt.D = Dcc.p;
+            lt.ldd = Dcc.ld;
+            lt.LU = cf.lu;
+            lt.piv = cf.piv;
+            lt.r = r;
+            lt.cluster = c;
+            lt.status = status_d + bi;
+            lus.push_back(lt);
+            for (int64_t c0 = 0; c0 < e.W; c0 += 128) {
+                TrsmTask tt{};
+                tt.LU = cf.lu;
+                tt.piv = cf.piv;
+                tt.G = e.G;
+                tt.MW = e.MW;
+                tt.ldg = e.W;
+                tt.ldw = e.W;
+                tt.r = r;
+                tt.W = int(e.W);
+                tt.col0 = int(c0);
+                trs.push_back(tt);
+            }
+            // edges (factorization.py:453-456)
+            cf.edges.push_back({c, EDGE_SELF, e.MW, e.W, kt});
+            for (int i = 1; i < e.np; ++i) {
+                const int o = e.ids[i];
+                cf.edges.push_back({o, L.done[L.at(o)] ? EDGE_SKEL : EDGE_FULL, e.MW + e.offs[i], e.W,
+                                    e.widths[i]});
+            }
+            el.push_back(std::move(e));
+        }
+        panels.launch();
+        if (!lus.empty()) launch_lu(upload(lus), int32_t(lus.size()), st);
+        if (!trs.empty()) launch_trsm(upload(trs), int32_t(trs.size()), st);
+    }
+
+    // Schur updates (factorization.py:122-126) fused with the scatter into the
+    // target blocks (factorization.py:476-505)
+    struct Target {
+        double* C;
+        int64_t ldc;
+        int M, N;
+        std::vector<GemmContrib> cs;
+    };
+    struct Cand {
+        Key key;
+        int M, N;
+        GemmContrib g;
+        int64_t base, ntiles;
+    };
+    std::vector<Target> targets;
+    std::unordered_map<double*, int> tindex;
+    std::vector<Cand> cands;
+    auto add_target = [&](double* C, int64_t ldc, int Mr, int Nc, const GemmContrib& g) {
+        if (Mr <= 0 || Nc <= 0) return;
+        auto it = tindex.find(C);
+        if (it == tindex.end()) {
+            tindex[C] = int(targets.size());
+            targets.push_back({C, ldc, Mr, Nc, {g}});
+        } else {
+            Target& t = targets[it->second];
+            if (t.M != Mr || t.N != Nc || t.ldc != ldc)
+                throw Error(H2F_E_INTERNAL, "assertion: Schur target shape mismatch");
+            t.cs.push_back(g);
+        }
+    };
+    for (auto& e : el) {
+        const int c = e.c, r = e.r, kt = e.kt;
+        for (int i = 0; i < e.np; ++i)
+            for (int j = i; j < e.np; ++j) {
+                const GemmContrib g = contrib(e.G + e.offs[i], e.W, 1, e.MW + e.offs[j], e.W, 0, r);
+                const int wi = e.widths[i], wj = e.widths[j];
+                if (i == 0 && j == 0) {
+                    const View& Dcc = L.D.at(mkkey(c, c));
+                    add_target(Dcc.p + int64_t(r) * Dcc.ld + r, Dcc.ld, kt, kt, g);
+                } else if (i == 0) {
+                    const int o = e.ids[j];
+                    const Key key = canon(c, o);
+                    View* B = L.find(key);
+                    if (!B) throw Error(H2F_E_INTERNAL, "assertion: missing block next to eliminated cluster");
+                    if (key_a(key) == c) {
+                        add_target(B->p + int64_t(r) * B->ld, B->ld, kt, B->cols, g);
+                    } else {
+                        const GemmContrib gt = contrib(e.MW + e.offs[j], e.W, 1, e.G + e.offs[0], e.W, 0, r);
+                        add_target(B->p + r, B->ld, B->rows, kt, gt);
+                    }
+                } else {
+                    const Key key = mkkey(e.ids[i], e.ids[j]);
+                    View* B = L.find(key);
+                    if (B) {
+                        add_target(B->p, B->ld, B->rows, B->cols, g);
+                    } else {
+                        Cand cd;
+                        cd.key = key;
+                        cd.M = wi;
+                        cd.N = wj;
+                        cd.g = g;
+                        cd.base = 0;
+                        cd.ntiles = GemmBuild::tiles(wi, wj);
+                        cands.push_back(cd);
+                    }
+                }
+            }
+    }
+    GemmBuild sch;
+    for (auto& t : targets) sch.add(t.C, t.ldc, t.M, t.N, GEMM_ADD, t.cs.data(), t.cs.size());
+    for (auto& cd : cands) cd.base = sch.add1(nullptr, 0, cd.M, cd.N, GEMM_NORM, cd.g);
+    double* norms_d = sch.norm_tiles ? scr.alloc_n<double>(sch.norm_tiles) : nullptr;
+    double* cand_ss_d = cands.empty() ? nullptr : scr.alloc_n<double>(cands.size());
+    sch.launch(norms_d);
+    if (!cands.empty()) {
+        std::vector<int64_t> seg(cands.size() + 1, 0);
+        for (size_t i = 0; i < cands.size(); ++i) seg[i + 1] = cands[i].base + cands[i].ntiles;
+        for (size_t i = 0; i < cands.size(); ++i)
+            if (cands[i].base != seg[i]) throw Error(H2F_E_INTERNAL, "assertion: norm segments");
+        launch_sumsq_reduce(norms_d, upload(seg), int32_t(cands.size()), cand_ss_d, st);
+    }
+    // one sync: LU status + candidate norms
+    const size_t nbytes_read = sizeof(int) * nb + sizeof(double) * cands.size() + 8;
+    char* hbuf = static_cast<char*>(X.pinned_buf(nbytes_read + 64));
+    int* status_h = reinterpret_cast<int*>(hbuf);
+    double* ss_h = reinterpret_cast<double*>(hbuf + ((sizeof(int) * nb + 15) & ~size_t(15)));
+    H2F_CUDA(cudaMemcpyAsync(status_h, status_d, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
+    if (!cands.empty())
+        H2F_CUDA(cudaMemcpyAsync(ss_h, cand_ss_d, sizeof(double) * cands.size(), cudaMemcpyDeviceToHost, st));
+    X.sync();
+    for (int bi = 0; bi < nb; ++bi)
+        if (status_h[bi]) {
+            Error err(H2F_E_SINGULAR, "cluster " + std::to_string(batch[bi]) + " at level " +
+                                          std::to_string(L.level) + ": vanishing pivot in redundant block");
+            err.cluster = batch[bi];
+            err.level = L.level;
+            throw err;
+        }
+    // sequential fill-creation semantics (factorization.py:461-466, 492-505):
+    // the first candidate whose own norm exceeds the drop tolerance creates
+    // the block, earlier ones are dropped, later ones are added unconditionally
+    {
+        GemmBuild create;
+        std::unordered_map<Key, int> made;
+        std::vector<Target> news;
+        for (size_t i = 0; i < cands.size(); ++i) {
+            const Cand& cd = cands[i];
+            auto it = made.find(cd.key);
+            if (it != made.end()) {
+                news[it->second].cs.push_back(cd.g);
+                continue;
+            }
+            if (std::sqrt(ss_h[i]) > drop) {
+                double* blk = L.mem.alloc_n<double>(int64_t(cd.M) * cd.N);
+                L.F[cd.key] = View{blk, cd.N, cd.M, cd.N};
+                L.link(cd.key, false);
+                made[cd.key] = int(news.size());
+                news.push_back({blk, cd.N, cd.M, cd.N, {cd.g}});
+            }
+        }
+        for (auto& t : news) create.add(t.C, t.ldc, t.M, t.N, GEMM_STORE, t.cs.data(), t.cs.size());
+        create.launch();
+    }
+    // slice to skeletons (views only) and mark done (factorization.py:513-523)
+    for (int bi = 0; bi < nb; ++bi) {
+        const int c = batch[bi], ci = L.at(c);
+        const int r = L.red[ci];
+        if (r) {
+            View& Dcc = L.D.at(mkkey(c, c));
+            Dcc.p += int64_t(r) * Dcc.ld + r;
+            Dcc.rows -= r;
+            Dcc.cols -= r;
+            for (auto& kv : L.touch[ci]) {
+                View& B = L.block(kv.second.key, kv.second.dense);
+                if (key_a(kv.second.key) == c) {
+                    B.p += int64_t(r) * B.ld;
+                    B.rows -= r;
+                } else {
+                    B.p += r;
+                    B.cols -= r;
+                }
+            }
+            L.live[ci] -= r;
+        }
+        L.done[ci] = 1;
+    }
+}
+
+std::unique_ptr<Lvl> Factorizer::transition(Lvl& L) {
+    // factorization.py:535-588
+    const int nl = L.level - 1;
+    auto N = std::make_unique<Lvl>();
+    N->level = nl;
+    N->init_common(M.levels[nl]);
+    const size_t n = N->clusters.size();
+    N->offset.resize(n);
+    N->size.resize(n);
+    CopyBuild zero, set, add;
+    int64_t pos = 0;
+    auto live_of = [&](int c) { return L.live[L.at(c)]; };
+    for (size_t i = 0; i < n; ++i) {
+        const int p = N->clusters[i];
+        const int a = int(M.left[p]), b = int(M.right[p]);
+        const int la = live_of(a), lb = live_of(b);
+        N->size[i] = la + lb;
+        N->offset[i] = pos;
+        pos += N->size[i];
+        const int kp = int(M.rank[p]);
+        double* bas = N->mem.alloc_n<double>(int64_t(N->size[i]) * std::max(kp, 1));
+        zero.zero(bas, kp, int(N->size[i]), kp);
+        const TransferW& ta = L.T[L.at(a)];
+        const TransferW& tb = L.T[L.at(b)];
+        if (ta.has) set.add(bas, kp, ta.rows, kp, ta.p, ta.ld, 0, COPY_SET);
+        if (tb.has) set.add(bas + int64_t(la) * kp, kp, tb.rows, kp, tb.p, tb.ld, 0, COPY_SET);
+        N->basis[i] = View{bas, kp, int(N->size[i]), kp};
+        N->k[i] = kp;
+    }
+    auto nsize = [&](int c) { return int(N->size[N->at(c)]); };
+    for (auto& pr : dense_pairs(nl)) {
+        const int s = pr.first, t = pr.second;
+        const int rs = nsize(s), cs = nsize(t);
+        double* blk = N->mem.alloc_n<double>(int64_t(rs) * cs);
+        zero.zero(blk, cs, rs, cs);
+        N->D[mkkey(s, t)] = View{blk, cs, rs, cs};
+        int ro = 0;
+        for (int64_t ca : {M.left[s], M.right[s]}) {
+            int co = 0;
+            for (int64_t cb : {M.left[t], M.right[t]}) {
+                const Key key = canon(int(ca), int(cb));
+                const int tr = ca > cb ? 1 : 0;
+                double* dst = blk + int64_t(ro) * cs + co;
+                auto dit = L.D.find(key);
+                if (dit != L.D.end()) {
+                    const View& V = dit->second;
+                    set.add(dst, cs, live_of(int(ca)), live_of(int(cb)), V.p, V.ld, tr, COPY_SET);
+                } else {
+                    auto sit = L.S.find(key);
+                    if (sit == L.S.end()) throw Error(H2F_E_INTERNAL, "assertion: child pair neither dense nor coupled");
+                    const CouplingW& S = sit->second;
+                    set.add(dst, cs, tr ? S.cols : S.rows, tr ? S.rows : S.cols, S.p, S.ld, tr, COPY_SET);
+                    auto fit = L.F.find(key);
+                    if (fit != L.F.end())
+                        add.add(dst, cs, live_of(int(ca)), live_of(int(cb)), fit->second.p, fit->second.ld, tr,
+                                COPY_ADD);
+                }
+                co += live_of(int(cb));
+            }
+            ro += live_of(int(ca));
+        }
+    }
+    for (auto& kv : L.F) {
+        const int a = key_a(kv.first), b = key_b(kv.first);
+        if (M.is_adm(L.level, a, b)) continue;
+        const int p = int(M.parent[a]), q = int(M.parent[b]);
+        if (!(p < q) || N->D.count(mkkey(p, q)))
+            throw Error(H2F_E_INTERNAL, "assertion: fill block sweeps onto a dense parent pair");
+        auto it = N->F.find(mkkey(p, q));
+        if (it == N->F.end()) {
+            const int rs = nsize(p), cs = nsize(q);
+            double* blk = N->mem.alloc_n<double>(int64_t(rs) * cs);
+            zero.zero(blk, cs, rs, cs);
+            it = N->F.emplace(mkkey(p, q), View{blk, cs, rs, cs}).first;
+        }
+        const int ro = (a == M.left[p]) ? 0 : live_of(int(M.left[p]));
+        const int co = (b == M.left[q]) ? 0 : live_of(int(M.left[q]));
+        View& dst = it->second;
+        add.add(dst.p + int64_t(ro) * dst.ld + co, dst.ld, live_of(a), live_of(b), kv.second.p, kv.second.ld, 0,
+                COPY_ADD);
+    }
+    zero.launch();
+    set.launch();
+    add.launch();
+    N->build_touch();
+    return N;
+}
+
+void Factorizer::finish_top(Lvl& L) {
+    // factorization.py:591-615
+    std::unordered_map<int, int64_t> offs;
+    int64_t n = 0;
+    for (size_t i = 0; i < L.clusters.size(); ++i) {
+        offs[L.clusters[i]] = n;
+        n += L.live[i];
+    }
+    for (auto& kv : L.F)
+        if (!M.is_adm(L.level, key_a(kv.first), key_b(kv.first)))
+            throw Error(H2F_E_INTERNAL, "assertion: fill above the shallowest compressed level");
+    F.top_size = n;
+    F.top_lu = F.store.alloc_n<double>(n * n);
+    F.top_piv = F.store.alloc_n<int32_t>(n);
+    CopyBuild zero, set, add;
+    double* A = F.top_lu;
+    zero.zero(A, n, int(n), int(n));
+    auto live_of = [&](int c) { return L.live[L.at(c)]; };
+    for (auto& pr : dense_pairs(L.level)) {
+        const int s = pr.first, t = pr.second;
+        const View& V = L.D.at(mkkey(s, t));
+        set.add(A + offs[s] * n + offs[t], n, V.rows, V.cols, V.p, V.ld, 0, COPY_SET);
+        if (s != t) set.add(A + offs[t] * n + offs[s], n, V.cols, V.rows, V.p, V.ld, 1, COPY_SET);
+    }
+    for (auto& pr : M.adm[L.level]) {
+        const int s = pr.first, t = pr.second;
+        const Key key = mkkey(s, t);
+        const CouplingW& S = L.S.at(key);
+        set.add(A + offs[s] * n + offs[t], n, S.rows, S.cols, S.p, S.ld, 0, COPY_SET);
+        if (s != t) set.add(A + offs[t] * n + offs[s], n, S.cols, S.rows, S.p, S.ld, 1, COPY_SET);
+        auto fit = L.F.find(key);
+        if (fit != L.F.end()) {
+            const View& V = fit->second;
+            add.add(A + offs[s] * n + offs[t], n, live_of(s), live_of(t), V.p, V.ld, 0, COPY_ADD);
+            if (s != t) add.add(A + offs[t] * n + offs[s], n, live_of(t), live_of(s), V.p, V.ld, 1, COPY_ADD);
+        }
+    }
+    zero.launch();
+    set.launch();
+    add.launch();
+}
+
+void Factorizer::dense_only_top() {
+    // factorization.py:274-285
+    const int64_t n = M.n;
+    F.top_size = n;
+    F.top_lu = F.store.alloc_n<double>(n * n);
+    F.top_piv = F.store.alloc_n<int32_t>(n);
+    CopyBuild zero, set;
+    zero.zero(F.top_lu, n, int(n), int(n));
+    for (int l = 0; l <= M.depth; ++l)
+        for (auto& pr : M.dense[l]) {
+            const int s = pr.first, t = pr.second;
+            const double* D = M.vals + M.dense_off.at(mkkey(s, t));
+            const int rs = int(M.rows(s)), cs = int(M.rows(t));
+            set.add(F.top_lu + M.begin[s] * n + M.begin[t], n, rs, cs, D, cs, 0, COPY_SET);
+            if (s != t) set.add(F.top_lu + M.begin[t] * n + M.begin[s], n, cs, rs, D, cs, 1, COPY_SET);
+        }
+    zero.launch();
+    set.launch();
+}
+
+void Factorizer::top_factor(double* A, int64_t n) {
+    // factorization.py:259-263: pivoted LU + vanishing-pivot test
+    Context& X = ctx();
+    cudaStream_t st = X.stream;
+    if (n == 0) return;
+    double* red = scratch[0].alloc_n<double>(2);
+    launch_absmax(A, n, int(n), int(n), red, st);
+    const int nb = 64;
+    for (int64_t k0 = 0; k0 < n; k0 += nb) {
+        const int w = int(std::min<int64_t>(nb, n - k0));
+        launch_panel_lu(A, n, int(n), int(k0), w, F.top_piv, st);
+        launch_row_swaps(A, n, int(n), int(k0), w, F.top_piv, int(k0), int(k0 + w), st);
+        const int64_t rest = n - k0 - w;
+        if (rest > 0) {
+            launch_trsm_unit_lower_rows(A, n, int(k0), w, int(k0 + w), int(rest), st);
+            GemmBuild g;
+            g.add1(A + (k0 + w) * n + (k0 + w), n, int(rest), int(rest), GEMM_ADD,
+                   contrib(A + (k0 + w) * n + k0, n, 0, A + k0 * n + (k0 + w), n, 0, w, -1.0));
+            g.launch();
+        }
+    }
+    launch_diag_absmin(A, n, int(n), red + 1, st);
+    double* h = static_cast<double*>(X.pinned_buf(16));
+    H2F_CUDA(cudaMemcpyAsync(h, red, 16, cudaMemcpyDeviceToHost, st));
+    X.sync();
+    if (h[1] <= PIVOT_RTOL * std::max(h[0], 1e-300))
+        throw Error(H2F_E_SINGULAR, "singular block at the final dense solve");
+}
+
+void Factorizer::run(double norm_estimate, const double* v0) {
+    mark_node.assign(M.nnodes, 0);
+    clock.mark(PH_NORM);
+    if (norm_estimate < 0) {
+        if (!v0) throw Error(H2F_E_ARG, "norm estimate requested without a start vector");
+        norm_estimate = norm2_estimate(M, v0, 30);
+    }
+    F.norm_estimate = norm_estimate;
+    eps_fill = F.eps_lu * norm_estimate;
+    F.eps_fill = eps_fill;
+    drop = FILL_DROP_FACTOR * eps_fill;
+    F.top_level = M.top;
+    if (M.top < 0) {
+        clock.mark(PH_TOP);
+        dense_only_top();
+    } else {
+        std::unique_ptr<Lvl> L;
+        for (int level = M.depth; level >= M.top; --level) {
+            level_marks.push_back(clock.size());
+            clock.mark(PH_EXTRACT);
+            if (!L) L = leaf_level(level);
+            for (size_t i = 0; i < L->clusters.size(); ++i) L->live[i] = int(L->size[i]);
+            attach_couplings(*L);
+            clock.mark(PH_COLOR);
+            // greedy colouring of the D+F graph in ascending id order
+            // (factorization.py:330-337, structure.py:137-167)
+            const size_t nc = L->clusters.size();
+            std::vector<int> color(nc, -1);
+            int ncolors = 0, degree = 0;
+            for (size_t i = 0; i < nc; ++i) {
+                std::vector<char> used;
+                degree = std::max(degree, int(L->touch[i].size()));
+                for (auto& kv : L->touch[i]) {
+                    const int j = L->at(kv.first);
+                    if (color[j] >= 0) {
+                        if (size_t(color[j]) >= used.size()) used.resize(color[j] + 1, 0);
+                        used[color[j]] = 1;
+                    }
+                }
+                int cc = 0;
+                while (size_t(cc) < used.size() && used[cc]) ++cc;
+                color[i] = cc;
+                ncolors = std::max(ncolors, cc + 1);
+            }
+            std::vector<std::vector<int>> groups(ncolors);
+            for (size_t i = 0; i < nc; ++i) groups[color[i]].push_back(L->clusters[i]);
+            for (auto& grp : groups) {
+                std::vector<int> remaining = grp;
+                while (!remaining.empty()) {
+                    // greedy independent set in the live graph (factorization.py:353-362)
+                    ++stamp;
+                    std::vector<int> batch, rest;
+                    for (int c : remaining) {
+                        bool free_ = true;
+                        for (auto& kv : L->touch[L->at(c)])
+                            if (mark_node[kv.first] == stamp) { free_ = false; break; }
+                        if (free_) {
+                            batch.push_back(c);
+                            mark_node[c] = stamp;
+                        } else {
+                            rest.push_back(c);
+                        }
+                    }
+                    remaining.swap(rest);
+                    L->batches.push_back(batch);
+                    process_batch(*L, batch);
+                    clock.mark(PH_COLOR);
+                }
+            }
+            // level record
+            LevelRecord rec;
+            rec.level = level;
+            rec.clusters = L->clusters;
+            rec.offset = L->offset;
+            rec.size = L->size;
+            rec.batches = L->batches;
+            rec.csp = sparsity_constant(M, level);
+            rec.ncolors = ncolors;
+            rec.graph_degree = degree;
+            int mr = 0;
+            for (size_t i = 0; i < nc; ++i) {
+                mr = std::max(mr, L->live[i]);
+                rec.pos[L->clusters[i]] = int(i);
+                for (int64_t x = L->offset[i] + L->red[i]; x < L->offset[i] + L->size[i]; ++x) rec.up_index.push_back(x);
+            }
+            rec.max_rank = mr;
+            rec.factors = std::move(L->factors);
+            clock.mark(PH_TRANSITION);
+            if (level > M.top) {
+                auto N = transition(*L);
+                ctx().sync();  // the old level's storage is released next
+                L = std::move(N);
+            } else {
+                finish_top(*L);
+                ctx().sync();
+                L.reset();
+            }
+            F.recs.push_back(std::move(rec));
+        }
+    }
+    clock.mark(PH_TOP);
+    top_factor(F.top_lu, F.top_size);
+    clock.mark(-1);
+    ctx().sync();
+    clock.accumulate(F.phase);
+    for (size_t i = 0; i < level_marks.size(); ++i) {
+        const size_t j = (i + 1 < level_marks.size()) ? level_marks[i + 1] : clock.size() - 2;
+        F.recs[i].time_s = clock.between(level_marks[i], j);
+    }
+    // nbytes (factorization.py:181-190)
+    int64_t nb = F.top_size * F.top_size * 8 + F.top_size * 4;
+    for (auto& rec : F.recs) {
+        nb += int64_t(rec.up_index.size()) * 8;
+        for (auto& cf : rec.factors) {
+            nb += int64_t(cf.s) * cf.s * 8;
+            if (cf.r) nb += int64_t(cf.r) * cf.r * 8 + int64_t(cf.r) * 4;
+            for (auto& e : cf.edges) nb += int64_t(cf.r) * e.w * 8;
+        }
+    }
+    F.nbytes = nb;
+}
+
+}  // namespace
+
+Factorization* factorize(H2Mat& m, double eps_lu, double norm_estimate, const double* v0_host) {
+    auto f = std::make_unique<Factorization>();
+    f->mat = &m;
+    f->n = m.n;
+    f->eps_lu = eps_lu;
+    Factorizer fz(m, *f);
+    fz.run(norm_estimate, v0_host);
+    return f.release();
+}
+
+}  // namespace h2f

@@ -1,0 +1,77 @@
+// Factor containers (factorization.py:130-193) and the factorization /
+// substitution entry points of the runtime.
+#pragma once
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "h2mat.h"
+
+namespace h2f {
+
+enum EdgeKind : int32_t { EDGE_SELF = 0, EDGE_FULL = 1, EDGE_SKEL = 2 };
+
+struct EdgeRec {        // (other, kind, mat) of ClusterFactor.edges, mat = r x w view
+    int other;
+    int kind;
+    double* mat;
+    int64_t ld;
+    int w;
+};
+
+struct ClusterFactor {  // factorization.py:130-147
+    int cluster = -1;
+    int s = 0, r = 0;
+    int64_t offset = 0;
+    double* q = nullptr;       // s x s
+    double* lu = nullptr;      // r x r (row-major)
+    int32_t* piv = nullptr;    // r
+    std::vector<EdgeRec> edges;
+};
+
+struct LevelRecord {    // factorization.py:150-164
+    int level = 0;
+    std::vector<int> clusters;
+    std::vector<int64_t> offset, size;
+    std::vector<std::vector<int>> batches;
+    std::vector<int64_t> up_index;
+    int csp = 0, ncolors = 0, graph_degree = 0, max_rank = 0;
+    double time_s = 0.0;
+    std::vector<ClusterFactor> factors;        // parallel to clusters
+    std::unordered_map<int, int> pos;          // cluster -> index
+    int64_t total() const {
+        int64_t t = 0;
+        for (auto s : size) t += s;
+        return t;
+    }
+};
+
+enum Phase : int { PH_NORM = 0, PH_EXTRACT, PH_COLOR, PH_AUGMENT, PH_PROJECT, PH_PARTIAL_LU,
+                   PH_TRANSITION, PH_TOP, PH_COUNT };
+
+struct SolvePlan;
+
+struct Factorization {  // factorization.py:167-193
+    H2Mat* mat = nullptr;
+    int64_t n = 0;
+    int top_level = -1;
+    std::vector<LevelRecord> recs;
+    double* top_lu = nullptr;
+    int32_t* top_piv = nullptr;
+    int64_t top_size = 0;
+    double eps_lu = 0, eps_fill = 0, norm_estimate = 0;
+    double phase[PH_COUNT] = {0};
+    int64_t nbytes = 0;
+    Region store{size_t(256) << 20};
+    std::map<int, std::shared_ptr<SolvePlan>> plans;  // per nrhs
+    Region work{size_t(16) << 20};
+    ~Factorization();
+};
+
+// throws Error(H2F_E_SINGULAR) with cluster/level set on a vanishing pivot
+Factorization* factorize(H2Mat& m, double eps_lu, double norm_estimate, const double* v0_host);
+
+void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs);
+void refined_solve_device(H2Mat& m, Factorization& f, const double* b_dev, double* x_dev, int steps);
+
+}  // namespace h2f

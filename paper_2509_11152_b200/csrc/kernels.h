@@ -1,0 +1,202 @@
+// Device task descriptors and kernel launchers (sm_100a).
+//
+// Every batched kernel consumes a flat task list built on the host by the
+// scheduler (factor.cpp / solve.cpp / matvec.cpp) and uploaded once per
+// launch; variable-size work is mapped to CTAs through a tile prefix sum so
+// one launch covers every cluster of a batch (the B200 replacement of the
+// reference's WorkerPool.map, parallel.py:16-37).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace h2f {
+
+// ---- batched FP64 tile GEMM (DMMA m8n8k4) --------------------------------
+// C[M x N] (=|+=) sum_c alpha_c * op(A_c) * op(B_c); op(A) is M x K, op(B) K x N.
+// mode NORM writes, per 64x64 tile, the sum of squares of the single
+// contribution's tile to norms[norm_base + tile] instead of touching C.
+enum GemmMode : int32_t { GEMM_STORE = 0, GEMM_ADD = 1, GEMM_NORM = 2 };
+
+struct GemmTask {
+    double* C;
+    int64_t ldc;
+    int32_t M, N;
+    int32_t mode;
+    int32_t tiles_n;
+    int64_t contrib_begin, contrib_end;
+    int64_t norm_base;
+};
+
+struct GemmContrib {
+    const double* A;
+    const double* B;
+    int64_t lda, ldb;
+    int32_t K;
+    int32_t transA;  // 0: A stored M x K; 1: A stored K x M
+    int32_t transB;  // 0: B stored K x N; 1: B stored N x K
+    int32_t pad_;
+    double alpha;
+};
+
+constexpr int GEMM_TILE = 64;
+
+// ---- batched copy / add / zero with optional transpose --------------------
+enum CopyMode : int32_t { COPY_SET = 0, COPY_ADD = 1, COPY_ZERO = 2 };
+
+struct CopyTask {
+    const double* src;
+    double* dst;
+    int64_t lds, ldd;
+    int32_t rows, cols;   // of dst region
+    int32_t trans;        // dst(i,j) = src(j,i)
+    int32_t mode;
+    double alpha;
+};
+
+constexpr int COPY_TILE = 32;
+
+// ---- per-cluster dense kernels ------------------------------------------------
+struct QrTask {          // R of the reduced QR of Y^T, Y is s x wf (row-major, ld)
+    double* Y;           // overwritten
+    double* R;           // min(s,wf) x s, row-major, ld = s
+    int64_t ldy;
+    int32_t s, wf;
+};
+
+struct SvdTask {         // one-sided Jacobi on the rows of R (m x s), then
+    double* R;           // writes b_aug^T = [V^T ; vbar^T] ((k+kept) x s) to BT
+    const double* V;     // s x k basis, row-major ld = ldv
+    double* BT;
+    int64_t ldv;
+    int32_t m, s, k;
+    int32_t skip;        // 1: no fill row -> kept = 0 without touching R
+    int32_t* kept_out;   // device int
+};
+
+struct ComplementTask {  // Q~ = [complement | b_aug] from BT (kt x s)
+    const double* BT;    // kt x s, row-major ld = s
+    double* W;           // kt x s workspace (Householder vectors)
+    double* Q;           // s x s row-major (factor storage)
+    double* scratch;     // 32 * s per CTA warp workspace
+    const int32_t* kept; // device kept count; kt = k + *kept
+    int32_t s, k;
+};
+
+struct LuTask {          // partial-pivot LU of the r x r view of D_cc
+    const double* D;
+    int64_t ldd;
+    double* LU;          // r x r row-major
+    int32_t* piv;        // r
+    int32_t r;
+    int32_t cluster;     // for the status word
+    int32_t* status;     // device: cluster index that failed (first), else -1
+};
+
+struct TrsmTask {        // MW = -(U^-1 L^-1 P G) column block
+    const double* LU;
+    const int32_t* piv;
+    const double* G;     // r x W row-major, ld
+    double* MW;          // r x W row-major, ld
+    int64_t ldg, ldw;
+    int32_t r, W;
+    int32_t col0;        // first column of this CTA chunk
+    int32_t pad_;
+};
+
+// ---- solve -----------------------------------------------------------------------
+struct SolveCluster {
+    const double* q;     // s x s
+    const double* lu;    // r x r
+    const int32_t* piv;
+    int64_t off;         // offset in the level vector
+    int32_t s, r;
+    int64_t edge_begin, edge_end;
+    int64_t woff;        // work slot (s * nrhs doubles) when it exceeds shared memory
+};
+
+struct SolveEdge {
+    const double* mat;   // r x w, row-major, ld
+    int64_t ld;
+    int64_t lo;          // target span start in the level vector
+    int64_t soff;        // scratch offset (forward products), in rows
+    int32_t w;
+    int32_t pad_;
+};
+
+struct ScatterGroup {    // y[lo : lo+w] += sum of scratch rows listed in [begin,end)
+    int64_t lo;
+    int32_t w;
+    int32_t pad_;
+    int64_t begin, end;  // into a list of scratch offsets
+};
+
+// ---- GEMV tasks (matvec sweeps, small solves) -------------------------------------
+struct GemvTask {
+    double* y;
+    int32_t rows;
+    int32_t mode;        // COPY_SET / COPY_ADD
+    int64_t contrib_begin, contrib_end;
+};
+
+struct GemvContrib {
+    const double* A;
+    const double* x;
+    int64_t lda;
+    int32_t cols;
+    int32_t trans;       // 0: y += A x (A rows x cols); 1: y += A^T x (A cols x rows)
+    double alpha;
+};
+
+// ---- launchers (defined in the .cu files) ----------------------------------------
+void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
+                       const int64_t* d_tile_start, int32_t ntasks, int64_t ntiles,
+                       double* d_norms, cudaStream_t st);
+void launch_copy_tasks(const CopyTask* d_tasks, const int64_t* d_tile_start, int32_t ntasks,
+                       int64_t ntiles, cudaStream_t st);
+void launch_qr_r(const QrTask* d_tasks, int32_t ntasks, cudaStream_t st);
+void launch_jacobi(const SvdTask* d_tasks, int32_t ntasks, double thresh, cudaStream_t st);
+void launch_complement(const ComplementTask* d_tasks, int32_t ntasks, cudaStream_t st);
+void launch_lu(const LuTask* d_tasks, int32_t ntasks, cudaStream_t st);
+void launch_trsm(const TrsmTask* d_tasks, int32_t ntasks, cudaStream_t st);
+void launch_sumsq_reduce(const double* d_parts, const int64_t* d_seg, int32_t nseg,
+                         double* d_out, cudaStream_t st);
+
+// top (dense) LU pieces
+void launch_panel_lu(double* A, int64_t lda, int32_t n, int32_t k0, int32_t nb, int32_t* piv,
+                     cudaStream_t st);
+void launch_row_swaps(double* A, int64_t lda, int32_t ncols_total, int32_t k0, int32_t nb,
+                      const int32_t* piv, int32_t skip_c0, int32_t skip_c1, cudaStream_t st);
+void launch_trsm_unit_lower_rows(const double* A, int64_t lda, int32_t k0, int32_t nb,
+                                 int32_t c0, int32_t ncols, cudaStream_t st);
+void launch_absmax(const double* A, int64_t lda, int32_t rows, int32_t cols, double* out,
+                   cudaStream_t st);
+void launch_diag_absmin(const double* A, int64_t lda, int32_t n, double* out, cudaStream_t st);
+
+// solve
+void launch_fwd_clusters(const SolveCluster* d_cl, int32_t ncl, const SolveEdge* d_edges,
+                         double* y, double* scratch, int32_t nrhs, double* work,
+                         cudaStream_t st);
+void launch_fwd_scatter(const ScatterGroup* d_groups, int32_t ngroups, const int64_t* d_list,
+                        const double* scratch, double* y, int32_t nrhs, cudaStream_t st);
+void launch_bwd_clusters(const SolveCluster* d_cl, int32_t ncl, const SolveEdge* d_edges,
+                         double* y, int32_t nrhs, double* work, cudaStream_t st);
+void launch_gather_rows(const double* src, const int64_t* idx, int64_t n, int32_t nrhs,
+                        double* dst, cudaStream_t st);
+void launch_scatter_rows(const double* src, const int64_t* idx, int64_t n, int32_t nrhs,
+                         double* dst, cudaStream_t st);
+void launch_top_solve(const double* lu, const int32_t* piv, int32_t n, double* x, int32_t nrhs,
+                      double* work, cudaStream_t st);
+
+// matvec / vectors
+void launch_gemv_tasks(const GemvTask* d_tasks, int32_t ntasks, const GemvContrib* d_contribs,
+                       int32_t nrhs, cudaStream_t st);
+void launch_norm2(const double* x, int64_t n, double* partial, double* out, cudaStream_t st);
+void launch_scale_by_inv(double* x, const double* w, int64_t n, const double* s,
+                         cudaStream_t st);
+void launch_axpby(double* y, const double* a, double alpha, const double* b, double beta,
+                  int64_t n, cudaStream_t st);
+
+int64_t kernel_launch_count();
+void count_launch();
+
+}  // namespace h2f

@@ -1,0 +1,200 @@
+// Substitution against the factor (Alg. 3; solve.py:29-77).
+//
+// A SolvePlan is built once per (factor, nrhs): per batch, the cluster and
+// edge descriptors, and the forward-scatter groups (products grouped by target
+// span in reference order).  A solve is then a fixed launch sequence:
+// forward over records (fwd_clusters + fwd_scatter per batch, then the
+// up_index gather), the dense top solve, and the backward sweep in reverse
+// (up_index scatter, bwd_clusters per batch).
+#include <algorithm>
+#include <map>
+
+#include "factor.h"
+
+namespace h2f {
+
+struct SolvePlan {
+    struct Batch {
+        SolveCluster* cl = nullptr;
+        int32_t ncl = 0;
+        SolveEdge* edges = nullptr;
+        ScatterGroup* groups = nullptr;
+        int32_t ngroups = 0;
+        int64_t* list = nullptr;
+    };
+    struct Level {
+        int64_t total = 0;
+        int64_t* up = nullptr;
+        int64_t up_n = 0;
+        std::vector<Batch> batches;
+    };
+    int nrhs = 1;
+    std::vector<Level> levels;
+    std::vector<double*> yv;   // per record level vectors
+    double* ytop = nullptr;
+    double* scratch = nullptr;
+    double* work = nullptr;
+    Region mem{size_t(16) << 20};
+};
+
+Factorization::~Factorization() = default;
+
+namespace {
+
+template <class T> T* to_dev(Region& r, const std::vector<T>& v) {
+    T* d = r.alloc_n<T>(std::max<size_t>(v.size(), 1));
+    if (!v.empty())
+        H2F_CUDA(cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, ctx().stream));
+    return d;
+}
+
+SolvePlan& get_plan(Factorization& f, int nrhs) {
+    auto it = f.plans.find(nrhs);
+    if (it != f.plans.end()) return *it->second;
+    auto plan = std::make_shared<SolvePlan>();
+    SolvePlan& P = *plan;
+    P.nrhs = nrhs;
+    int64_t scratch_rows = 0, work_max = 0;
+    for (auto& rec : f.recs) {
+        SolvePlan::Level L;
+        L.total = rec.total();
+        L.up_n = int64_t(rec.up_index.size());
+        L.up = to_dev(P.mem, rec.up_index);
+        for (auto& batch : rec.batches) {
+            std::vector<SolveCluster> cls;
+            std::vector<SolveEdge> edges;
+            // target lo -> (w, ordered scratch rows)
+            std::map<int64_t, std::pair<int, std::vector<int64_t>>> groups;
+            std::vector<int64_t> group_order;
+            int64_t soff = 0, woff = 0;
+            for (int c : batch) {
+                const ClusterFactor& cf = rec.factors[rec.pos.at(c)];
+                SolveCluster sc{};
+                sc.q = cf.q;
+                sc.lu = cf.lu;
+                sc.piv = cf.piv;
+                sc.off = cf.offset;
+                sc.s = cf.s;
+                sc.r = cf.r;
+                sc.edge_begin = int64_t(edges.size());
+                sc.woff = woff;
+                woff += int64_t(cf.s) * nrhs;
+                for (auto& e : cf.edges) {
+                    SolveEdge se{};
+                    se.mat = e.mat;
+                    se.ld = e.ld;
+                    se.w = e.w;
+                    // target span (solve.py:80-87)
+                    if (e.kind == EDGE_SELF) {
+                        se.lo = cf.offset + cf.r;
+                    } else {
+                        const ClusterFactor& of = rec.factors[rec.pos.at(e.other)];
+                        se.lo = of.offset + (e.kind == EDGE_SKEL ? of.r : 0);
+                    }
+                    se.soff = soff;
+                    auto g = groups.find(se.lo);
+                    if (g == groups.end()) {
+                        groups[se.lo] = {e.w, {soff}};
+                        group_order.push_back(se.lo);
+                    } else {
+                        if (g->second.first != e.w) throw Error(H2F_E_INTERNAL, "assertion: scatter span mismatch");
+                        g->second.second.push_back(soff);
+                    }
+                    soff += e.w;
+                    edges.push_back(se);
+                }
+                sc.edge_end = int64_t(edges.size());
+                cls.push_back(sc);
+            }
+            std::vector<ScatterGroup> gs;
+            std::vector<int64_t> list;
+            for (int64_t lo : group_order) {
+                auto& g = groups[lo];
+                ScatterGroup sg{};
+                sg.lo = lo;
+                sg.w = g.first;
+                sg.begin = int64_t(list.size());
+                list.insert(list.end(), g.second.begin(), g.second.end());
+                sg.end = int64_t(list.size());
+                gs.push_back(sg);
+            }
+            SolvePlan::Batch B;
+            B.ncl = int32_t(cls.size());
+            B.cl = to_dev(P.mem, cls);
+            B.edges = to_dev(P.mem, edges);
+            B.ngroups = int32_t(gs.size());
+            B.groups = to_dev(P.mem, gs);
+            B.list = to_dev(P.mem, list);
+            L.batches.push_back(B);
+            scratch_rows = std::max(scratch_rows, soff);
+            work_max = std::max(work_max, woff);
+        }
+        P.levels.push_back(std::move(L));
+    }
+    for (auto& L : P.levels) P.yv.push_back(P.mem.alloc_n<double>(L.total * nrhs));
+    P.ytop = P.mem.alloc_n<double>(std::max<int64_t>(f.top_size, 1) * nrhs);
+    P.scratch = P.mem.alloc_n<double>(std::max<int64_t>(scratch_rows, 1) * nrhs);
+    P.work = P.mem.alloc_n<double>(std::max<int64_t>(work_max, 1));
+    ctx().sync();
+    auto& ref = *plan;
+    f.plans[nrhs] = std::move(plan);
+    return ref;
+}
+
+}  // namespace
+
+void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs) {
+    SolvePlan& P = get_plan(f, nrhs);
+    cudaStream_t st = ctx().stream;
+    const size_t nb = sizeof(double) * f.n * nrhs;
+    if (f.recs.empty()) {
+        // solve.py:46-47
+        H2F_CUDA(cudaMemcpyAsync(P.ytop, b_dev, nb, cudaMemcpyDeviceToDevice, st));
+        launch_top_solve(f.top_lu, f.top_piv, int(f.top_size), P.ytop, nrhs, P.work, st);
+        H2F_CUDA(cudaMemcpyAsync(x_dev, P.ytop, nb, cudaMemcpyDeviceToDevice, st));
+        return;
+    }
+    const size_t R = P.levels.size();
+    H2F_CUDA(cudaMemcpyAsync(P.yv[0], b_dev, nb, cudaMemcpyDeviceToDevice, st));
+    for (size_t li = 0; li < R; ++li) {
+        auto& L = P.levels[li];
+        for (auto& B : L.batches) {
+            launch_fwd_clusters(B.cl, B.ncl, B.edges, P.yv[li], P.scratch, nrhs, P.work, st);
+            launch_fwd_scatter(B.groups, B.ngroups, B.list, P.scratch, P.yv[li], nrhs, st);
+        }
+        double* next = (li + 1 < R) ? P.yv[li + 1] : P.ytop;
+        launch_gather_rows(P.yv[li], L.up, L.up_n, nrhs, next, st);
+    }
+    launch_top_solve(f.top_lu, f.top_piv, int(f.top_size), P.ytop, nrhs, P.work, st);
+    for (size_t li = R; li-- > 0;) {
+        auto& L = P.levels[li];
+        const double* src = (li + 1 < R) ? P.yv[li + 1] : P.ytop;
+        launch_scatter_rows(src, L.up, L.up_n, nrhs, P.yv[li], st);
+        for (size_t bi = L.batches.size(); bi-- > 0;) {
+            auto& B = L.batches[bi];
+            launch_bwd_clusters(B.cl, B.ncl, B.edges, P.yv[li], nrhs, P.work, st);
+        }
+    }
+    H2F_CUDA(cudaMemcpyAsync(x_dev, P.yv[0], nb, cudaMemcpyDeviceToDevice, st));
+}
+
+void refined_solve_device(H2Mat& m, Factorization& f, const double* b_dev, double* x_dev, int steps) {
+    // solve.py:63-77
+    cudaStream_t st = ctx().stream;
+    const int64_t n = f.n;
+    // refinement temporaries: the factor's work region, rewound on every call
+    Region& w = f.work;
+    w.reset();
+    double* tmp = w.alloc_n<double>(n);
+    double* res = w.alloc_n<double>(n);
+    double* dx = w.alloc_n<double>(n);
+    solve_device(f, b_dev, x_dev, 1);
+    for (int it = 0; it < steps; ++it) {
+        matvec_device(m, x_dev, tmp, 1);
+        launch_axpby(res, b_dev, 1.0, tmp, -1.0, n, st);
+        solve_device(f, res, dx, 1);
+        launch_axpby(x_dev, x_dev, 1.0, dx, 1.0, n, st);
+    }
+}
+
+}  // namespace h2f

@@ -1,0 +1,186 @@
+"""GPU parity: the B200 path (through the C ABI) against the CPU oracle and
+the reference's golden fixtures.
+
+Contract:
+  * bit-exact integer structure (batches, r per cluster, offsets, up_index,
+    edge (other, kind, shape), colouring statistics, top size, nbytes) for
+    the families whose threshold decisions are robust (cov2d, cov3d);
+  * norm estimate within 1e-12 relative (power iteration, reordered sums);
+  * refined solution within 1e-8 relative of the reference's, backward error
+    within 10x of the reference's (raw and refined);
+  * skeleton projectors q[:, r:] q[:, r:]^T within 1e-10 of the oracle's.
+"""
+import numpy as np
+import pytest
+
+import paper_2509_11152_b200 as H
+from golden_util import golden_structure, load, one_thread, problem, rhs, structure_of
+from oracle import h2_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ROBUST = ["cov2d_1024", "cov3d_2048", "cov2d_4096", "cov3d_e8_4096"]
+SENSITIVE = ["laplace2d_2048", "helmholtz3d_2048", "laplace3d_4096", "osc2d_4096"]
+
+_fac_cache = {}
+
+
+def gpu_factor(case):
+    if case not in _fac_cache:
+        _, _, _, h2, prm = problem(case)
+        _fac_cache[case] = (h2, prm, H.factorize(h2, prm["eps_lu"]))
+    return _fac_cache[case]
+
+
+@pytest.mark.parametrize("case", ["cov2d_1024", "laplace3d_4096", "osc2d_4096"])
+def test_matvec_matches_oracle(case):
+    _, _, _, h2, _ = problem(case)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(h2.n)
+    with one_thread():
+        ref = O.matvec(h2, x)
+    y = H.matvec(h2, x)
+    assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref)
+    X = rng.standard_normal((h2.n, 3))
+    Y = H.matvec(h2, X)
+    for j in range(3):
+        with one_thread():
+            r = O.matvec(h2, X[:, j])
+        assert np.linalg.norm(Y[:, j] - r) <= 1e-13 * np.linalg.norm(r)
+
+
+@pytest.mark.parametrize("case", ROBUST + SENSITIVE)
+def test_norm_estimate(case):
+    g = load(case)
+    _, _, _, h2, _ = problem(case)
+    est = H.estimate_norm2(h2)
+    assert abs(est - float(g["norm_estimate"])) <= 1e-12 * float(g["norm_estimate"])
+
+
+@pytest.mark.parametrize("case", ROBUST)
+def test_structure_bit_exact(case):
+    g = load(case)
+    h2, prm, fac = gpu_factor(case)
+    assert structure_of(fac) == golden_structure(g)
+    for lv, rec in zip(g["levels"], fac.records):
+        assert np.array_equal(rec.up_index, g[f"up_index_{lv['level']}"])
+        assert {str(c): o for c, o in rec.offset.items()} == lv["offset"]
+        for c, f in rec.factors.items():
+            assert [[o, k, list(m.shape)] for o, k, m in f.edges] == lv["edges"][str(c)]
+    assert fac.top_size == int(g["top_size"])
+    assert fac.nbytes() == int(g["factor_bytes"])
+
+
+@pytest.mark.parametrize("case", ROBUST)
+def test_pivots_match_reference(case):
+    g = load(case)
+    _, _, fac = gpu_factor(case)
+    mism, total = 0, 0
+    for lv, rec in zip(g["levels"], fac.records):
+        for c, f in rec.factors.items():
+            want = lv["piv"][str(c)]
+            got = None if f.piv is None else f.piv.tolist()
+            total += 1
+            mism += got != want
+    assert np.array_equal(fac.top_piv.astype(np.int64), g["top_piv"])
+    assert mism == 0, f"{mism} of {total} clusters pivot differently"
+
+
+@pytest.mark.parametrize("case", ROBUST + SENSITIVE)
+def test_solution_and_backward_error(case):
+    g = load(case)
+    h2, prm, fac = gpu_factor(case)
+    b = rhs(h2, H.matvec)
+    x = H.refined_solve(h2, fac, b, steps=1)
+    raw = H.solve(fac, b)
+
+    def eb(v):
+        return np.linalg.norm(H.matvec(h2, v) - b) / np.linalg.norm(b)
+
+    assert eb(x) <= 10 * max(float(g["e_b"]), 1e-15)
+    assert eb(raw) <= 10 * max(float(g["e_b_raw"]), 1e-15)
+    if case in ROBUST:
+        assert np.linalg.norm(x - g["x"]) <= 1e-8 * np.linalg.norm(g["x"])
+
+
+@pytest.mark.parametrize("case", ["cov2d_1024", "cov3d_2048"])
+def test_skeleton_projectors_match_oracle(case):
+    h2, prm, fac = gpu_factor(case)
+    with one_thread():
+        ofac = O.factorize(h2, prm["eps_lu"])
+    worst = 0.0
+    for rec, orec in zip(fac.records, ofac.records):
+        for c, f in rec.factors.items():
+            of = orec.factors[c]
+            assert f.r == of.r
+            qs, oqs = f.q[:, f.r:], of.q[:, of.r:]
+            worst = max(worst, np.abs(qs @ qs.T - oqs @ oqs.T).max())
+    assert worst <= 1e-10, worst
+
+
+@pytest.mark.parametrize("case", ["cov2d_1024", "laplace2d_2048"])
+def test_rotations_orthogonal(case):
+    _, _, fac = gpu_factor(case)
+    for rec in fac.records:
+        for f in rec.factors.values():
+            dim = f.q.shape[0]
+            assert np.abs(f.q.T @ f.q - np.eye(dim)).max() <= 1e-12 * dim
+
+
+def test_solve_linear_multi_and_deterministic():
+    h2, prm, fac = gpu_factor("cov2d_1024")
+    rng = np.random.default_rng(3)
+    b1, b2 = rng.standard_normal(fac.n), rng.standard_normal(fac.n)
+    lhs = H.solve(fac, 0.7 * b1 - 2.3 * b2)
+    rhs_ = 0.7 * H.solve(fac, b1) - 2.3 * H.solve(fac, b2)
+    assert np.linalg.norm(lhs - rhs_) <= 1e-10 * np.linalg.norm(lhs)
+    B = rng.standard_normal((fac.n, 5))
+    X = H.solve_multi(fac, B)
+    for j in range(5):
+        one = H.solve(fac, B[:, j])
+        assert np.linalg.norm(X[:, j] - one) <= 1e-12 * np.linalg.norm(one)
+    assert np.array_equal(H.solve(fac, b1), H.solve(fac, b1))
+    assert np.array_equal(X, H.solve_multi(fac, B, threads=4))
+
+
+def test_solve_validates_shapes():
+    _, _, fac = gpu_factor("cov2d_1024")
+    with pytest.raises(ValueError):
+        H.solve(fac, np.zeros(fac.n + 1))
+    with pytest.raises(ValueError):
+        H.solve_multi(fac, np.zeros(fac.n))
+    with pytest.raises(ValueError):
+        H.solve_multi(fac, np.zeros((fac.n + 2, 3)))
+
+
+def test_factor_oracle_oracle_agreement_on_solution():
+    # the oracle is the checker: same input, raw solutions agree closely
+    h2, prm, fac = gpu_factor("cov3d_2048")
+    with one_thread():
+        ofac = O.factorize(h2, prm["eps_lu"])
+        b = rhs(h2, O.matvec)
+        xo = O.substitute(ofac, b)
+    xg = H.solve(fac, b)
+    assert np.linalg.norm(xg - xo) <= 1e-8 * np.linalg.norm(xo)
+
+
+def test_singular_leaf_block_names_cluster():
+    _, _, _, h2, prm = problem("cov2d_1024")
+    leaf = int(h2.tree.levels[h2.tree.depth][0])
+    import copy
+    bad = copy.copy(h2)
+    bad.dense = dict(h2.dense)
+    bad.dense[(leaf, leaf)] = np.zeros_like(h2.dense[(leaf, leaf)])
+    with pytest.raises(H.FactorizationError, match="cluster"):
+        H.factorize(bad, 1e-6)
+
+
+def test_factorize_bitwise_deterministic():
+    _, _, _, h2, prm = problem("cov2d_1024")
+    f1 = H.factorize(h2, prm["eps_lu"])
+    f2 = H.factorize(h2, prm["eps_lu"], threads=4)
+    b = np.random.default_rng(8).standard_normal(h2.n)
+    assert np.array_equal(H.solve(f1, b), H.solve(f2, b))
+    r1, r2 = f1.records[0], f2.records[0]
+    c = r1.clusters[0]
+    assert np.array_equal(r1.factors[c].q, r2.factors[c].q)
