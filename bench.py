@@ -1,0 +1,360 @@
+"""Benchmark: H2 factor + solve time on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
+
+One step = factorize(h2, eps_lu) (30-step norm estimate included, as in the
+reference) + refined_solve(h2, fac, b, steps=1), the pair the reference's
+harness times (harness.py:203-213).  `value` is measured with the operator
+and b already resident in HBM, with CUDA events on the library's stream;
+`e2e` goes through the public Python API with host buffers (operator upload,
+b H2D, x D2H inside the timed region).  Multi-GPU (torchrun): every rank
+factors its own replica (weak scaling, "replicas only" for now, see
+DESIGN.md), max over ranks.
+
+--impl reference times the CPU oracle (the reference algorithm restated,
+oracle/h2_oracle.py; the reference package itself is pure Python and cannot
+be shipped to the GPU box) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs reachable on one GPU.  n, problem row, overrides.
+CONFIGS = {
+    1: dict(problem="cov2d", n=16384, over={}, desc="2D exp covariance N=16384 (configs[0])"),
+    2: dict(problem="helmholtz3d", n=131072, over={"kappa": 0.0},
+            desc="3D Laplace 1/r N=131072 single GPU (configs[1])"),
+    4: dict(problem="helmholtz3d", n=524288, over={"dim": 2, "p0": 8, "eta": 0.9},
+            desc="2D oscillatory cos(3r)/r N=524288 (configs[3])"),
+}
+DEFAULT_CONFIG = int(os.environ.get("H2F_BENCH_CONFIG", "1"))
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def load_peaks():
+    try:
+        with open(PEAKS) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                for nm, flag in zip(names, parts[5:9]):
+                    if flag.lower().startswith("active"):
+                        reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(want_nccl=True):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist_mod.init_process_group("nccl" if want_nccl else "gloo")
+        dist = dist_mod
+    return world, rank, local, dist
+
+
+def max_over_ranks(value, dist, device=None):
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def build_input(cfg):
+    import paper_2509_11152_b200 as H
+    t0 = time.perf_counter()
+    tree, part, spec, h2, prm = H.build_problem(cfg["problem"], cfg["n"], **cfg["over"])
+    return h2, prm, time.perf_counter() - t0
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle on a bounded sample
+# ---------------------------------------------------------------------------
+
+def cpu_sample(cfg, budget_s=25.0):
+    """Time the oracle's factorize + refined_solve on the workload itself when
+    it fits the budget, else on two smaller N of the same family and
+    extrapolate to the full N with the fitted log-log slope."""
+    from threadpoolctl import threadpool_limits
+
+    import paper_2509_11152_b200.problem as P
+    from oracle import h2_oracle as O
+
+    def run(n):
+        tree, part, spec, h2, prm = P.build_problem(cfg["problem"], n, **cfg["over"])
+        with threadpool_limits(1):
+            t0 = time.perf_counter()
+            fac = O.factorize(h2, prm["eps_lu"])
+            x_ref = np.random.Generator(np.random.Philox(7)).standard_normal(n)
+            b = O.matvec(h2, x_ref)
+            O.refined_solve(h2, fac, b, steps=1)
+            return time.perf_counter() - t0
+
+    n_full = cfg["n"]
+    small = {1: [n_full], 2: [4096, 8192], 4: [8192, 16384]}.get(
+        next(k for k, v in CONFIGS.items() if v is cfg), [n_full])
+    if small == [n_full]:
+        t = run(n_full)
+        return {"value": t, "sample": f"full workload {cfg['desc']}, oracle factorize+refined_solve",
+                "extrapolated": False}
+    ts = [run(n) for n in small]
+    slope = float(np.log(ts[1] / ts[0]) / np.log(small[1] / small[0]))
+    est = ts[1] * (n_full / small[1]) ** slope
+    return {"value": est, "sample": f"oracle factorize+refined_solve at N={small} "
+            f"({ts[0]:.2f}s, {ts[1]:.2f}s), log-log slope {slope:.2f} extrapolated to N={n_full}",
+            "extrapolated": True}
+
+
+def run_reference(args, cfg):
+    world, rank, local, dist = dist_setup(want_nccl=False)
+    if rank != 0:
+        return
+    steps = []
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(cfg)
+        if i >= args.warmup:
+            steps.append(s["value"])
+        if i == 0 and s["extrapolated"] and args.warmup + args.steps > 2:
+            # each extrapolated sample costs ~25 s; one timed step is enough
+            steps = [s["value"]]
+            break
+    v = float(np.mean(steps))
+    line = {
+        "impl": "reference", "metric": "H2 factor+solve time (s)", "value": v, "unit": "s",
+        "n_gpus": args.gpus, "steps": len(steps), "warmup": args.warmup, "higher_is_better": False,
+        "dtype": "f64", "data": "synthetic", "scaling": "weak",
+        "config": {"workload": cfg["desc"], "n": cfg["n"], "problem": cfg["problem"], **cfg["over"]},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": s["sample"]},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "vs_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def run_b200(args, cfg):
+    world, rank, local, dist = dist_setup(want_nccl=True)
+    os.environ["H2F_DEVICE"] = str(local)
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    # buffers owned by torch (allocated before the library claims its arena)
+    n = cfg["n"]
+    b_dev = torch.empty(n, dtype=torch.float64, device=dev)
+    x_dev = torch.empty(n, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > L2
+
+    import paper_2509_11152_b200 as H
+    from paper_2509_11152_b200 import _lib as L
+    from paper_2509_11152_b200.h2core import device_matrix, power_start
+
+    h2, prm, t_build = build_input(cfg)
+    lib = L.ensure_init()
+    dmma_tf = L.bench_dmma(20000)
+    dm = device_matrix(h2)
+    x_true = np.random.Generator(np.random.Philox(7)).standard_normal(n)
+    b_host = H.matvec(h2, x_true)
+    b_dev.copy_(torch.from_numpy(b_host))
+    v0 = np.ascontiguousarray(power_start(n))
+    stream = torch.cuda.ExternalStream(L.stream_handle(), device=dev)
+
+    import ctypes as C
+
+    def step():
+        fh = C.c_void_p()
+        st = L.Status()
+        L.check(lib.h2f_factorize(dm.handle, float(prm["eps_lu"]), -1.0, L.ptr(v0), C.byref(fh),
+                                  C.byref(st)), "factorize")
+        L.check(lib.h2f_refined_solve_dev(dm.handle, fh, C.c_void_p(b_dev.data_ptr()),
+                                          C.c_void_p(x_dev.data_ptr()), 1), "refined_solve")
+        return fh
+
+    for _ in range(args.warmup):
+        lib.h2f_factor_destroy(step())
+    torch.cuda.synchronize()
+    launches0 = L.kernel_launches()
+    L.profile_enable(True)
+    L.profile_reset()
+    clocks = ClockSampler(local)
+    times = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between timed steps (outside the timed window)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fh = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+        lib.h2f_factor_destroy(fh)
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    prof = L.profile_get()
+    L.profile_enable(False)
+    launches = (L.kernel_launches() - launches0) / args.steps
+    t_step = max_over_ranks(float(np.mean(times)), dist, dev)
+
+    # accuracy of the last step
+    x = x_dev.cpu().numpy()
+    e_b = float(np.linalg.norm(H.matvec(h2, x) - b_host) / np.linalg.norm(b_host))
+
+    # e2e through the public API with host buffers (operator upload included)
+    e2e_times = []
+    h2d = d2h = 0
+    for _ in range(max(1, min(args.steps, 2))):
+        if hasattr(h2, "_h2f_device"):
+            object.__setattr__(h2, "_h2f_device", None)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fac = H.factorize(h2, prm["eps_lu"])
+        xh = H.refined_solve(h2, fac, b_host, steps=1)
+        e2e_times.append(time.perf_counter() - t0)
+        h2d = h2_bytes(h2) + b_host.nbytes
+        d2h = xh.nbytes
+        del fac
+    t_e2e = max_over_ranks(float(np.mean(e2e_times)), dist, dev)
+
+    peaks, peak_kind = load_peaks()
+    roof = roofline(prof, peaks, peak_kind, dmma_tf)
+    line = {
+        "metric": "H2 factor+solve time (s)", "value": t_step, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg["desc"], "n": n, "problem": cfg["problem"], **cfg["over"],
+                   "eps_lu": prm["eps_lu"], "eps": prm["eps"], "leaf": prm["m"],
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "flushed between timed steps (256 MB write)"},
+        "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(round(launches)),
+        "roofline": roof,
+        "clocks": clk,
+        "backward_error": e_b,
+        "fp64_dmma_tflops_measured": dmma_tf,
+        "input_build_s": t_build,
+        "phase_seconds_last": None,
+        "kernels": {k: {"ms": v["seconds"] * 1e3 / args.steps, "launches": v["launches"] // args.steps,
+                        "gflop": v["flops"] / 1e9 / args.steps, "gbytes": v["bytes"] / 1e9 / args.steps}
+                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["seconds"])},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        s = cpu_sample(cfg)
+        line["cpu_baseline"] = {"value": s["value"], "unit": "s", "cores": 1, "kind": "port",
+                                "sample": s["sample"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def h2_bytes(h2):
+    return sum(b.nbytes for s in (h2.leaf_basis, h2.transfer, h2.coupling, h2.dense) for b in s.values())
+
+
+def roofline(prof, peaks, peak_kind, dmma_tf):
+    """Dominant kernel (most device time) against its bound."""
+    if not prof:
+        return None
+    name, p = max(prof.items(), key=lambda kv: kv[1]["seconds"])
+    if p["seconds"] <= 0:
+        return None
+    ai = p["flops"] / max(p["bytes"], 1.0)
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    ridge = dmma_tf * 1e12 / (hbm * 1e9)
+    if ai >= ridge:
+        achieved = p["flops"] / p["seconds"] / 1e12
+        return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": dmma_tf, "unit": "TFLOP/s",
+                "frac": achieved / dmma_tf, "traffic": None,
+                "peak_source": "FP64 DMMA m8n8k4 peak measured in this run (MEASURED_PEAKS.json has no FP64)",
+                "launches": p["launches"], "seconds": p["seconds"]}
+    achieved = p["bytes"] / p["seconds"] / 1e9
+    return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "peak_source": f"{peak_kind} hbm_gbs",
+            "launches": p["launches"], "seconds": p["seconds"]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

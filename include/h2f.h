@@ -109,6 +109,14 @@ typedef struct {
     int64_t offset;          /* offset in the level vector                       */
 } h2f_cluster_info;
 
+typedef struct {
+    char name[32];
+    int64_t launches;
+    double seconds;          /* sum of CUDA-event durations of the launches      */
+    double flops;            /* algorithmic FP64 flops (SURVEY.md §8d formulas)   */
+    double bytes;            /* algorithmic HBM bytes                            */
+} h2f_kernel_profile;
+
 /* ---- context ------------------------------------------------------------ */
 int h2f_init(int device, double arena_gb);   /* arena_gb <= 0: automatic      */
 const char* h2f_last_error(void);
@@ -116,6 +124,14 @@ int h2f_stream(void** stream_out);           /* cudaStream_t of the library    *
 int h2f_device_count(int* count);
 int h2f_kernel_launches(int64_t* count);     /* kernels launched so far        */
 int h2f_memory_stats(int64_t* arena_bytes, int64_t* in_use, int64_t* peak);
+
+/* ---- measurement ----------------------------------------------------------- */
+int h2f_profile_enable(int on);              /* CUDA events around every launch */
+int h2f_profile_reset(void);
+int h2f_profile_count(int32_t* nkernels);
+int h2f_profile_get(int32_t kid, h2f_kernel_profile* out);   /* syncs the stream */
+/* FP64 DMMA (m8n8k4) throughput probe: all SMs, iters MMAs per warp chain */
+int h2f_bench_dmma(int64_t iters, double* tflops);
 
 /* ---- H2 matrix ----------------------------------------------------------- */
 int h2f_matrix_create(const h2f_matrix_desc* desc, const double* vals, h2f_matrix* out);

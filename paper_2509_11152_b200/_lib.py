@@ -37,6 +37,11 @@ class MatrixDesc(C.Structure):
     ]
 
 
+class KernelProfile(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("seconds", C.c_double),
+                ("flops", C.c_double), ("bytes", C.c_double)]
+
+
 class Status(C.Structure):
     _fields_ = [("code", C.c_int32), ("cluster", C.c_int32), ("level", C.c_int32)]
 
@@ -67,6 +72,11 @@ _SIGS = {
     "h2f_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "h2f_kernel_launches": (C.c_int, [i64p]),
     "h2f_memory_stats": (C.c_int, [i64p, i64p, i64p]),
+    "h2f_profile_enable": (C.c_int, [C.c_int]),
+    "h2f_profile_reset": (C.c_int, []),
+    "h2f_profile_count": (C.c_int, [i32p]),
+    "h2f_profile_get": (C.c_int, [C.c_int32, C.POINTER(KernelProfile)]),
+    "h2f_bench_dmma": (C.c_int, [C.c_int64, f64p]),
     "h2f_matrix_create": (C.c_int, [C.POINTER(MatrixDesc), f64p, C.POINTER(C.c_void_p)]),
     "h2f_matrix_destroy": (C.c_int, [C.c_void_p]),
     "h2f_matrix_nbytes": (C.c_int, [C.c_void_p, i64p]),
@@ -177,3 +187,31 @@ def memory_stats():
     a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
     check(ensure_init().h2f_memory_stats(C.byref(a), C.byref(b), C.byref(c)))
     return {"arena_bytes": a.value, "in_use": b.value, "peak": c.value}
+
+
+def profile_enable(on=True):
+    check(ensure_init().h2f_profile_enable(1 if on else 0))
+
+
+def profile_reset():
+    check(ensure_init().h2f_profile_reset())
+
+
+def profile_get():
+    """{kernel name: {launches, seconds, flops, bytes}} since the last reset."""
+    n = C.c_int32()
+    check(lib().h2f_profile_count(C.byref(n)))
+    out = {}
+    for k in range(n.value):
+        p = KernelProfile()
+        check(lib().h2f_profile_get(k, C.byref(p)))
+        if p.launches:
+            out[p.name.decode()] = {"launches": p.launches, "seconds": p.seconds, "flops": p.flops,
+                                    "bytes": p.bytes}
+    return out
+
+
+def bench_dmma(iters=20000):
+    v = C.c_double()
+    check(ensure_init().h2f_bench_dmma(int(iters), C.byref(v)))
+    return v.value

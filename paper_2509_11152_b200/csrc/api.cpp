@@ -92,6 +92,37 @@ int h2f_memory_stats(int64_t* arena_bytes, int64_t* in_use, int64_t* peak) {
     });
 }
 
+int h2f_profile_enable(int on) {
+    return guard([&] { ctx().prof.on = on != 0; });
+}
+
+int h2f_profile_reset(void) {
+    return guard([&] { ctx().prof.reset(); });
+}
+
+int h2f_profile_count(int32_t* nkernels) {
+    *nkernels = K_COUNT;
+    return H2F_OK;
+}
+
+int h2f_profile_get(int32_t kid, h2f_kernel_profile* out) {
+    return guard([&] {
+        if (kid < 0 || kid >= K_COUNT) throw Error(H2F_E_ARG, "kernel id out of range");
+        Profiler& P = ctx().prof;
+        P.collect();
+        std::memset(out, 0, sizeof(*out));
+        std::strncpy(out->name, kernel_name(kid), sizeof(out->name) - 1);
+        out->launches = P.totals[kid].launches;
+        out->seconds = P.totals[kid].seconds;
+        out->flops = P.totals[kid].flops;
+        out->bytes = P.totals[kid].bytes;
+    });
+}
+
+int h2f_bench_dmma(int64_t iters, double* tflops) {
+    return guard([&] { *tflops = bench_dmma(iters, ctx().stream); });
+}
+
 int h2f_matrix_create(const h2f_matrix_desc* desc, const double* vals, h2f_matrix* out) {
     return guard([&] {
         if (!desc || !out) throw Error(H2F_E_ARG, "null argument");

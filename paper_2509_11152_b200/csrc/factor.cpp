@@ -109,6 +109,7 @@ struct GemmBuild {
     std::vector<GemmContrib> contribs;
     std::vector<int64_t> tile_start{0};
     int64_t norm_tiles = 0;
+    double flops = 0, bytes = 0;  // algorithmic work of the launch (profiler)
 
     static int64_t tiles(int M, int N) { return cdiv(M, GEMM_TILE) * cdiv(N, GEMM_TILE); }
     // returns the task's norm base (mode NORM) or -1
@@ -124,6 +125,11 @@ struct GemmBuild {
         t.contrib_begin = int64_t(contribs.size());
         contribs.insert(contribs.end(), cs, cs + nc);
         t.contrib_end = int64_t(contribs.size());
+        for (size_t i = 0; i < nc; ++i) {
+            flops += 2.0 * M * N * cs[i].K;
+            bytes += 8.0 * (double(M) * cs[i].K + double(cs[i].K) * N);
+        }
+        bytes += mode == GEMM_ADD ? 16.0 * M * N : (mode == GEMM_STORE ? 8.0 * M * N : 0.0);
         t.norm_base = -1;
         const int64_t nt = tiles(M, N);
         if (mode == GEMM_NORM) {
@@ -137,13 +143,14 @@ struct GemmBuild {
     int64_t add1(double* C, int64_t ldc, int M, int N, int mode, const GemmContrib& c) {
         return add(C, ldc, M, N, mode, &c, 1);
     }
-    void launch(double* norms = nullptr) {
+    void launch(int kid, double* norms = nullptr, double bytes_override = -1.0) {
         if (tasks.empty()) return;
         Context& X = ctx();
         auto* dt = X.up.put(tasks);
         auto* dc = X.up.put(contribs);
         auto* ds = X.up.put(tile_start);
         X.up.flush(X.stream);
+        ProfScope ps(kid, flops, bytes_override >= 0 ? bytes_override : bytes);
         launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), tile_start.back(), norms, X.stream);
     }
 };
@@ -165,6 +172,7 @@ inline GemmContrib contrib(const double* A, int64_t lda, int transA, const doubl
 struct CopyBuild {
     std::vector<CopyTask> tasks;
     std::vector<int64_t> tile_start{0};
+    double bytes = 0;
     void add(double* dst, int64_t ldd, int rows, int cols, const double* src, int64_t lds, int trans,
              int mode, double alpha = 1.0) {
         if (rows <= 0 || cols <= 0) return;
@@ -180,6 +188,7 @@ struct CopyBuild {
         t.alpha = alpha;
         tasks.push_back(t);
         tile_start.push_back(tile_start.back() + cdiv(rows, COPY_TILE) * cdiv(cols, COPY_TILE));
+        bytes += double(rows) * cols * (mode == COPY_ZERO ? 8.0 : (mode == COPY_ADD ? 24.0 : 16.0));
     }
     void zero(double* dst, int64_t ldd, int rows, int cols) { add(dst, ldd, rows, cols, nullptr, 0, 0, COPY_ZERO); }
     void launch() {
@@ -188,6 +197,7 @@ struct CopyBuild {
         auto* dt = X.up.put(tasks);
         auto* ds = X.up.put(tile_start);
         X.up.flush(X.stream);
+        ProfScope ps(K_COPY, 0.0, bytes);
         launch_copy_tasks(dt, ds, int32_t(tasks.size()), tile_start.back(), X.stream);
     }
 };
@@ -400,11 +410,33 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             cmp.push_back(ct);
         }
         gather.launch();
-        g1.launch();
-        g2.launch();
-        if (!qr.empty()) launch_qr_r(upload(qr), int32_t(qr.size()), st);
-        launch_jacobi(upload(svd), int32_t(svd.size()), drop, st);
-        launch_complement(upload(cmp), int32_t(cmp.size()), st);
+        g1.launch(K_GEMM_AUG);
+        g2.launch(K_GEMM_AUG);
+        double qf = 0, qb = 0, jf = 0, jb = 0, cf = 0, cb = 0;
+        for (auto& t : qr) {
+            const double s = t.s, w = t.wf;
+            qf += 2.0 * w * s * s - (w >= s ? 2.0 / 3.0 * s * s * s : 0.0);
+            qb += 8.0 * s * w + 8.0 * s * s;
+        }
+        for (auto& t : svd) {
+            const double m = t.m, s = t.s;
+            jf += 22.0 * m * m * s;  // c_svd = 22 convention
+            jb += 16.0 * m * s;
+            cf += 4.0 * s * s * s;
+            cb += 16.0 * s * s;
+        }
+        {
+            ProfScope ps(K_QR, qf, qb);
+            if (!qr.empty()) launch_qr_r(upload(qr), int32_t(qr.size()), st);
+        }
+        {
+            ProfScope ps(K_JACOBI, jf, jb);
+            launch_jacobi(upload(svd), int32_t(svd.size()), drop, st);
+        }
+        {
+            ProfScope ps(K_COMPLEMENT, cf, cb);
+            launch_complement(upload(cmp), int32_t(cmp.size()), st);
+        }
     }
     int* kept_h = static_cast<int*>(X.pinned_buf(sizeof(int) * nb));
     H2F_CUDA(cudaMemcpyAsync(kept_h, kept_d, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
@@ -454,8 +486,8 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             }
             B = View{out, B.cols, B.rows, B.cols};
         }
-        p1.launch();
-        p2.launch();
+        p1.launch(K_GEMM_PROJECT);
+        p2.launch(K_GEMM_PROJECT);
     }
 
     // ------------------------------------------------------------- eliminate
@@ -550,8 +582,22 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             el.push_back(std::move(e));
         }
         panels.launch();
-        if (!lus.empty()) launch_lu(upload(lus), int32_t(lus.size()), st);
-        if (!trs.empty()) launch_trsm(upload(trs), int32_t(trs.size()), st);
+        double lf = 0, lb = 0, tf = 0, tb = 0;
+        for (auto& e : el) {
+            const double r = e.r, W = double(e.W);
+            lf += 2.0 / 3.0 * r * r * r;
+            lb += 16.0 * r * r;
+            tf += 2.0 * r * r * W;
+            tb += 16.0 * r * W + 8.0 * r * r;
+        }
+        {
+            ProfScope ps(K_LU, lf, lb);
+            if (!lus.empty()) launch_lu(upload(lus), int32_t(lus.size()), st);
+        }
+        {
+            ProfScope ps(K_TRSM, tf, tb);
+            if (!trs.empty()) launch_trsm(upload(trs), int32_t(trs.size()), st);
+        }
     }
 
     // Schur updates (factorization.py:122-126) fused with the scatter into the
@@ -623,16 +669,22 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             }
     }
     GemmBuild sch;
+    // algorithmic bytes: panels G and -W read once per
+    // cluster, every existing target element read+written once
+    double schur_bytes = 0;
+    for (auto& e : el) schur_bytes += 16.0 * e.r * double(e.W);
+    for (auto& t : targets) schur_bytes += 16.0 * t.M * double(t.N);
     for (auto& t : targets) sch.add(t.C, t.ldc, t.M, t.N, GEMM_ADD, t.cs.data(), t.cs.size());
     for (auto& cd : cands) cd.base = sch.add1(nullptr, 0, cd.M, cd.N, GEMM_NORM, cd.g);
     double* norms_d = sch.norm_tiles ? scr.alloc_n<double>(sch.norm_tiles) : nullptr;
     double* cand_ss_d = cands.empty() ? nullptr : scr.alloc_n<double>(cands.size());
-    sch.launch(norms_d);
+    sch.launch(K_GEMM_SCHUR, norms_d, schur_bytes);
     if (!cands.empty()) {
         std::vector<int64_t> seg(cands.size() + 1, 0);
         for (size_t i = 0; i < cands.size(); ++i) seg[i + 1] = cands[i].base + cands[i].ntiles;
         for (size_t i = 0; i < cands.size(); ++i)
             if (cands[i].base != seg[i]) throw Error(H2F_E_INTERNAL, "assertion: norm segments");
+        ProfScope ps(K_REDUCE, 0.0, 8.0 * double(sch.norm_tiles));
         launch_sumsq_reduce(norms_d, upload(seg), int32_t(cands.size()), cand_ss_d, st);
     }
     // one sync: LU status + candidate norms
@@ -675,7 +727,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             }
         }
         for (auto& t : news) create.add(t.C, t.ldc, t.M, t.N, GEMM_STORE, t.cs.data(), t.cs.size());
-        create.launch();
+        create.launch(K_GEMM_CREATE);
     }
     // slice to skeletons (views only) and mark done (factorization.py:513-523)
     for (int bi = 0; bi < nb; ++bi) {
@@ -862,15 +914,19 @@ void Factorizer::top_factor(double* A, int64_t n) {
     const int nb = 64;
     for (int64_t k0 = 0; k0 < n; k0 += nb) {
         const int w = int(std::min<int64_t>(nb, n - k0));
-        launch_panel_lu(A, n, int(n), int(k0), w, F.top_piv, st);
-        launch_row_swaps(A, n, int(n), int(k0), w, F.top_piv, int(k0), int(k0 + w), st);
+        {
+            ProfScope ps(K_TOP_PANEL, double(n - k0) * w * w, 16.0 * double(n - k0) * w);
+            launch_panel_lu(A, n, int(n), int(k0), w, F.top_piv, st);
+        }
         const int64_t rest = n - k0 - w;
+        ProfScope ps(K_TOP_MISC, double(rest) * w * w, 16.0 * double(n) * w + 16.0 * double(rest) * w);
+        launch_row_swaps(A, n, int(n), int(k0), w, F.top_piv, int(k0), int(k0 + w), st);
         if (rest > 0) {
             launch_trsm_unit_lower_rows(A, n, int(k0), w, int(k0 + w), int(rest), st);
             GemmBuild g;
             g.add1(A + (k0 + w) * n + (k0 + w), n, int(rest), int(rest), GEMM_ADD,
                    contrib(A + (k0 + w) * n + k0, n, 0, A + k0 * n + (k0 + w), n, 0, w, -1.0));
-            g.launch();
+            g.launch(K_GEMM_TOP);
         }
     }
     launch_diag_absmin(A, n, int(n), red + 1, st);

@@ -221,6 +221,12 @@ MatvecPlan& matvec_plan(H2Mat& m, int nrhs) {
         if (b.tasks.empty()) continue;
         GemvLaunch L;
         L.ntasks = int32_t(b.tasks.size());
+        for (auto& t : b.tasks)
+            for (int64_t ci = t.contrib_begin; ci < t.contrib_end; ++ci) {
+                const double e = double(t.rows) * b.contribs[ci].cols;
+                L.flops += 2.0 * e * nrhs;
+                L.bytes += 8.0 * e + 8.0 * b.contribs[ci].cols * nrhs;
+            }
         L.tasks = P.mem.alloc_n<GemvTask>(b.tasks.size());
         L.contribs = P.mem.alloc_n<GemvContrib>(std::max<size_t>(b.contribs.size(), 1));
         H2F_CUDA(cudaMemcpyAsync(L.tasks, b.tasks.data(), sizeof(GemvTask) * b.tasks.size(),
@@ -237,7 +243,10 @@ MatvecPlan& matvec_plan(H2Mat& m, int nrhs) {
 }
 
 static void run_plan(MatvecPlan& P) {
-    for (auto& L : P.launches) launch_gemv_tasks(L.tasks, L.ntasks, L.contribs, P.nrhs, ctx().stream);
+    for (auto& L : P.launches) {
+        ProfScope ps(K_MATVEC, L.flops, L.bytes);
+        launch_gemv_tasks(L.tasks, L.ntasks, L.contribs, P.nrhs, ctx().stream);
+    }
 }
 
 void matvec_device(H2Mat& m, const double* x_dev, double* y_dev, int nrhs) {

@@ -22,6 +22,7 @@ struct GemvLaunch {
     GemvTask* tasks;
     GemvContrib* contribs;
     int32_t ntasks;
+    double flops = 0, bytes = 0;
 };
 
 struct MatvecPlan {

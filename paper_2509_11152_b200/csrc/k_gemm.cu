@@ -221,6 +221,21 @@ __global__ void sumsq_reduce_kernel(const double* __restrict__ parts, const int6
     if (lane == 0) out[w] = s;
 }
 
+__global__ void __launch_bounds__(128) dmma_peak_kernel(int64_t iters, double* out) {
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+    double a = 1.0 + 1e-3 * threadIdx.x, b = 1.0 - 1e-3 * threadIdx.x;
+    for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma_8x8x4(c[i][0], c[i][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+    if (s == 12345.678) out[threadIdx.x] = s;  // keeps the chain alive
+}
+
 int grid_for(int64_t ntiles, int per_sm) {
     const int64_t cap = (int64_t)148 * per_sm;
     return (int)(ntiles < cap ? ntiles : cap);
@@ -242,6 +257,30 @@ void launch_copy_tasks(const CopyTask* d_tasks, const int64_t* d_tile_start, int
     if (ntiles <= 0) return;
     copy_tasks_kernel<<<grid_for(ntiles, 16), 256, 0, st>>>(d_tasks, d_tile_start, ntasks, ntiles);
     count_launch();
+}
+
+double bench_dmma(int64_t iters, cudaStream_t st) {
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = sms * 8;
+    double* out = nullptr;
+    cudaMalloc(&out, 128 * sizeof(double));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    dmma_peak_kernel<<<grid, 128, 0, st>>>(iters / 10 + 1, out);  // warm-up
+    cudaEventRecord(a, st);
+    dmma_peak_kernel<<<grid, 128, 0, st>>>(iters, out);
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    const double flops = double(grid) * 4 /*warps*/ * double(iters) * 8 * 512.0;
+    return flops / (ms * 1e-3) / 1e12;
 }
 
 void launch_sumsq_reduce(const double* d_parts, const int64_t* d_seg, int32_t nseg, double* d_out,

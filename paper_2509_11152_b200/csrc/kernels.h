@@ -196,6 +196,7 @@ void launch_scale_by_inv(double* x, const double* w, int64_t n, const double* s,
 void launch_axpby(double* y, const double* a, double alpha, const double* b, double beta,
                   int64_t n, cudaStream_t st);
 
+double bench_dmma(int64_t iters, cudaStream_t st);
 int64_t kernel_launch_count();
 void count_launch();
 

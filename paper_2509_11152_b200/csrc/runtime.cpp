@@ -166,6 +166,74 @@ Uploader::~Uploader() {
     for (auto& c : chunks_) cudaFreeHost(c.host);
 }
 
+// ---------------------------------------------------------------- Profiler
+const char* kernel_name(int kid) {
+    static const char* names[K_COUNT] = {
+        "gemm_augment", "gemm_project", "gemm_schur", "gemm_fill_create", "gemm_top_update", "copy_tasks",
+        "qr_r", "jacobi_svd", "complement", "lu_redundant", "trsm_eliminator", "norm_reduce", "top_panel_lu",
+        "top_misc", "solve_fwd_clusters", "solve_fwd_scatter", "solve_bwd_clusters", "solve_top",
+        "solve_misc", "matvec_gemv", "vector_ops"};
+    return (kid >= 0 && kid < K_COUNT) ? names[kid] : "?";
+}
+
+cudaEvent_t Profiler::get_event() {
+    if (!pool_.empty()) {
+        cudaEvent_t e = pool_.back();
+        pool_.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    H2F_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+int Profiler::begin(int kid, double flops, double bytes) {
+    if (!on) return -1;
+    Rec r{kid, get_event(), get_event(), flops, bytes};
+    H2F_CUDA(cudaEventRecord(r.a, ctx().stream));
+    pending_.push_back(r);
+    return int(pending_.size()) - 1;
+}
+
+void Profiler::end(int slot) {
+    if (slot < 0 || slot >= int(pending_.size())) return;
+    H2F_CUDA(cudaEventRecord(pending_[slot].b, ctx().stream));
+}
+
+void Profiler::collect() {
+    if (pending_.empty()) return;
+    H2F_CUDA(cudaStreamSynchronize(ctx().stream));
+    for (auto& r : pending_) {
+        float ms = 0.f;
+        H2F_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        Total& t = totals[r.kid];
+        t.launches += 1;
+        t.seconds += ms * 1e-3;
+        t.flops += r.flops;
+        t.bytes += r.bytes;
+        pool_.push_back(r.a);
+        pool_.push_back(r.b);
+    }
+    pending_.clear();
+}
+
+void Profiler::reset() {
+    collect();
+    for (auto& t : totals) t = Total{};
+}
+
+Profiler::~Profiler() {
+    for (auto e : pool_) cudaEventDestroy(e);
+}
+
+ProfScope::ProfScope(int kid, double flops, double bytes) {
+    if (ctx_ready() && ctx().prof.on) slot = ctx().prof.begin(kid, flops, bytes);
+}
+
+ProfScope::~ProfScope() {
+    if (slot >= 0) ctx().prof.end(slot);
+}
+
 // ---------------------------------------------------------------- Context
 void* Context::pinned_buf(size_t bytes) {
     if (bytes > pinned_cap) {

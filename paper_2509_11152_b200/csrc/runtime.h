@@ -96,6 +96,38 @@ class Uploader {
     size_t cur_ = 0, used_ = 0, flushed_ = 0;
 };
 
+// ---- per-kernel profiler (CUDA events around launches; off by default) ------
+enum KernelId : int {
+    K_GEMM_AUG = 0, K_GEMM_PROJECT, K_GEMM_SCHUR, K_GEMM_CREATE, K_GEMM_TOP, K_COPY, K_QR, K_JACOBI,
+    K_COMPLEMENT, K_LU, K_TRSM, K_REDUCE, K_TOP_PANEL, K_TOP_MISC, K_SOLVE_FWD, K_SOLVE_SCATTER,
+    K_SOLVE_BWD, K_SOLVE_TOP, K_SOLVE_MISC, K_MATVEC, K_VECTOR, K_COUNT
+};
+const char* kernel_name(int kid);
+
+class Profiler {
+  public:
+    bool on = false;
+    int begin(int kid, double flops, double bytes);
+    void end(int slot);
+    void collect();  // syncs the stream, folds finished pairs into the totals
+    void reset();
+    struct Total { int64_t launches = 0; double seconds = 0, flops = 0, bytes = 0; };
+    Total totals[K_COUNT];
+    ~Profiler();
+
+  private:
+    struct Rec { int kid; cudaEvent_t a, b; double flops, bytes; };
+    std::vector<Rec> pending_;
+    std::vector<cudaEvent_t> pool_;
+    cudaEvent_t get_event();
+};
+
+struct ProfScope {
+    int slot = -1;
+    ProfScope(int kid, double flops = 0, double bytes = 0);
+    ~ProfScope();
+};
+
 struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -104,6 +136,7 @@ struct Context {
     // pinned staging for small device->host reads
     char* pinned = nullptr;
     size_t pinned_cap = 0;
+    Profiler prof;
     void* pinned_buf(size_t bytes);
     void sync();  // stream sync + uploader reset
 };

@@ -21,6 +21,7 @@ struct SolvePlan {
         ScatterGroup* groups = nullptr;
         int32_t ngroups = 0;
         int64_t* list = nullptr;
+        double fwd_flops = 0, fwd_bytes = 0, sc_bytes = 0;
     };
     struct Level {
         int64_t total = 0;
@@ -67,6 +68,7 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
             std::map<int64_t, std::pair<int, std::vector<int64_t>>> groups;
             std::vector<int64_t> group_order;
             int64_t soff = 0, woff = 0;
+            double flops_b = 0, bytes_b = 0;
             for (int c : batch) {
                 const ClusterFactor& cf = rec.factors[rec.pos.at(c)];
                 SolveCluster sc{};
@@ -105,6 +107,11 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
                 }
                 sc.edge_end = int64_t(edges.size());
                 cls.push_back(sc);
+                double ew = 0;
+                for (auto& e : cf.edges) ew += double(e.w);
+                flops_b += (2.0 * cf.s * cf.s + 2.0 * cf.r * ew + double(cf.r) * cf.r) * nrhs;
+                bytes_b += 8.0 * (double(cf.s) * cf.s + double(cf.r) * cf.r + cf.r * ew) +
+                           16.0 * (cf.s + ew) * nrhs;
             }
             std::vector<ScatterGroup> gs;
             std::vector<int64_t> list;
@@ -125,6 +132,9 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
             B.ngroups = int32_t(gs.size());
             B.groups = to_dev(P.mem, gs);
             B.list = to_dev(P.mem, list);
+            B.fwd_flops = flops_b;
+            B.fwd_bytes = bytes_b;
+            B.sc_bytes = 16.0 * double(soff) * nrhs;
             L.batches.push_back(B);
             scratch_rows = std::max(scratch_rows, soff);
             work_max = std::max(work_max, woff);
@@ -159,19 +169,28 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
     for (size_t li = 0; li < R; ++li) {
         auto& L = P.levels[li];
         for (auto& B : L.batches) {
-            launch_fwd_clusters(B.cl, B.ncl, B.edges, P.yv[li], P.scratch, nrhs, P.work, st);
+            {
+                ProfScope ps(K_SOLVE_FWD, B.fwd_flops, B.fwd_bytes);
+                launch_fwd_clusters(B.cl, B.ncl, B.edges, P.yv[li], P.scratch, nrhs, P.work, st);
+            }
+            ProfScope ps(K_SOLVE_SCATTER, 0.0, B.sc_bytes);
             launch_fwd_scatter(B.groups, B.ngroups, B.list, P.scratch, P.yv[li], nrhs, st);
         }
         double* next = (li + 1 < R) ? P.yv[li + 1] : P.ytop;
         launch_gather_rows(P.yv[li], L.up, L.up_n, nrhs, next, st);
     }
-    launch_top_solve(f.top_lu, f.top_piv, int(f.top_size), P.ytop, nrhs, P.work, st);
+    {
+        const double nt = double(f.top_size);
+        ProfScope ps(K_SOLVE_TOP, 2.0 * nt * nt * nrhs, 8.0 * nt * nt);
+        launch_top_solve(f.top_lu, f.top_piv, int(f.top_size), P.ytop, nrhs, P.work, st);
+    }
     for (size_t li = R; li-- > 0;) {
         auto& L = P.levels[li];
         const double* src = (li + 1 < R) ? P.yv[li + 1] : P.ytop;
         launch_scatter_rows(src, L.up, L.up_n, nrhs, P.yv[li], st);
         for (size_t bi = L.batches.size(); bi-- > 0;) {
             auto& B = L.batches[bi];
+            ProfScope ps(K_SOLVE_BWD, B.fwd_flops, B.fwd_bytes);
             launch_bwd_clusters(B.cl, B.ncl, B.edges, P.yv[li], nrhs, P.work, st);
         }
     }
