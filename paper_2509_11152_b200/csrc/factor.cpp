@@ -18,6 +18,7 @@
 // partial-pivot LU whose trailing updates run on the DMMA tile GEMM.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <numeric>
 #include <set>
@@ -253,6 +254,8 @@ class Factorizer {
     std::vector<int> mark_node;  // node-indexed batch membership stamp
     int stamp = 0;
 
+    void blocked_qr(const std::vector<QrTask>& tasks, Region& scr);
+    void jacobi_multi_cta(const std::vector<SvdTask>& tasks, Region& scr);
     std::unique_ptr<Lvl> leaf_level(int level);
     void attach_couplings(Lvl& L);
     void process_batch(Lvl& L, const std::vector<int>& batch);
@@ -262,6 +265,109 @@ class Factorizer {
     void top_factor(double* A, int64_t n);
     std::vector<std::pair<int, int>> dense_pairs(int level) const;
 };
+
+
+// R of QR(Z^T) for large n: blocked Householder, panels of BQR_NB columns
+// (bqr_panel) + split-K V^T M_trail (DMMA) + T^T reduction + trailing update
+// M_trail -= V W2 (DMMA).  All clusters of the batch advance together.
+void Factorizer::blocked_qr(const std::vector<QrTask>& tasks, Region& scr) {
+    cudaStream_t st = ctx().stream;
+    constexpr int KCH = 1024;
+    struct Q_ {
+        QrTask t;
+        int nref;
+        double *V, *T, *P, *W2;
+    };
+    std::vector<Q_> q;
+    int maxp = 0;
+    for (auto& t : tasks) {
+        Q_ x;
+        x.t = t;
+        x.nref = std::min(t.s, t.wf);
+        x.V = scr.alloc_n<double>(int64_t(BQR_NB) * t.wf);
+        x.T = scr.alloc_n<double>(BQR_NB * BQR_NB);
+        x.P = scr.alloc_n<double>(cdiv(t.wf, KCH) * BQR_NB * int64_t(t.s));
+        x.W2 = scr.alloc_n<double>(int64_t(BQR_NB) * t.s);
+        maxp = std::max<int>(maxp, int(cdiv(x.nref, BQR_NB)));
+        q.push_back(x);
+    }
+    for (int p = 0; p < maxp; ++p) {
+        std::vector<BqrPanelTask> pan;
+        std::vector<BqrReduceTask> red;
+        GemmBuild gk, gu;
+        int max_trail = 0;
+        for (auto& x : q) {
+            const int j0 = p * BQR_NB;
+            if (j0 >= x.nref) continue;
+            const int nbp = std::min(BQR_NB, x.nref - j0);
+            const int n = x.t.s, wf = x.t.wf, L = wf - j0;
+            pan.push_back(BqrPanelTask{x.t.Y, x.V, x.T, x.t.ldy, wf, j0, nbp, 0});
+            const int ntrail = n - (j0 + nbp);
+            if (ntrail <= 0) continue;
+            const int nch = int(cdiv(L, KCH));
+            double* Zt = x.t.Y + int64_t(j0 + nbp) * x.t.ldy + j0;
+            for (int ch = 0; ch < nch; ++ch) {
+                const int k = std::min(KCH, L - ch * KCH);
+                gk.add1(x.P + int64_t(ch) * BQR_NB * ntrail, ntrail, BQR_NB, ntrail, GEMM_STORE,
+                        contrib(x.V + int64_t(ch) * KCH, L, 0, Zt + int64_t(ch) * KCH, x.t.ldy, 1, k));
+            }
+            red.push_back(BqrReduceTask{x.P, x.T, x.W2, nch, ntrail});
+            max_trail = std::max(max_trail, ntrail);
+            gu.add1(Zt, x.t.ldy, ntrail, L, GEMM_ADD, contrib(x.W2, ntrail, 1, x.V, L, 0, nbp, -1.0));
+        }
+        if (pan.empty()) break;
+        launch_bqr_panel(upload(pan), int32_t(pan.size()), st);
+        gk.launch(-1);
+        if (!red.empty()) launch_bqr_reduce(upload(red), int32_t(red.size()), max_trail, st);
+        gu.launch(-1);
+    }
+    std::vector<RExtractTask> ex;
+    int maxn = 0;
+    for (auto& x : q) {
+        ex.push_back(RExtractTask{x.t.Y, x.t.R, x.t.ldy, x.nref, x.t.s});
+        maxn = std::max(maxn, x.t.s);
+    }
+    launch_r_extract(upload(ex), int32_t(ex.size()), maxn, st);
+}
+
+// Jacobi SVD for large n: several co-resident CTAs per cluster
+void Factorizer::jacobi_multi_cta(const std::vector<SvdTask>& tasks, Region& scr) {
+    cudaStream_t st = ctx().stream;
+    int sms = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    std::vector<int> want(tasks.size());
+    int total = 0;
+    for (size_t i = 0; i < tasks.size(); ++i) {
+        want[i] = std::max<int>(1, int(cdiv((tasks[i].m + 1) / 2, 16)));
+        total += want[i];
+    }
+    while (total > sms) {  // shrink the largest allocations until co-resident
+        auto it = std::max_element(want.begin(), want.end());
+        if (*it <= 1) break;
+        --*it;
+        --total;
+    }
+    if (total > sms) throw Error(H2F_E_INTERNAL, "assertion: too many clusters for the co-resident Jacobi");
+    uint32_t* bars = scr.alloc_n<uint32_t>(2 * tasks.size());
+    int32_t* flags = scr.alloc_n<int32_t>(64 * tasks.size());
+    H2F_CUDA(cudaMemsetAsync(bars, 0, sizeof(uint32_t) * 2 * tasks.size(), st));
+    H2F_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * 64 * tasks.size(), st));
+    std::vector<CoopSvdTask> ct;
+    std::vector<int32_t> owner;
+    int cta0 = 0;
+    for (size_t i = 0; i < tasks.size(); ++i) {
+        ct.push_back(CoopSvdTask{tasks[i], cta0, want[i], bars + 2 * i, flags + 64 * i});
+        for (int c = 0; c < want[i]; ++c) owner.push_back(int32_t(i));
+        cta0 += want[i];
+    }
+    auto* dct = upload(ct);
+    auto* down = upload(owner);
+    launch_jacobi_coop(dct, int32_t(owner.size()), down, drop, st);
+}
 
 std::vector<std::pair<int, int>> Factorizer::dense_pairs(int level) const {
     std::vector<std::pair<int, int>> out(M.inner[level]);
@@ -342,106 +448,155 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     auto in_batch = [&](int c) { return mark_node[c] == stamp; };
 
     // ------------------------------------------------------------- augment
+    // factorization.py:62-99, 377-407.  The fill row is projected onto the
+    // orthogonal complement of V first: Z = V_perp^T F has the singular values
+    // of (I - V V^T) F, so the QR/SVD work on (s-k) instead of s rows.
     clock.mark(PH_AUGMENT);
     std::vector<double*> Q(nb);
     int* kept_d = scr.alloc_n<int>(nb);
+    struct Aug {
+        int s, k, n, wf;
+        bool skip;
+        View V;
+        double *BT, *QV, *U;
+    };
+    std::vector<Aug> aug(nb);
     {
         CopyBuild gather;
-        GemmBuild g1, g2;
-        std::vector<QrTask> qr;
-        std::vector<SvdTask> svd;
-        std::vector<ComplementTask> cmp;
+        GemmBuild gz;
+        std::vector<ComplementTask> cmpV;
+        std::vector<QrTask> qr_small, qr_big;
+        std::vector<SvdTask> svd_small, svd_big;
+        int max_n_small = 1;
+        // H2F_SMALL_N_MAX (tests) lowers the shared-memory QR/SVD cut-off so
+        // the large-n (blocked QR, multi-CTA Jacobi) path runs on small inputs
+        int small_n_max = SMEM_DENSE_MAX_N;
+        if (const char* env = std::getenv("H2F_SMALL_N_MAX"))
+            small_n_max = std::min(SMEM_DENSE_MAX_N, std::atoi(env));
+        H2F_CUDA(cudaMemsetAsync(kept_d, 0, sizeof(int) * nb, st));
         for (int bi = 0; bi < nb; ++bi) {
             const int c = batch[bi], ci = L.at(c);
-            const int s = int(L.size[ci]);
-            const View V = L.basis[ci];
-            const int k = V.cols;
-            // fill row: F blocks in sorted key order (== sorted by partner id)
+            Aug& A = aug[bi];
+            A.s = int(L.size[ci]);
+            A.V = L.basis[ci];
+            A.k = A.V.cols;
+            A.n = A.s - A.k;
+            const int s = A.s, k = A.k, n = A.n;
             struct Part { View v; int trans; int w; };
             std::vector<Part> parts;
-            int wf = 0;
-            for (auto& kv : L.touch[ci]) {
+            A.wf = 0;
+            for (auto& kv : L.touch[ci]) {  // sorted key order == sorted partner id
                 if (kv.second.dense) continue;
                 const View& B = L.F.at(kv.second.key);
                 const bool row = key_a(kv.second.key) == c;
                 parts.push_back({B, row ? 0 : 1, row ? B.cols : B.rows});
-                wf += parts.back().w;
+                A.wf += parts.back().w;
             }
-            const bool skip = (wf == 0 || k == s);
-            const int m = skip ? 0 : std::min(s, wf);
-            double* R = scr.alloc_n<double>(int64_t(std::max(m, 1)) * s);
-            double* BT = scr.alloc_n<double>(int64_t(s) * s);
+            A.skip = (A.wf == 0 || k == s);
+            Q[bi] = F.store.alloc_n<double>(int64_t(s) * s);
+            A.BT = scr.alloc_n<double>(int64_t(s) * s);
+            A.QV = A.skip ? Q[bi] : scr.alloc_n<double>(int64_t(s) * s);
             double* Wc = scr.alloc_n<double>(int64_t(s) * s);
             double* cs = scr.alloc_n<double>(int64_t(16) * s);
-            Q[bi] = F.store.alloc_n<double>(int64_t(s) * s);
-            if (!skip) {
-                double* Y = scr.alloc_n<double>(int64_t(s) * wf);
-                int off = 0;
-                for (auto& p : parts) {
-                    gather.add(Y + off, wf, s, p.w, p.v.p, p.v.ld, p.trans, COPY_SET);
-                    off += p.w;
-                }
-                if (k > 0) {
-                    double* Cb = scr.alloc_n<double>(int64_t(k) * wf);
-                    g1.add1(Cb, wf, k, wf, GEMM_STORE, contrib(V.p, V.ld, 1, Y, wf, 0, s));
-                    g2.add1(Y, wf, s, wf, GEMM_ADD, contrib(V.p, V.ld, 0, Cb, wf, 0, k, -1.0));
-                }
-                qr.push_back(QrTask{Y, R, wf, s, wf});
+            // BT rows 0..k-1 = V^T ; complement of V -> QV = [V_perp | V]
+            gather.add(A.BT, s, k, s, A.V.p, A.V.ld, 1, COPY_SET);
+            cmpV.push_back(ComplementTask{A.BT, Wc, A.QV, cs, s, k});
+            if (A.skip) continue;
+            const int wf = A.wf;
+            double* Fb = scr.alloc_n<double>(int64_t(s) * wf);
+            int off = 0;
+            for (auto& p : parts) {
+                gather.add(Fb + off, wf, s, p.w, p.v.p, p.v.ld, p.trans, COPY_SET);
+                off += p.w;
             }
-            SvdTask sv{};
-            sv.R = R;
-            sv.V = V.p;
-            sv.BT = BT;
-            sv.ldv = V.ld;
-            sv.m = m;
-            sv.s = s;
-            sv.k = k;
-            sv.skip = skip ? 1 : 0;
-            sv.kept_out = kept_d + bi;
-            svd.push_back(sv);
-            ComplementTask ct{};
-            ct.BT = BT;
-            ct.W = Wc;
-            ct.Q = Q[bi];
-            ct.scratch = cs;
-            ct.kept = kept_d + bi;
-            ct.s = s;
-            ct.k = k;
-            cmp.push_back(ct);
+            double* Z = scr.alloc_n<double>(int64_t(n) * wf);
+            gz.add1(Z, wf, n, wf, GEMM_STORE, contrib(A.QV, s, 1, Fb, wf, 0, s));
+            double* R = scr.alloc_n<double>(int64_t(n) * n);
+            A.U = scr.alloc_n<double>(int64_t(n) * n);
+            const int m = std::min(n, wf);
+            SvdTask sv{R, A.U, m, n, kept_d + bi, 0};
+            if (n <= small_n_max) {
+                qr_small.push_back(QrTask{Z, R, wf, n, wf});
+                svd_small.push_back(sv);
+                max_n_small = std::max(max_n_small, n);
+            } else {
+                qr_big.push_back(QrTask{Z, R, wf, n, wf});
+                svd_big.push_back(sv);
+            }
         }
         gather.launch();
-        g1.launch(K_GEMM_AUG);
-        g2.launch(K_GEMM_AUG);
-        double qf = 0, qb = 0, jf = 0, jb = 0, cf = 0, cb = 0;
-        for (auto& t : qr) {
-            const double s = t.s, w = t.wf;
-            qf += 2.0 * w * s * s - (w >= s ? 2.0 / 3.0 * s * s * s : 0.0);
-            qb += 8.0 * s * w + 8.0 * s * s;
-        }
-        for (auto& t : svd) {
-            const double m = t.m, s = t.s;
-            jf += 22.0 * m * m * s;  // c_svd = 22 convention
-            jb += 16.0 * m * s;
-            cf += 4.0 * s * s * s;
-            cb += 16.0 * s * s;
-        }
-        {
-            ProfScope ps(K_QR, qf, qb);
-            if (!qr.empty()) launch_qr_r(upload(qr), int32_t(qr.size()), st);
-        }
-        {
-            ProfScope ps(K_JACOBI, jf, jb);
-            launch_jacobi(upload(svd), int32_t(svd.size()), drop, st);
+        double cf = 0, cb = 0;
+        for (auto& t : cmpV) {
+            cf += 4.0 * double(t.s) * t.s * t.s;
+            cb += 16.0 * double(t.s) * t.s;
         }
         {
             ProfScope ps(K_COMPLEMENT, cf, cb);
-            launch_complement(upload(cmp), int32_t(cmp.size()), st);
+            launch_complement(upload(cmpV), int32_t(cmpV.size()), st);
+        }
+        gz.launch(K_GEMM_AUG);
+        double qf = 0, qb = 0, jf = 0, jb = 0;
+        for (auto* v : {&qr_small, &qr_big})
+            for (auto& t : *v) {
+                const double n = t.s, w = t.wf;
+                qf += 2.0 * w * n * n - (w >= n ? 2.0 / 3.0 * n * n * n : 0.0);
+                qb += 8.0 * n * w + 8.0 * n * n;
+            }
+        for (auto* v : {&svd_small, &svd_big})
+            for (auto& t : *v) {
+                jf += 22.0 * double(t.m) * t.m * t.n;  // c_svd = 22 convention
+                jb += 16.0 * double(t.m) * t.n;
+            }
+        {
+            ProfScope ps(K_QR, qf, qb);
+            if (!qr_small.empty()) launch_qr_r_smem(upload(qr_small), int32_t(qr_small.size()), max_n_small, st);
+            if (!qr_big.empty()) blocked_qr(qr_big, scr);
+        }
+        {
+            ProfScope ps(K_JACOBI, jf, jb);
+            if (!svd_small.empty())
+                launch_jacobi_smem(upload(svd_small), int32_t(svd_small.size()), max_n_small, drop, st);
+            if (!svd_big.empty()) jacobi_multi_cta(svd_big, scr);
         }
     }
     int* kept_h = static_cast<int*>(X.pinned_buf(sizeof(int) * nb));
     H2F_CUDA(cudaMemcpyAsync(kept_h, kept_d, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
     X.sync();
     std::vector<int> kept(kept_h, kept_h + nb);
+    {
+        // b_aug = [V, V_perp U_kept] re-orthogonalised, then Q~ = [complement | b_aug]
+        CopyBuild keep;
+        GemmBuild gv;
+        std::vector<ReorthTask> ro;
+        std::vector<ComplementTask> cmp;
+        for (int bi = 0; bi < nb; ++bi) {
+            Aug& A = aug[bi];
+            if (A.skip) continue;
+            if (kept[bi] == 0) {
+                keep.add(Q[bi], A.s, A.s, A.s, A.QV, A.s, 0, COPY_SET);
+                continue;
+            }
+            const int s = A.s, k = A.k, n = A.n, kp = kept[bi];
+            gv.add1(A.BT + int64_t(k) * s, s, kp, s, GEMM_STORE, contrib(A.U, n, 0, A.QV, s, 1, n));
+            ro.push_back(ReorthTask{A.V.p, A.BT, scr.alloc_n<double>(int64_t(std::max(k, 1)) * kp), A.V.ld, s, k,
+                                    kp, 0});
+            cmp.push_back(ComplementTask{A.BT, scr.alloc_n<double>(int64_t(s) * s), Q[bi],
+                                         scr.alloc_n<double>(int64_t(16) * s), s, k + kp});
+        }
+        keep.launch();
+        gv.launch(K_GEMM_AUG);
+        double rf = 0, cf = 0, cb = 0;
+        for (auto& t : ro) rf += 4.0 * double(t.s) * t.k * t.kept;
+        for (auto& t : cmp) {
+            cf += 4.0 * double(t.s) * t.s * t.s;
+            cb += 16.0 * double(t.s) * t.s;
+        }
+        {
+            ProfScope ps(K_COMPLEMENT, rf + cf, cb);
+            if (!ro.empty()) launch_reorth(upload(ro), int32_t(ro.size()), st);
+            if (!cmp.empty()) launch_complement(upload(cmp), int32_t(cmp.size()), st);
+        }
+    }
     for (int bi = 0; bi < nb; ++bi) {
         const int c = batch[bi], ci = L.at(c);
         const int kt = L.k[ci] + kept[bi];

@@ -77,6 +77,59 @@ __global__ void __launch_bounds__(DT) qr_r_kernel(const QrTask* __restrict__ tas
     }
 }
 
+// ---- sequential TSQR in shared memory ---------------------------------------
+// R of the QR of Z^T (Z is n x wf, row-major): R (n x n) stays in shared
+// memory and absorbs Z^T 32 rows (= 32 columns of Z) at a time, one row per
+// lane, by Householder reflectors of length 33 on the stacked [R; chunk].
+constexpr int QB = 32;
+
+__global__ void __launch_bounds__(DT) qr_r_smem_kernel(const QrTask* __restrict__ tasks) {
+    const QrTask T = tasks[blockIdx.x];
+    extern __shared__ double sm[];
+    const int n = T.s, wf = T.wf;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = DT / 32;
+    double* R = sm;              // n x n
+    double* Cc = sm + n * n;     // chunk, column c at Cc[c*QB + i]
+    double* vt = Cc + n * QB;    // tau broadcast
+    for (int e = threadIdx.x; e < n * n; e += DT) R[e] = 0.0;
+    for (int col0 = 0; col0 < wf; col0 += QB) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < n * QB; e += DT) {
+            const int c = e / QB, i = e % QB;
+            Cc[e] = (col0 + i < wf) ? T.Y[(int64_t)c * T.ldy + col0 + i] : 0.0;
+        }
+        __syncthreads();
+        for (int j = 0; j < n; ++j) {
+            if (warp == 0) {
+                const double x = Cc[j * QB + lane];
+                const double ss = warp_sum(x * x);
+                double beta, tau, scal;
+                reflector(R[j * n + j], ss, beta, tau, scal);
+                if (tau != 0.0) Cc[j * QB + lane] = x * scal;
+                if (lane == 0) {
+                    R[j * n + j] = beta;
+                    vt[0] = tau;
+                }
+            }
+            __syncthreads();
+            const double tau = vt[0];
+            if (tau != 0.0) {
+                const double v = Cc[j * QB + lane];
+                for (int c = j + 1 + warp; c < n; c += nw) {
+                    const double y = Cc[c * QB + lane];
+                    double d = warp_sum(v * y) + R[j * n + c];
+                    d *= tau;
+                    Cc[c * QB + lane] = y - d * v;
+                    if (lane == 0) R[j * n + c] -= d;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += DT) T.R[e] = R[e];
+}
+
 // circle-method round robin: player list [0, rot...]; pair i of round st
 __device__ __forceinline__ void rr_pair(int i, int st, int mm, int& p, int& q) {
     auto pos = [&](int j) { return j == 0 ? 0 : 1 + ((j - 1 + st) % (mm - 1)); };
@@ -84,38 +137,23 @@ __device__ __forceinline__ void rr_pair(int i, int st, int mm, int& p, int& q) {
     q = pos(mm - 1 - i);
 }
 
-__global__ void __launch_bounds__(DT) jacobi_kernel(const SvdTask* __restrict__ tasks, double thresh) {
-    const SvdTask T = tasks[blockIdx.x];
-    extern __shared__ double dsh[];  // sig[m] then rank (int) [m]
-    __shared__ double sh[DT / 32];
-    __shared__ int rotated;
-    __shared__ int kept_s;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = DT / 32;
-    const int s = T.s, k = T.k, m = T.m;
-
-    // b_aug^T rows 0..k-1 = V^T
-    for (int64_t e = threadIdx.x; e < (int64_t)k * s; e += DT) {
-        const int l = (int)(e / s), i = (int)(e % s);
-        T.BT[(int64_t)l * s + i] = T.V[(int64_t)i * T.ldv + l];
-    }
-    if (T.skip || m == 0) {
-        if (threadIdx.x == 0) *T.kept_out = 0;
-        return;
-    }
-    const double tol = 2.220446049250313e-16 * sqrt((double)s);
+// one-sided (Hestenes) Jacobi on the m rows (length n) of A, in place
+__device__ void jacobi_sweeps(double* A, int m, int n, int* flag) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const double tol = 2.220446049250313e-16 * sqrt((double)n);
     const int mm = m + (m & 1);
     for (int sweep = 0; sweep < 60; ++sweep) {
-        if (threadIdx.x == 0) rotated = 0;
+        if (threadIdx.x == 0) *flag = 0;
         __syncthreads();
         for (int st = 0; st < mm - 1; ++st) {
             for (int pi = warp; pi < mm / 2; pi += nw) {
                 int p, q;
                 rr_pair(pi, st, mm, p, q);
                 if (p >= m || q >= m) continue;
-                double* rp = T.R + (int64_t)p * s;
-                double* rq = T.R + (int64_t)q * s;
+                double* rp = A + (int64_t)p * n;
+                double* rq = A + (int64_t)q * n;
                 double a = 0.0, b = 0.0, g = 0.0;
-                for (int i = lane; i < s; i += 32) {
+                for (int i = lane; i < n; i += 32) {
                     const double x = rp[i], y = rq[i];
                     a += x * x;
                     b += y * y;
@@ -128,73 +166,106 @@ __global__ void __launch_bounds__(DT) jacobi_kernel(const SvdTask* __restrict__ 
                     const double zeta = (b - a) / (2.0 * g);
                     const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                     const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
-                    for (int i = lane; i < s; i += 32) {
+                    for (int i = lane; i < n; i += 32) {
                         const double x = rp[i], y = rq[i];
                         rp[i] = c * x - sn * y;
                         rq[i] = sn * x + c * y;
                     }
-                    if (lane == 0) rotated = 1;
+                    if (lane == 0) *flag = 1;
                 }
             }
             __syncthreads();
         }
-        const int any = rotated;
+        const int any = *flag;
         __syncthreads();
         if (!any) break;
     }
-    double* sig = dsh;
-    int* rnk = reinterpret_cast<int*>(dsh + m);
+}
+
+// sigma = row norms, count sigma >= thresh, write the kept rows normalised in
+// descending sigma order (first index wins ties)
+__device__ void jacobi_finish(const double* A, int m, int n, double thresh, double* sig, int* rnk,
+                              int* kept_s, double* U, int* kept_out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int i = warp; i < m; i += nw) {
-        const double* ri = T.R + (int64_t)i * s;
+        const double* ri = A + (int64_t)i * n;
         double a = 0.0;
-        for (int c = lane; c < s; c += 32) a += ri[c] * ri[c];
+        for (int c = lane; c < n; c += 32) a += ri[c] * ri[c];
         a = warp_sum(a);
         if (lane == 0) sig[i] = sqrt(a);
     }
+    if (threadIdx.x == 0) *kept_s = 0;
     __syncthreads();
-    if (threadIdx.x == 0) kept_s = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < m; i += DT) {
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
         int r = 0;
         const double si = sig[i];
         for (int j = 0; j < m; ++j) r += (sig[j] > si) || (sig[j] == si && j < i);
         rnk[i] = r;
-        if (si >= thresh) atomicAdd(&kept_s, 1);
+        if (si >= thresh) atomicAdd(kept_s, 1);
     }
     __syncthreads();
-    const int kept = kept_s;
-    if (threadIdx.x == 0) *T.kept_out = kept;
-    if (kept == 0) return;
-    // pass 1: u_j = rotated row / sigma  -> BT rows k..k+kept-1
+    const int kept = *kept_s;
+    if (threadIdx.x == 0) *kept_out = kept;
     for (int i = warp; i < m; i += nw) {
         const int j = rnk[i];
         if (j >= kept) continue;
         const double inv = 1.0 / sig[i];
-        const double* ri = T.R + (int64_t)i * s;
-        double* dst = T.BT + (int64_t)(k + j) * s;
-        for (int c = lane; c < s; c += 32) dst[c] = ri[c] * inv;
+        const double* ri = A + (int64_t)i * n;
+        for (int c = lane; c < n; c += 32) U[(int64_t)j * n + c] = ri[c] * inv;
     }
+}
+
+__global__ void __launch_bounds__(DT) jacobi_kernel(const SvdTask* __restrict__ tasks, double thresh) {
+    const SvdTask T = tasks[blockIdx.x];
+    extern __shared__ double dsh[];  // sig[m] then rank (int) [m]
+    __shared__ int flag, kept_s;
+    if (T.m == 0) {
+        if (threadIdx.x == 0) *T.kept_out = 0;
+        return;
+    }
+    jacobi_sweeps(T.R, T.m, T.n, &flag);
+    jacobi_finish(T.R, T.m, T.n, thresh, dsh, reinterpret_cast<int*>(dsh + T.m), &kept_s, T.U, T.kept_out);
+}
+
+__global__ void __launch_bounds__(DT) jacobi_smem_kernel(const SvdTask* __restrict__ tasks, double thresh) {
+    const SvdTask T = tasks[blockIdx.x];
+    extern __shared__ double dsh[];  // A[m*n], sig[m], rank[m]
+    __shared__ int flag, kept_s;
+    const int m = T.m, n = T.n;
+    if (m == 0) {
+        if (threadIdx.x == 0) *T.kept_out = 0;
+        return;
+    }
+    double* A = dsh;
+    for (int e = threadIdx.x; e < m * n; e += DT) A[e] = T.R[e];
     __syncthreads();
-    // pass 2: C = V^T U (k x kept) stored in R (free now)
-    double* C = T.R;
+    jacobi_sweeps(A, m, n, &flag);
+    jacobi_finish(A, m, n, thresh, A + m * n, reinterpret_cast<int*>(A + m * n + m), &kept_s, T.U,
+                  T.kept_out);
+}
+
+// rows k..k+kept-1 of BT: re-orthogonalise against V and normalise
+// (factorization.py:82-84)
+__global__ void __launch_bounds__(DT) reorth_kernel(const ReorthTask* __restrict__ tasks) {
+    const ReorthTask T = tasks[blockIdx.x];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = DT / 32;
+    const int s = T.s, k = T.k, kept = T.kept;
     for (int64_t e = warp; e < (int64_t)k * kept; e += nw) {
         const int l = (int)(e / kept), j = (int)(e % kept);
         const double* u = T.BT + (int64_t)(k + j) * s;
         double d = 0.0;
         for (int i = lane; i < s; i += 32) d += T.V[(int64_t)i * T.ldv + l] * u[i];
         d = warp_sum(d);
-        if (lane == 0) C[e] = d;
+        if (lane == 0) T.C[e] = d;
     }
     __syncthreads();
-    // pass 3: u_j -= V C[:, j]
     for (int64_t e = threadIdx.x; e < (int64_t)kept * s; e += DT) {
         const int j = (int)(e / s), i = (int)(e % s);
         double d = 0.0;
-        for (int l = 0; l < k; ++l) d += T.V[(int64_t)i * T.ldv + l] * C[(int64_t)l * kept + j];
+        for (int l = 0; l < k; ++l) d += T.V[(int64_t)i * T.ldv + l] * T.C[(int64_t)l * kept + j];
         T.BT[(int64_t)(k + j) * s + i] -= d;
     }
     __syncthreads();
-    // pass 4: normalise columns
     for (int j = warp; j < kept; j += nw) {
         double* u = T.BT + (int64_t)(k + j) * s;
         double a = 0.0;
@@ -211,7 +282,7 @@ __global__ void __launch_bounds__(DT) complement_kernel(const ComplementTask* __
     __shared__ double sh[DT / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = DT / 32;
     const int s = T.s;
-    const int kt = T.k + *T.kept;
+    const int kt = T.kt;
     const int r = s - kt;
     for (int64_t e = threadIdx.x; e < (int64_t)kt * s; e += DT) T.W[e] = T.BT[e];
     __syncthreads();
@@ -263,6 +334,230 @@ __global__ void __launch_bounds__(DT) complement_kernel(const ComplementTask* __
     for (int64_t e = threadIdx.x; e < (int64_t)kt * s; e += DT) {
         const int c = (int)(e / s), row = (int)(e % s);
         T.Q[(int64_t)row * s + r + c] = T.BT[e];
+    }
+}
+
+// ---- blocked Householder QR (large n) --------------------------------------
+// Panel: factor columns j0..j0+nbp-1 of M = Z^T (rows of Z) in place, then
+// write the explicit reflectors V (unit lower, BQR_NB x L) and the compact-WY
+// factor T (LAPACK dlarft, forward/columnwise).  The trailing update
+// M_trail -= V (T^T (V^T M_trail)) runs on the DMMA tile GEMM.
+__global__ void __launch_bounds__(DT) bqr_panel_kernel(const BqrPanelTask* __restrict__ tasks) {
+    const BqrPanelTask T = tasks[blockIdx.x];
+    __shared__ double sh[DT / 32];
+    __shared__ double taus[BQR_NB];
+    __shared__ double G[BQR_NB][BQR_NB];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = DT / 32;
+    const int wf = T.wf, j0 = T.j0, nbp = T.nbp, L = wf - j0;
+    for (int jj = 0; jj < nbp; ++jj) {
+        const int j = j0 + jj;
+        double* zj = T.Z + (int64_t)j * T.ldz;
+        double ss = 0.0;
+        for (int i = j + 1 + threadIdx.x; i < wf; i += DT) ss += zj[i] * zj[i];
+        ss = block_sum(ss, sh);
+        double beta, tau, scal;
+        reflector(zj[j], ss, beta, tau, scal);
+        if (tau != 0.0)
+            for (int i = j + 1 + threadIdx.x; i < wf; i += DT) zj[i] *= scal;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            zj[j] = beta;
+            taus[jj] = tau;
+        }
+        if (tau != 0.0)
+            for (int c = jj + 1 + warp; c < nbp; c += nw) {
+                double* zc = T.Z + (int64_t)(j0 + c) * T.ldz;
+                double d = 0.0;
+                for (int i = j + 1 + lane; i < wf; i += 32) d += zj[i] * zc[i];
+                d = (warp_sum(d) + zc[j]) * tau;
+                for (int i = j + 1 + lane; i < wf; i += 32) zc[i] -= d * zj[i];
+                __syncwarp();
+                if (lane == 0) zc[j] -= d;
+            }
+        __syncthreads();
+    }
+    // explicit V
+    for (int64_t e = threadIdx.x; e < (int64_t)BQR_NB * L; e += DT) {
+        const int jj = (int)(e / L), ip = (int)(e % L);
+        const int i = j0 + ip, j = j0 + jj;
+        double v = 0.0;
+        if (jj < nbp) v = (i < j) ? 0.0 : (i == j ? 1.0 : T.Z[(int64_t)j * T.ldz + i]);
+        T.V[e] = v;
+    }
+    __syncthreads();
+    // Gram V V^T (warp a computes row a)
+    if (warp < BQR_NB) {
+        const int a = warp;
+        double acc[BQR_NB];
+#pragma unroll
+        for (int b = 0; b < BQR_NB; ++b) acc[b] = 0.0;
+        const double* va = T.V + (int64_t)a * L;
+        for (int ip = lane; ip < L; ip += 32) {
+            const double x = va[ip];
+#pragma unroll
+            for (int b = 0; b < BQR_NB; ++b) acc[b] += x * T.V[(int64_t)b * L + ip];
+        }
+#pragma unroll
+        for (int b = 0; b < BQR_NB; ++b) {
+            const double g = warp_sum(acc[b]);
+            if (lane == 0) G[a][b] = g;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double Tm[BQR_NB][BQR_NB];
+        for (int a = 0; a < BQR_NB; ++a)
+            for (int b = 0; b < BQR_NB; ++b) Tm[a][b] = 0.0;
+        for (int jj = 0; jj < nbp; ++jj) {
+            const double tau = taus[jj];
+            double tmp[BQR_NB];
+            for (int a = 0; a < jj; ++a) tmp[a] = -tau * G[a][jj];
+            for (int a = 0; a < jj; ++a) {
+                double acc = 0.0;
+                for (int b = a; b < jj; ++b) acc += Tm[a][b] * tmp[b];
+                Tm[a][jj] = acc;
+            }
+            Tm[jj][jj] = tau;
+        }
+        for (int a = 0; a < BQR_NB; ++a)
+            for (int b = 0; b < BQR_NB; ++b) T.T[a * BQR_NB + b] = Tm[a][b];
+    }
+}
+
+// W2[a][c] = sum_b T[b][a] * (sum_chunks P[chunk][b][c])
+__global__ void bqr_reduce_kernel(const BqrReduceTask* __restrict__ tasks) {
+    const BqrReduceTask R = tasks[blockIdx.y];
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= R.ntrail) return;
+    double S[BQR_NB];
+#pragma unroll
+    for (int b = 0; b < BQR_NB; ++b) S[b] = 0.0;
+    for (int ch = 0; ch < R.nchunks; ++ch) {
+        const double* P = R.P + (int64_t)ch * BQR_NB * R.ntrail;
+#pragma unroll
+        for (int b = 0; b < BQR_NB; ++b) S[b] += P[(int64_t)b * R.ntrail + c];
+    }
+#pragma unroll
+    for (int a = 0; a < BQR_NB; ++a) {
+        double acc = 0.0;
+#pragma unroll
+        for (int b = 0; b <= a; ++b) acc += R.T[b * BQR_NB + a] * S[b];
+        R.W2[(int64_t)a * R.ntrail + c] = acc;
+    }
+}
+
+__global__ void r_extract_kernel(const RExtractTask* __restrict__ tasks) {
+    const RExtractTask X = tasks[blockIdx.y];
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)X.n * X.n) return;
+    const int j = (int)(e / X.n), c = (int)(e % X.n);
+    X.R[e] = (j < X.m && c >= j) ? X.Z[(int64_t)c * X.ldz + j] : 0.0;
+}
+
+// ---- multi-CTA Jacobi (large n) ---------------------------------------------
+// CTAs [cta0, cta0+ncta) of the grid own one cluster; each round-robin step's
+// pairs are spread over all their warps, with a global-memory barrier between
+// steps.  Loads/stores bypass L1 (other SMs write the rows).
+__device__ __forceinline__ void cta_group_barrier(uint32_t* bar, int nct) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile uint32_t* gen = bar + 1;
+        const uint32_t g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == uint32_t(nct - 1)) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(DT) jacobi_coop_kernel(const CoopSvdTask* __restrict__ tasks,
+                                                        const int* __restrict__ cta_task, double thresh) {
+    const CoopSvdTask CT = tasks[cta_task[blockIdx.x]];
+    const int rank = blockIdx.x - CT.cta0, nct = CT.ncta;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = DT / 32;
+    const int m = CT.t.m, n = CT.t.n;
+    double* A = CT.t.R;
+    extern __shared__ double dsh[];
+    __shared__ int kept_s;
+    if (m == 0) {
+        if (rank == 0 && threadIdx.x == 0) *CT.t.kept_out = 0;
+        return;
+    }
+    const double tol = 2.220446049250313e-16 * sqrt((double)n);
+    const int mm = m + (m & 1);
+    const int gw = rank * nw + warp, gnw = nct * nw;
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        for (int st = 0; st < mm - 1; ++st) {
+            for (int pi = gw; pi < mm / 2; pi += gnw) {
+                int p, q;
+                rr_pair(pi, st, mm, p, q);
+                if (p >= m || q >= m) continue;
+                double* rp = A + (int64_t)p * n;
+                double* rq = A + (int64_t)q * n;
+                double a = 0.0, b = 0.0, g = 0.0;
+                for (int i = lane; i < n; i += 32) {
+                    const double x = __ldcg(rp + i), y = __ldcg(rq + i);
+                    a += x * x;
+                    b += y * y;
+                    g += x * y;
+                }
+                a = warp_sum(a);
+                b = warp_sum(b);
+                g = warp_sum(g);
+                if (g != 0.0 && a > 0.0 && b > 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b)) {
+                    const double zeta = (b - a) / (2.0 * g);
+                    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                    const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+                    for (int i = lane; i < n; i += 32) {
+                        const double x = __ldcg(rp + i), y = __ldcg(rq + i);
+                        __stcg(rp + i, c * x - sn * y);
+                        __stcg(rq + i, sn * x + c * y);
+                    }
+                    if (lane == 0) CT.flags[sweep] = 1;
+                }
+            }
+            cta_group_barrier(CT.bar, nct);
+        }
+        const int any = *(volatile int*)(CT.flags + sweep);
+        if (!any) break;
+    }
+    if (rank != 0) return;
+    double* sig = dsh;
+    int* rnk = reinterpret_cast<int*>(dsh + m);
+    for (int i = warp; i < m; i += nw) {
+        const double* ri = A + (int64_t)i * n;
+        double a = 0.0;
+        for (int c = lane; c < n; c += 32) {
+            const double x = __ldcg(ri + c);
+            a += x * x;
+        }
+        a = warp_sum(a);
+        if (lane == 0) sig[i] = sqrt(a);
+    }
+    if (threadIdx.x == 0) kept_s = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += DT) {
+        int r = 0;
+        const double si = sig[i];
+        for (int j = 0; j < m; ++j) r += (sig[j] > si) || (sig[j] == si && j < i);
+        rnk[i] = r;
+        if (si >= thresh) atomicAdd(&kept_s, 1);
+    }
+    __syncthreads();
+    const int kept = kept_s;
+    if (threadIdx.x == 0) *CT.t.kept_out = kept;
+    for (int i = warp; i < m; i += nw) {
+        const int j = rnk[i];
+        if (j >= kept) continue;
+        const double inv = 1.0 / sig[i];
+        const double* ri = A + (int64_t)i * n;
+        for (int c = lane; c < n; c += 32) CT.t.U[(int64_t)j * n + c] = __ldcg(ri + c) * inv;
     }
 }
 
@@ -478,27 +773,73 @@ void launch_qr_r(const QrTask* d_tasks, int32_t ntasks, cudaStream_t st) {
     count_launch();
 }
 
+void launch_qr_r_smem(const QrTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st) {
+    if (ntasks <= 0) return;
+    const size_t smem = sizeof(double) * (size_t(max_n) * max_n + size_t(max_n) * QB + 8);
+    cudaFuncSetAttribute(qr_r_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    qr_r_smem_kernel<<<ntasks, DT, smem, st>>>(d_tasks);
+    count_launch();
+}
+
 void launch_jacobi(const SvdTask* d_tasks, int32_t ntasks, double thresh, cudaStream_t st) {
     if (ntasks <= 0) return;
-    // sig[m] + rank[m] with m <= 2048
-    const size_t smem = 2048 * (sizeof(double) + sizeof(int));
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    const size_t smem = 4096 * (sizeof(double) + sizeof(int));  // sig + rank, m <= 4096
+    cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     jacobi_kernel<<<ntasks, DT, smem, st>>>(d_tasks, thresh);
+    count_launch();
+}
+
+void launch_jacobi_smem(const SvdTask* d_tasks, int32_t ntasks, int32_t max_n, double thresh,
+                        cudaStream_t st) {
+    if (ntasks <= 0) return;
+    const size_t smem = sizeof(double) * (size_t(max_n) * max_n + max_n) + sizeof(int) * max_n + 64;
+    cudaFuncSetAttribute(jacobi_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    jacobi_smem_kernel<<<ntasks, DT, smem, st>>>(d_tasks, thresh);
+    count_launch();
+}
+
+void launch_reorth(const ReorthTask* d_tasks, int32_t ntasks, cudaStream_t st) {
+    if (ntasks <= 0) return;
+    reorth_kernel<<<ntasks, DT, 0, st>>>(d_tasks);
+    count_launch();
+}
+
+void launch_bqr_panel(const BqrPanelTask* d_tasks, int32_t ntasks, cudaStream_t st) {
+    if (ntasks <= 0) return;
+    bqr_panel_kernel<<<ntasks, DT, 0, st>>>(d_tasks);
+    count_launch();
+}
+
+void launch_bqr_reduce(const BqrReduceTask* d_tasks, int32_t ntasks, int32_t max_ntrail, cudaStream_t st) {
+    if (ntasks <= 0 || max_ntrail <= 0) return;
+    dim3 grid((max_ntrail + 127) / 128, ntasks);
+    bqr_reduce_kernel<<<grid, 128, 0, st>>>(d_tasks);
+    count_launch();
+}
+
+void launch_r_extract(const RExtractTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st) {
+    if (ntasks <= 0) return;
+    dim3 grid((unsigned)(((int64_t)max_n * max_n + 255) / 256), ntasks);
+    r_extract_kernel<<<grid, 256, 0, st>>>(d_tasks);
+    count_launch();
+}
+
+void launch_jacobi_coop(const CoopSvdTask* d_tasks, int32_t total_ctas, const int32_t* d_cta_task,
+                        double thresh, cudaStream_t st) {
+    if (total_ctas <= 0) return;
+    const size_t smem = 4096 * (sizeof(double) + sizeof(int));
+    cudaFuncSetAttribute(jacobi_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    void* args[] = {(void*)&d_tasks, (void*)&d_cta_task, (void*)&thresh};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)jacobi_coop_kernel, dim3(total_ctas), dim3(DT),
+                                                args, smem, st);
+    if (e != cudaSuccess) jacobi_coop_kernel<<<total_ctas, DT, smem, st>>>(d_tasks, d_cta_task, thresh);
     count_launch();
 }
 
 void launch_complement(const ComplementTask* d_tasks, int32_t ntasks, cudaStream_t st) {
     if (ntasks <= 0) return;
-    const size_t smem = 2048 * sizeof(double);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(complement_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
+    const size_t smem = 4096 * sizeof(double);
+    cudaFuncSetAttribute(complement_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     complement_kernel<<<ntasks, DT, smem, st>>>(d_tasks);
     count_launch();
 }

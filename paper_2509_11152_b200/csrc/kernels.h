@@ -63,23 +63,62 @@ struct QrTask {          // R of the reduced QR of Y^T, Y is s x wf (row-major, 
     int32_t s, wf;
 };
 
-struct SvdTask {         // one-sided Jacobi on the rows of R (m x s), then
-    double* R;           // writes b_aug^T = [V^T ; vbar^T] ((k+kept) x s) to BT
-    const double* V;     // s x k basis, row-major ld = ldv
-    double* BT;
-    int64_t ldv;
-    int32_t m, s, k;
-    int32_t skip;        // 1: no fill row -> kept = 0 without touching R
+struct SvdTask {         // one-sided Jacobi on the rows of R (m x n, ld n): writes the
+    double* R;           // left singular vectors u_j (length n) of R^T with
+    double* U;           // sigma_j >= thresh as rows of U, sorted by sigma desc
+    int32_t m, n;
     int32_t* kept_out;   // device int
+    int32_t pad_;
 };
 
-struct ComplementTask {  // Q~ = [complement | b_aug] from BT (kt x s)
+struct ReorthTask {      // rows k..k+kept-1 of BT: u -= V (V^T u); u /= |u|
+    const double* V;     // s x k, row-major ld = ldv
+    double* BT;          // (k+kept) x s
+    double* C;           // k x kept scratch
+    int64_t ldv;
+    int32_t s, k, kept;
+    int32_t pad_;
+};
+
+struct ComplementTask {  // Q~ = [complement | b_aug] from BT (kt x s rows = columns of b_aug)
     const double* BT;    // kt x s, row-major ld = s
     double* W;           // kt x s workspace (Householder vectors)
-    double* Q;           // s x s row-major (factor storage)
-    double* scratch;     // 32 * s per CTA warp workspace
-    const int32_t* kept; // device kept count; kt = k + *kept
-    int32_t s, k;
+    double* Q;           // s x s row-major
+    double* scratch;     // 16 * s warp workspace
+    int32_t s, kt;
+};
+
+// blocked Householder QR of M = Z^T (Z is n x wf row-major), panel of BQR_NB
+// columns = BQR_NB rows of Z.  The panel kernel factors the panel in place and
+// writes V (explicit unit-lower, nbp x L, L = wf - j0) and T (BQR_NB^2, upper).
+constexpr int BQR_NB = 16;
+struct BqrPanelTask {
+    double* Z;           // n x wf, ld = ldz
+    double* V;           // BQR_NB x L (ld L)
+    double* T;           // BQR_NB x BQR_NB
+    int64_t ldz;
+    int32_t wf, j0, nbp, pad_;
+};
+
+struct BqrReduceTask {   // W2 = T^T * sum_c P_c  (BQR_NB x ntrail)
+    const double* P;     // nchunks x (BQR_NB x ntrail)
+    const double* T;
+    double* W2;
+    int32_t nchunks, ntrail;
+};
+
+struct RExtractTask {    // R[j][c] = c >= j ? Z[c][j] : 0  (j < m, c < n)
+    const double* Z;
+    double* R;           // n x n
+    int64_t ldz;
+    int32_t m, n;
+};
+
+struct CoopSvdTask {     // multi-CTA Jacobi: CTAs [cta0, cta0+ncta) own one cluster
+    SvdTask t;
+    int32_t cta0, ncta;
+    uint32_t* bar;       // [2] barrier counter + generation
+    int32_t* flags;      // [64] per-sweep rotation flags (zeroed)
 };
 
 struct LuTask {          // partial-pivot LU of the r x r view of D_cc
@@ -154,7 +193,16 @@ void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
 void launch_copy_tasks(const CopyTask* d_tasks, const int64_t* d_tile_start, int32_t ntasks,
                        int64_t ntiles, cudaStream_t st);
 void launch_qr_r(const QrTask* d_tasks, int32_t ntasks, cudaStream_t st);
+void launch_qr_r_smem(const QrTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st);
 void launch_jacobi(const SvdTask* d_tasks, int32_t ntasks, double thresh, cudaStream_t st);
+void launch_jacobi_smem(const SvdTask* d_tasks, int32_t ntasks, int32_t max_n, double thresh, cudaStream_t st);
+void launch_reorth(const ReorthTask* d_tasks, int32_t ntasks, cudaStream_t st);
+void launch_bqr_panel(const BqrPanelTask* d_tasks, int32_t ntasks, cudaStream_t st);
+void launch_bqr_reduce(const BqrReduceTask* d_tasks, int32_t ntasks, int32_t max_ntrail, cudaStream_t st);
+void launch_r_extract(const RExtractTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st);
+void launch_jacobi_coop(const CoopSvdTask* d_tasks, int32_t total_ctas, const int32_t* d_cta_task,
+                        double thresh, cudaStream_t st);
+constexpr int SMEM_DENSE_MAX_N = 144;  // n x n doubles resident in shared memory
 void launch_complement(const ComplementTask* d_tasks, int32_t ntasks, cudaStream_t st);
 void launch_lu(const LuTask* d_tasks, int32_t ntasks, cudaStream_t st);
 void launch_trsm(const TrsmTask* d_tasks, int32_t ntasks, cudaStream_t st);

@@ -188,7 +188,7 @@ cudaEvent_t Profiler::get_event() {
 }
 
 int Profiler::begin(int kid, double flops, double bytes) {
-    if (!on) return -1;
+    if (!on || kid < 0) return -1;
     Rec r{kid, get_event(), get_event(), flops, bytes};
     H2F_CUDA(cudaEventRecord(r.a, ctx().stream));
     pending_.push_back(r);

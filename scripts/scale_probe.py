@@ -18,9 +18,11 @@ for item in cases:
     t0 = time.perf_counter()
     fac = H.factorize(h2, prm["eps_lu"])
     tf = time.perf_counter() - t0
+    _lib.profile_enable(True); _lib.profile_reset()
     t0 = time.perf_counter()
     fac2 = H.factorize(h2, prm["eps_lu"])
     tf2 = time.perf_counter() - t0
+    prof = _lib.profile_get(); _lib.profile_enable(False)
     x_ref = np.random.Generator(np.random.Philox(7)).standard_normal(n)
     b = H.matvec(h2, x_ref)
     t0 = time.perf_counter()
@@ -36,4 +38,6 @@ for item in cases:
         "batches": sum(r.nbatches for r in fac2.records),
         "phases": {k: round(v, 4) for k, v in fac2.phase_seconds.items()},
         "levels": [(r.level, round(r.time_s, 4), r.nbatches, r.max_rank) for r in fac2.records],
-        "mem": _lib.memory_stats()}), flush=True)
+        "mem": _lib.memory_stats(),
+        "kernels": {k: [round(v["seconds"], 4), v["launches"], round(v["flops"] / max(v["seconds"], 1e-12) / 1e9, 1)]
+                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["seconds"])}}), flush=True)

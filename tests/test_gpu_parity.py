@@ -189,3 +189,23 @@ def test_factorize_bitwise_deterministic():
     r1, r2 = f1.records[0], f2.records[0]
     c = r1.clusters[0]
     assert np.array_equal(r1.factors[c].q, r2.factors[c].q)
+
+
+@pytest.mark.parametrize("case", ["cov2d_4096", "cov3d_2048", "laplace3d_4096"])
+def test_large_n_path_matches_shared_memory_path(case, monkeypatch):
+    """Force the blocked-Householder QR + multi-CTA Jacobi (used for n > 144
+    at upper levels of large problems) on small inputs and compare with the
+    shared-memory path: same integer structure, same solution."""
+    g = load(case)
+    _, _, _, h2, prm = problem(case)
+    monkeypatch.setenv("H2F_SMALL_N_MAX", "8")
+    fac_big = H.factorize(h2, prm["eps_lu"])
+    monkeypatch.delenv("H2F_SMALL_N_MAX")
+    _, _, fac = gpu_factor(case)
+    assert structure_of(fac_big) == structure_of(fac)
+    b = rhs(h2, H.matvec)
+    x1 = H.refined_solve(h2, fac_big, b)
+    x2 = H.refined_solve(h2, fac, b)
+    assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x2)
+    if case != "laplace3d_4096":
+        assert structure_of(fac_big) == golden_structure(g)
