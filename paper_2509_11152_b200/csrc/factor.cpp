@@ -465,7 +465,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         CopyBuild gather;
         GemmBuild gz;
         std::vector<ComplementTask> cmpV;
-        std::vector<QrTask> qr_small, qr_big;
+        std::vector<QrTask> qr_small, qr_big, qr_seg;
         std::vector<SvdTask> svd_small, svd_big;
         int max_n_small = 1;
         // H2F_SMALL_N_MAX (tests) lowers the shared-memory QR/SVD cut-off so
@@ -516,11 +516,24 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             const int m = std::min(n, wf);
             SvdTask sv{R, A.U, m, n, kept_d + bi, 0};
             if (n <= small_n_max) {
-                qr_small.push_back(QrTask{Z, R, wf, n, wf});
+                // two-level TSQR: segments of <= seg columns fold into
+                // their own R (written transposed side by side), then one
+                // CTA folds the stacked R's
+                const int seg = std::max(256, 4 * n);
+                const int nseg = int(cdiv(wf, seg));
+                if (nseg > 1) {
+                    double* ST = scr.alloc_n<double>(int64_t(n) * nseg * n);
+                    for (int sg = 0; sg < nseg; ++sg)
+                        qr_seg.push_back(QrTask{Z, ST + int64_t(sg) * n, wf, n, wf, sg * seg,
+                                                std::min(wf, (sg + 1) * seg), int64_t(nseg) * n});
+                    qr_small.push_back(QrTask{ST, R, int64_t(nseg) * n, n, nseg * n, 0, nseg * n, 0});
+                } else {
+                    qr_small.push_back(QrTask{Z, R, wf, n, wf, 0, wf, 0});
+                }
                 svd_small.push_back(sv);
                 max_n_small = std::max(max_n_small, n);
             } else {
-                qr_big.push_back(QrTask{Z, R, wf, n, wf});
+                qr_big.push_back(QrTask{Z, R, wf, n, wf, 0, wf, 0});
                 svd_big.push_back(sv);
             }
         }
@@ -549,6 +562,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             }
         {
             ProfScope ps(K_QR, qf, qb);
+            if (!qr_seg.empty()) launch_qr_r_smem(upload(qr_seg), int32_t(qr_seg.size()), max_n_small, st);
             if (!qr_small.empty()) launch_qr_r_smem(upload(qr_small), int32_t(qr_small.size()), max_n_small, st);
             if (!qr_big.empty()) blocked_qr(qr_big, scr);
         }

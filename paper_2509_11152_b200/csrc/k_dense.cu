@@ -86,13 +86,13 @@ constexpr int QB = 32;
 __global__ void __launch_bounds__(DT) qr_r_smem_kernel(const QrTask* __restrict__ tasks) {
     const QrTask T = tasks[blockIdx.x];
     extern __shared__ double sm[];
-    const int n = T.s, wf = T.wf;
+    const int n = T.s, wf = T.c1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = DT / 32;
     double* R = sm;              // n x n
     double* Cc = sm + n * n;     // chunk, column c at Cc[c*QB + i]
     double* vt = Cc + n * QB;    // tau broadcast
     for (int e = threadIdx.x; e < n * n; e += DT) R[e] = 0.0;
-    for (int col0 = 0; col0 < wf; col0 += QB) {
+    for (int col0 = T.c0; col0 < wf; col0 += QB) {
         __syncthreads();
         for (int e = threadIdx.x; e < n * QB; e += DT) {
             const int c = e / QB, i = e % QB;
@@ -127,7 +127,14 @@ __global__ void __launch_bounds__(DT) qr_r_smem_kernel(const QrTask* __restrict_
         }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < n * n; e += DT) T.R[e] = R[e];
+    if (T.ldrt > 0) {
+        for (int e = threadIdx.x; e < n * n; e += DT) {
+            const int j = e / n, c = e % n;
+            T.R[(int64_t)c * T.ldrt + j] = R[e];
+        }
+    } else {
+        for (int e = threadIdx.x; e < n * n; e += DT) T.R[e] = R[e];
+    }
 }
 
 // circle-method round robin: player list [0, rot...]; pair i of round st

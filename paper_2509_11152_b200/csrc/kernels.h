@@ -57,10 +57,14 @@ constexpr int COPY_TILE = 32;
 
 // ---- per-cluster dense kernels ------------------------------------------------
 struct QrTask {          // R of the reduced QR of Y^T, Y is s x wf (row-major, ld)
-    double* Y;           // overwritten
+    double* Y;           // overwritten (global path) / read (smem path)
     double* R;           // min(s,wf) x s, row-major, ld = s
     int64_t ldy;
     int32_t s, wf;
+    // smem path only: fold columns [c0, c1) of Y; if ldrt > 0 write R^T to
+    // R + c*ldrt + j (the stacked-R input of a second TSQR level)
+    int32_t c0, c1;
+    int64_t ldrt;
 };
 
 struct SvdTask {         // one-sided Jacobi on the rows of R (m x n, ld n): writes the
