@@ -18,6 +18,7 @@
 // partial-pivot LU whose trailing updates run on the DMMA tile GEMM.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <numeric>
@@ -36,6 +37,7 @@ struct View {
     double* p = nullptr;
     int64_t ld = 0;
     int rows = 0, cols = 0;
+    int stamp = 0, tidx = -1;  // Schur-target slot of the current batch
 };
 
 struct CouplingW {    // coupling block with logical zero padding (factorization.py:396-403)
@@ -54,6 +56,29 @@ struct TransferW {    // transfer with logical zero rows (factorization.py:404-4
 struct Entry {
     Key key;
     bool dense;
+    View* v;  // the block itself (std::map nodes are stable)
+};
+
+// neighbour list of one cluster: flat, sorted by partner id (the order the
+// reference's sorted neighbour entries follow)
+class Nbrs {
+  public:
+    using Item = std::pair<int, Entry>;
+    void set(int o, const Entry& e) {
+        auto it = std::lower_bound(v_.begin(), v_.end(), o, [](const Item& a, int b) { return a.first < b; });
+        if (it != v_.end() && it->first == o) it->second = e;
+        else v_.insert(it, {o, e});
+    }
+    const Entry* find(int o) const {
+        auto it = std::lower_bound(v_.begin(), v_.end(), o, [](const Item& a, int b) { return a.first < b; });
+        return (it != v_.end() && it->first == o) ? &it->second : nullptr;
+    }
+    std::vector<Item>::const_iterator begin() const { return v_.begin(); }
+    std::vector<Item>::const_iterator end() const { return v_.end(); }
+    size_t size() const { return v_.size(); }
+
+  private:
+    std::vector<Item> v_;
 };
 
 struct Lvl {
@@ -65,7 +90,8 @@ struct Lvl {
     std::vector<char> done;
     std::vector<View> basis;
     std::map<Key, View> D, F;
-    std::vector<std::map<int, Entry>> touch;
+    std::vector<View*> diag;  // D(c, c) per position
+    std::vector<Nbrs> touch;
     std::unordered_map<Key, CouplingW> S;
     std::vector<TransferW> T;
     Region mem{size_t(256) << 20};
@@ -74,8 +100,9 @@ struct Lvl {
 
     int at(int c) const { return pos.at(c); }
     void link(Key key, bool dense) {
-        touch[at(key_a(key))][key_b(key)] = {key, dense};
-        touch[at(key_b(key))][key_a(key)] = {key, dense};
+        View* v = &block(key, dense);
+        touch[at(key_a(key))].set(key_b(key), {key, dense, v});
+        touch[at(key_b(key))].set(key_a(key), {key, dense, v});
     }
     View& block(Key key, bool dense) { return dense ? D.at(key) : F.at(key); }
     View* find(Key key) {
@@ -94,13 +121,19 @@ struct Lvl {
         done.assign(n, 0);
         basis.assign(n, {});
         touch.assign(n, {});
+        diag.assign(n, nullptr);
         T.assign(n, {});
         factors.assign(n, {});
     }
     void build_touch() {
         for (auto& kv : D)
             if (key_a(kv.first) != key_b(kv.first)) link(kv.first, true);
+            else diag[at(key_a(kv.first))] = &kv.second;
         for (auto& kv : F) link(kv.first, false);
+    }
+    View& dcc(int ci) {
+        if (!diag[ci]) throw Error(H2F_E_INTERNAL, "assertion: cluster without a diagonal block");
+        return *diag[ci];
     }
 };
 
@@ -253,6 +286,12 @@ class Factorizer {
     std::vector<size_t> level_marks;
     std::vector<int> mark_node;  // node-indexed batch membership stamp
     int stamp = 0;
+    int target_stamp = 0;
+    bool level_prof = false;
+    FILE* aug_log = nullptr;  // H2F_AUG_LOG=path: per-cluster augmentation shapes (development aid)
+    double level_prev[K_COUNT] = {};
+    std::chrono::steady_clock::time_point level_t0;
+    void dump_level_profile(int level);
 
     void blocked_qr(const std::vector<QrTask>& tasks, Region& scr);
     void jacobi_multi_cta(const std::vector<SvdTask>& tasks, Region& scr);
@@ -487,7 +526,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             A.wf = 0;
             for (auto& kv : L.touch[ci]) {  // sorted key order == sorted partner id
                 if (kv.second.dense) continue;
-                const View& B = L.F.at(kv.second.key);
+                const View& B = *kv.second.v;
                 const bool row = key_a(kv.second.key) == c;
                 parts.push_back({B, row ? 0 : 1, row ? B.cols : B.rows});
                 A.wf += parts.back().w;
@@ -577,6 +616,11 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     H2F_CUDA(cudaMemcpyAsync(kept_h, kept_d, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
     X.sync();
     std::vector<int> kept(kept_h, kept_h + nb);
+    if (aug_log) {
+        for (int bi = 0; bi < nb; ++bi)
+            std::fprintf(aug_log, "%d %d %d %d %d %d %d %d\n", L.level, batch_counter, nb, aug[bi].s, aug[bi].k,
+                         aug[bi].wf, kept[bi], aug[bi].skip ? 1 : 0);
+    }
     {
         // b_aug = [V, V_perp U_kept] re-orthogonalised, then Q~ = [complement | b_aug]
         CopyBuild keep;
@@ -697,7 +741,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             for (auto& kv : L.touch[ci]) {
                 e.ids.push_back(kv.first);
                 e.ents.push_back(kv.second);
-                const View& B = L.block(kv.second.key, kv.second.dense);
+                const View& B = *kv.second.v;
                 e.widths.push_back(key_a(kv.second.key) == c ? B.cols : B.rows);
             }
             e.np = int(e.ids.size());
@@ -708,12 +752,12 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             e.MW = F.store.alloc_n<double>(int64_t(r) * e.W);
             cf.lu = F.store.alloc_n<double>(int64_t(r) * r);
             cf.piv = F.store.alloc_n<int32_t>(r);
-            const View& Dcc = L.D.at(mkkey(c, c));
+            const View& Dcc = L.dcc(ci);
             // panel 0: d_cc[:r, r:]
             panels.add(e.G, e.W, r, kt, Dcc.p + r, Dcc.ld, 0, COPY_SET);
             for (int i = 1; i < e.np; ++i) {
                 const Entry& en = e.ents[i - 1];
-                const View& B = L.block(en.key, en.dense);
+                const View& B = *en.v;
                 if (key_a(en.key) == c)
                     panels.add(e.G + e.offs[i], e.W, r, B.cols, B.p, B.ld, 0, COPY_SET);
                 else
@@ -770,12 +814,14 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     }
 
     // Schur updates (factorization.py:122-126) fused with the scatter into the
-    // target blocks (factorization.py:476-505)
-    struct Target {
+    // target blocks (factorization.py:476-505).  (target, contribution) pairs
+    // are collected in reference order and grouped per target by a stable
+    // counting sort; block lookups go through the per-cluster neighbour maps.
+    struct THdr {
         double* C;
         int64_t ldc;
         int M, N;
-        std::vector<GemmContrib> cs;
+        int64_t count;
     };
     struct Cand {
         Key key;
@@ -783,50 +829,66 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         GemmContrib g;
         int64_t base, ntiles;
     };
-    std::vector<Target> targets;
-    std::unordered_map<double*, int> tindex;
+    std::vector<THdr> thdr;
+    std::vector<std::pair<int, GemmContrib>> tcon;
     std::vector<Cand> cands;
-    auto add_target = [&](double* C, int64_t ldc, int Mr, int Nc, const GemmContrib& g) {
+    {
+        size_t guess = 0;
+        for (auto& e : el) guess += size_t(e.np) * (e.np + 1) / 2;
+        tcon.reserve(guess);
+    }
+    const int tstamp = ++target_stamp;
+    // every target is a (sub)block of one View; the view carries its slot
+    auto add_target = [&](View& Vw, double* C, int64_t ldc, int Mr, int Nc, const GemmContrib& g) {
         if (Mr <= 0 || Nc <= 0) return;
-        auto it = tindex.find(C);
-        if (it == tindex.end()) {
-            tindex[C] = int(targets.size());
-            targets.push_back({C, ldc, Mr, Nc, {g}});
-        } else {
-            Target& t = targets[it->second];
-            if (t.M != Mr || t.N != Nc || t.ldc != ldc)
-                throw Error(H2F_E_INTERNAL, "assertion: Schur target shape mismatch");
-            t.cs.push_back(g);
+        if (Vw.stamp != tstamp) {
+            Vw.stamp = tstamp;
+            Vw.tidx = int(thdr.size());
+            thdr.push_back({C, ldc, Mr, Nc, 0});
         }
+        THdr& t = thdr[Vw.tidx];
+        if (t.C != C || t.M != Mr || t.N != Nc || t.ldc != ldc)
+            throw Error(H2F_E_INTERNAL, "assertion: Schur target shape mismatch");
+        ++t.count;
+        tcon.push_back({Vw.tidx, g});
     };
     for (auto& e : el) {
         const int c = e.c, r = e.r, kt = e.kt;
+        std::vector<int> opos(e.np);
+        for (int i = 1; i < e.np; ++i) opos[i] = L.at(e.ids[i]);
+        std::vector<Nbrs::Item>::const_iterator walk{}, walk_end{};
         for (int i = 0; i < e.np; ++i)
             for (int j = i; j < e.np; ++j) {
                 const GemmContrib g = contrib(e.G + e.offs[i], e.W, 1, e.MW + e.offs[j], e.W, 0, r);
                 const int wi = e.widths[i], wj = e.widths[j];
                 if (i == 0 && j == 0) {
-                    const View& Dcc = L.D.at(mkkey(c, c));
-                    add_target(Dcc.p + int64_t(r) * Dcc.ld + r, Dcc.ld, kt, kt, g);
+                    View& Dcc = L.dcc(e.ci);
+                    add_target(Dcc, Dcc.p + int64_t(r) * Dcc.ld + r, Dcc.ld, kt, kt, g);
                 } else if (i == 0) {
-                    const int o = e.ids[j];
-                    const Key key = canon(c, o);
-                    View* B = L.find(key);
-                    if (!B) throw Error(H2F_E_INTERNAL, "assertion: missing block next to eliminated cluster");
-                    if (key_a(key) == c) {
-                        add_target(B->p + int64_t(r) * B->ld, B->ld, kt, B->cols, g);
+                    const Entry& en = e.ents[j - 1];
+                    View* B = en.v;
+                    if (key_a(en.key) == c) {
+                        add_target(*B, B->p + int64_t(r) * B->ld, B->ld, kt, B->cols, g);
                     } else {
                         const GemmContrib gt = contrib(e.MW + e.offs[j], e.W, 1, e.G + e.offs[0], e.W, 0, r);
-                        add_target(B->p + r, B->ld, B->rows, kt, gt);
+                        add_target(*B, B->p + r, B->ld, B->rows, kt, gt);
                     }
                 } else {
-                    const Key key = mkkey(e.ids[i], e.ids[j]);
-                    View* B = L.find(key);
+                    View* B = nullptr;
+                    if (i == j) {
+                        B = L.diag[opos[i]];
+                        walk = L.touch[opos[i]].begin();
+                        walk_end = L.touch[opos[i]].end();
+                    } else {
+                        // ids[] ascending: merge-walk the neighbour list of ids[i]
+                        while (walk != walk_end && walk->first < e.ids[j]) ++walk;
+                        if (walk != walk_end && walk->first == e.ids[j]) B = walk->second.v;
+                    }
                     if (B) {
-                        add_target(B->p, B->ld, B->rows, B->cols, g);
+                        add_target(*B, B->p, B->ld, B->rows, B->cols, g);
                     } else {
                         Cand cd;
-                        cd.key = key;
+                        cd.key = mkkey(e.ids[i], e.ids[j]);
                         cd.M = wi;
                         cd.N = wj;
                         cd.g = g;
@@ -842,8 +904,20 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     // cluster, every existing target element read+written once
     double schur_bytes = 0;
     for (auto& e : el) schur_bytes += 16.0 * e.r * double(e.W);
-    for (auto& t : targets) schur_bytes += 16.0 * t.M * double(t.N);
-    for (auto& t : targets) sch.add(t.C, t.ldc, t.M, t.N, GEMM_ADD, t.cs.data(), t.cs.size());
+    {
+        std::vector<int64_t> start(thdr.size() + 1, 0);
+        for (size_t t = 0; t < thdr.size(); ++t) start[t + 1] = start[t] + thdr[t].count;
+        std::vector<int64_t> fill(start.begin(), start.end() - 1);
+        std::vector<GemmContrib> grouped(tcon.size());
+        for (auto& pc : tcon) grouped[fill[pc.first]++] = pc.second;
+        sch.tasks.reserve(thdr.size() + cands.size());
+        sch.contribs.reserve(tcon.size() + cands.size());
+        for (size_t t = 0; t < thdr.size(); ++t) {
+            const THdr& h = thdr[t];
+            schur_bytes += 16.0 * h.M * double(h.N);
+            sch.add(h.C, h.ldc, h.M, h.N, GEMM_ADD, grouped.data() + start[t], size_t(h.count));
+        }
+    }
     for (auto& cd : cands) cd.base = sch.add1(nullptr, 0, cd.M, cd.N, GEMM_NORM, cd.g);
     double* norms_d = sch.norm_tiles ? scr.alloc_n<double>(sch.norm_tiles) : nullptr;
     double* cand_ss_d = cands.empty() ? nullptr : scr.alloc_n<double>(cands.size());
@@ -879,6 +953,12 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     {
         GemmBuild create;
         std::unordered_map<Key, int> made;
+        struct Target {
+            double* C;
+            int64_t ldc;
+            int M, N;
+            std::vector<GemmContrib> cs;
+        };
         std::vector<Target> news;
         for (size_t i = 0; i < cands.size(); ++i) {
             const Cand& cd = cands[i];
@@ -903,12 +983,12 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         const int c = batch[bi], ci = L.at(c);
         const int r = L.red[ci];
         if (r) {
-            View& Dcc = L.D.at(mkkey(c, c));
+            View& Dcc = L.dcc(ci);
             Dcc.p += int64_t(r) * Dcc.ld + r;
             Dcc.rows -= r;
             Dcc.cols -= r;
             for (auto& kv : L.touch[ci]) {
-                View& B = L.block(kv.second.key, kv.second.dense);
+                View& B = *kv.second.v;
                 if (key_a(kv.second.key) == c) {
                     B.p += int64_t(r) * B.ld;
                     B.rows -= r;
@@ -1080,12 +1160,20 @@ void Factorizer::top_factor(double* A, int64_t n) {
     if (n == 0) return;
     double* red = scratch[0].alloc_n<double>(2);
     launch_absmax(A, n, int(n), int(n), red, st);
-    const int nb = 64;
+    const int nb = TOP_PANEL_NB;
+    const int g = top_panel_grid(int(n));
+    TopPanelScratch ps_scr;
+    ps_scr.val = scratch[0].alloc_n<double>(2 * g);
+    ps_scr.idx = scratch[0].alloc_n<int>(2 * g);
+    ps_scr.rows = scratch[0].alloc_n<double>(int64_t(2) * g * TOP_PANEL_NB);
+    ps_scr.rowk = scratch[0].alloc_n<double>(2 * TOP_PANEL_NB);
+    ps_scr.bar = scratch[0].alloc_n<unsigned>(2);
     for (int64_t k0 = 0; k0 < n; k0 += nb) {
         const int w = int(std::min<int64_t>(nb, n - k0));
         {
             ProfScope ps(K_TOP_PANEL, double(n - k0) * w * w, 16.0 * double(n - k0) * w);
-            launch_panel_lu(A, n, int(n), int(k0), w, F.top_piv, st);
+            if (!launch_coop_panel_lu(A, n, int(n), int(k0), w, F.top_piv, ps_scr, st))
+                launch_panel_lu(A, n, int(n), int(k0), w, F.top_piv, st);
         }
         const int64_t rest = n - k0 - w;
         ProfScope ps(K_TOP_MISC, double(rest) * w * w, 16.0 * double(n) * w + 16.0 * double(rest) * w);
@@ -1106,8 +1194,34 @@ void Factorizer::top_factor(double* A, int64_t n) {
         throw Error(H2F_E_SINGULAR, "singular block at the final dense solve");
 }
 
+// H2F_LEVEL_PROF=1 (with the profiler on): per-level kernel seconds and host
+// wall time on stderr (development aid)
+void Factorizer::dump_level_profile(int level) {
+    Profiler& P = ctx().prof;
+    P.collect();
+    const auto now = std::chrono::steady_clock::now();
+    const double wall = std::chrono::duration<double>(now - level_t0).count();
+    level_t0 = now;
+    std::fprintf(stderr, "[level %d] wall %.4f s:", level, wall);
+    double dev = 0;
+    for (int k = 0; k < K_COUNT; ++k) {
+        const double d = P.totals[k].seconds - level_prev[k];
+        level_prev[k] = P.totals[k].seconds;
+        dev += d;
+        if (d > 1e-4) std::fprintf(stderr, " %s=%.4f", kernel_name(k), d);
+    }
+    std::fprintf(stderr, " | kernels %.4f\n", dev);
+}
+
 void Factorizer::run(double norm_estimate, const double* v0) {
+    level_prof = std::getenv("H2F_LEVEL_PROF") != nullptr && ctx().prof.on;
+    if (level_prof) {
+        ctx().prof.collect();
+        for (int k = 0; k < K_COUNT; ++k) level_prev[k] = ctx().prof.totals[k].seconds;
+        level_t0 = std::chrono::steady_clock::now();
+    }
     mark_node.assign(M.nnodes, 0);
+    if (const char* p = std::getenv("H2F_AUG_LOG")) aug_log = std::fopen(p, "a");
     clock.mark(PH_NORM);
     if (norm_estimate < 0) {
         if (!v0) throw Error(H2F_E_ARG, "norm estimate requested without a start vector");
@@ -1204,6 +1318,7 @@ void Factorizer::run(double norm_estimate, const double* v0) {
                 L.reset();
             }
             F.recs.push_back(std::move(rec));
+            if (level_prof) dump_level_profile(level);
         }
     }
     clock.mark(PH_TOP);
@@ -1211,6 +1326,7 @@ void Factorizer::run(double norm_estimate, const double* v0) {
     clock.mark(-1);
     ctx().sync();
     clock.accumulate(F.phase);
+    if (aug_log) std::fclose(aug_log);
     for (size_t i = 0; i < level_marks.size(); ++i) {
         const size_t j = (i + 1 < level_marks.size()) ? level_marks[i + 1] : clock.size() - 2;
         F.recs[i].time_s = clock.between(level_marks[i], j);

@@ -15,59 +15,165 @@ namespace h2f {
 namespace {
 
 constexpr int ST = 256;
+constexpr int STW = ST / 32;
+
+// In-place triangular solve of one vector v (length r, stride vs) held in
+// shared memory by the whole CTA: 64-row blocks, the off-block products by
+// all warps, the 64x64 diagonal block by warp 0 through shuffles.
+// LOWER: unit lower (L of LU); else upper with diagonal (U of LU).
+template <bool LOWER>
+__device__ void cta_trsv(const double* __restrict__ A, int r, double* v) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nblk = (r + 63) / 64;
+    for (int t = 0; t < nblk; ++t) {
+        const int b = LOWER ? t : nblk - 1 - t;
+        const int r0 = b * 64, rb = min(64, r - r0);
+        // rows of block b minus the already solved part
+        const int c0 = LOWER ? 0 : r0 + rb, c1 = LOWER ? r0 : r;
+        if (c1 > c0) {
+            for (int i = warp; i < rb; i += STW) {
+                const double* ai = A + (int64_t)(r0 + i) * r;
+                double acc = 0.0;
+                for (int j = c0 + lane; j < c1; j += 32) acc += ai[j] * v[j];
+                acc = warp_sum(acc);
+                if (lane == 0) v[r0 + i] -= acc;
+            }
+            __syncthreads();
+        }
+        if (warp == 0) {
+            double v0 = lane < rb ? v[r0 + lane] : 0.0, v1 = lane + 32 < rb ? v[r0 + lane + 32] : 0.0;
+            if (LOWER) {
+                for (int k = 0; k < rb; ++k) {
+                    const double xk = __shfl_sync(0xffffffffu, k < 32 ? v0 : v1, k & 31);
+                    const double* ak = A + (int64_t)r0 * r + r0 + k;
+                    if (lane > k && lane < rb) v0 -= ak[(int64_t)lane * r] * xk;
+                    if (lane + 32 > k && lane + 32 < rb) v1 -= ak[(int64_t)(lane + 32) * r] * xk;
+                }
+            } else {
+                for (int k = rb - 1; k >= 0; --k) {
+                    const double* ak = A + (int64_t)r0 * r + r0 + k;
+                    if (lane == (k & 31)) {
+                        const double d = ak[(int64_t)k * r];
+                        if (k < 32) v0 /= d; else v1 /= d;
+                    }
+                    const double xk = __shfl_sync(0xffffffffu, k < 32 ? v0 : v1, k & 31);
+                    if (lane < k) v0 -= ak[(int64_t)lane * r] * xk;
+                    if (lane + 32 < k) v1 -= ak[(int64_t)(lane + 32) * r] * xk;
+                }
+            }
+            if (lane < rb) v[r0 + lane] = v0;
+            if (lane + 32 < rb) v[r0 + lane + 32] = v1;
+        }
+        __syncthreads();
+    }
+}
+
 
 __global__ void __launch_bounds__(ST)
-fwd_clusters_kernel(const SolveCluster* __restrict__ cls, const SolveEdge* __restrict__ edges,
-                    double* __restrict__ y, double* __restrict__ scratch, int nrhs,
-                    double* __restrict__ work) {
-    const SolveCluster C = cls[blockIdx.x];
+solve_tasks_kernel(const SolveTask* __restrict__ tasks, const SolveCluster* __restrict__ cls,
+                   const SolveEdge* __restrict__ edges, double* __restrict__ y, double* __restrict__ scratch,
+                   double* __restrict__ work, int nrhs) {
+    extern __shared__ double sv[];
+    const SolveTask T = tasks[blockIdx.x];
+    const SolveCluster C = cls[T.cl];
     const int s = C.s, r = C.r;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* yc = y + C.off * nrhs;
-    extern __shared__ double tmp[];  // s * nrhs when it fits, else the cluster's work slot
-    double* t = ((int64_t)s * nrhs <= 6144) ? tmp : work + C.woff;
-    // 1. rotate: t = Q^T y_c
-    for (int64_t e = threadIdx.x; e < (int64_t)s * nrhs; e += ST) {
-        const int j = (int)(e / nrhs), rh = (int)(e % nrhs);
-        double acc = 0.0;
-        for (int i = 0; i < s; ++i) acc += C.q[(int64_t)i * s + j] * yc[(int64_t)i * nrhs + rh];
-        t[e] = acc;
-    }
-    __syncthreads();
-    for (int64_t e = threadIdx.x; e < (int64_t)s * nrhs; e += ST) yc[e] = t[e];
-    __syncthreads();
-    if (r == 0) return;
-    // 2. products p_e = mat_e^T y_R
-    for (int64_t ei = C.edge_begin; ei < C.edge_end; ++ei) {
-        const SolveEdge E = edges[ei];
-        double* out = scratch + E.soff * nrhs;
-        for (int64_t e = threadIdx.x; e < (int64_t)E.w * nrhs; e += ST) {
-            const int j = (int)(e / nrhs), rh = (int)(e % nrhs);
+    double* wk = work + C.woff;             // s x nrhs
+    double* tb = work + C.woff + (int64_t)s * nrhs;  // r x nrhs
+    switch (T.kind) {
+    case ST_ROT_T: {
+        // 64 columns x 4 row groups, partial sums reduced through shared memory
+        const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+        const int j = T.begin + tx;
+        for (int rh = 0; rh < nrhs; ++rh) {
+            for (int i = threadIdx.x; i < s; i += ST) sv[i] = yc[(int64_t)i * nrhs + rh];
+            __syncthreads();
             double acc = 0.0;
-            for (int k = 0; k < r; ++k) acc += E.mat[(int64_t)k * E.ld + j] * yc[(int64_t)k * nrhs + rh];
-            out[e] = acc;
+            if (j < T.end)
+                for (int i = ty; i < s; i += 4) acc += C.q[(int64_t)i * s + j] * sv[i];
+            sv[s + ty * 64 + tx] = acc;
+            __syncthreads();
+            if (ty == 0 && j < T.end)
+                wk[(int64_t)j * nrhs + rh] = ((sv[s + tx] + sv[s + 64 + tx]) + sv[s + 128 + tx]) + sv[s + 192 + tx];
+            __syncthreads();
         }
+        break;
     }
-    __syncthreads();
-    // 3. pivots + unit lower solve on y_R (one warp)
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        for (int k = 0; k < r; ++k) {
-            const int p = C.piv[k];
-            if (p != k)
-                for (int rh = lane; rh < nrhs; rh += 32) {
-                    const double a = yc[(int64_t)k * nrhs + rh];
-                    yc[(int64_t)k * nrhs + rh] = yc[(int64_t)p * nrhs + rh];
-                    yc[(int64_t)p * nrhs + rh] = a;
-                }
-            __syncwarp();
-        }
-        for (int k = 0; k < r; ++k) {
-            for (int64_t e = lane; e < (int64_t)(r - k - 1) * nrhs; e += 32) {
-                const int i = k + 1 + (int)(e / nrhs), rh = (int)(e % nrhs);
-                yc[(int64_t)i * nrhs + rh] -= C.lu[(int64_t)i * r + k] * yc[(int64_t)k * nrhs + rh];
+    case ST_PROD: {
+        const int64_t j = T.begin + threadIdx.x;
+        for (int rh = 0; rh < nrhs; ++rh) {
+            for (int k = threadIdx.x; k < r; k += ST) sv[k] = wk[(int64_t)k * nrhs + rh];
+            __syncthreads();
+            if (j < T.end) {
+                double acc = 0.0;
+                const double* mj = C.mw + j;
+                for (int k = 0; k < r; ++k) acc += mj[(int64_t)k * C.W] * sv[k];
+                scratch[(C.soff + j) * nrhs + rh] = acc;
             }
-            __syncwarp();
+            __syncthreads();
         }
+        break;
+    }
+    case ST_LSOLVE: {
+        for (int rh = 0; rh < nrhs; ++rh) {
+            for (int i = threadIdx.x; i < r; i += ST) sv[i] = wk[(int64_t)i * nrhs + rh];
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int k = 0; k < r; ++k) {
+                    const int p = C.piv[k];
+                    if (p != k) { const double a = sv[k]; sv[k] = sv[p]; sv[p] = a; }
+                }
+            __syncthreads();
+            cta_trsv<true>(C.lu, r, sv);
+            for (int i = threadIdx.x; i < s; i += ST)
+                yc[(int64_t)i * nrhs + rh] = i < r ? sv[i] : wk[(int64_t)i * nrhs + rh];
+            __syncthreads();
+        }
+        break;
+    }
+    case ST_USOLVE: {
+        for (int rh = 0; rh < nrhs; ++rh) {
+            for (int i = threadIdx.x; i < r; i += ST) sv[i] = yc[(int64_t)i * nrhs + rh];
+            __syncthreads();
+            cta_trsv<false>(C.lu, r, sv);
+            for (int i = threadIdx.x; i < s; i += ST)
+                wk[(int64_t)i * nrhs + rh] = i < r ? sv[i] : yc[(int64_t)i * nrhs + rh];
+            __syncthreads();
+        }
+        break;
+    }
+    case ST_GATHER: {
+        for (int k = T.begin + warp; k < T.end; k += STW)
+            for (int rh = 0; rh < nrhs; ++rh) {
+                double acc = 0.0;
+                for (int64_t ei = C.edge_begin; ei < C.edge_end; ++ei) {
+                    const SolveEdge E = edges[ei];
+                    const double* mk = E.mat + (int64_t)k * E.ld;
+                    const double* ys = y + E.lo * nrhs + rh;
+                    for (int j = lane; j < E.w; j += 32) acc += mk[j] * ys[(int64_t)j * nrhs];
+                }
+                acc = warp_sum(acc);
+                if (lane == 0) tb[(int64_t)k * nrhs + rh] = acc;
+            }
+        break;
+    }
+    case ST_ROT: {
+        for (int rh = 0; rh < nrhs; ++rh) {
+            for (int j = threadIdx.x; j < s; j += ST)
+                sv[j] = wk[(int64_t)j * nrhs + rh] + (j < r ? tb[(int64_t)j * nrhs + rh] : 0.0);
+            __syncthreads();
+            for (int i = T.begin + warp; i < T.end; i += STW) {
+                const double* qi = C.q + (int64_t)i * s;
+                double acc = 0.0;
+                for (int j = lane; j < s; j += 32) acc += qi[j] * sv[j];
+                acc = warp_sum(acc);
+                if (lane == 0) yc[(int64_t)i * nrhs + rh] = acc;
+            }
+            __syncthreads();
+        }
+        break;
+    }
     }
 }
 
@@ -80,59 +186,6 @@ fwd_scatter_kernel(const ScatterGroup* __restrict__ groups, const int64_t* __res
         for (int64_t l = G.begin; l < G.end; ++l) acc += scratch[list[l] * nrhs + e];
         y[G.lo * nrhs + e] = acc;
     }
-}
-
-__global__ void __launch_bounds__(ST)
-bwd_clusters_kernel(const SolveCluster* __restrict__ cls, const SolveEdge* __restrict__ edges,
-                    double* __restrict__ y, int nrhs, double* __restrict__ work) {
-    const SolveCluster C = cls[blockIdx.x];
-    const int s = C.s, r = C.r;
-    double* yc = y + C.off * nrhs;
-    extern __shared__ double tmp[];
-    double* t = ((int64_t)s * nrhs <= 6144) ? tmp : work + C.woff;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = ST / 32;
-    if (r > 0) {
-        // 1. upper solve on y_R (one warp, column oriented)
-        if (threadIdx.x < 32) {
-            for (int k = r - 1; k >= 0; --k) {
-                const double ukk = C.lu[(int64_t)k * r + k];
-                for (int rh = lane; rh < nrhs; rh += 32) yc[(int64_t)k * nrhs + rh] /= ukk;
-                __syncwarp();
-                for (int64_t e = lane; e < (int64_t)k * nrhs; e += 32) {
-                    const int i = (int)(e / nrhs), rh = (int)(e % nrhs);
-                    yc[(int64_t)i * nrhs + rh] -= C.lu[(int64_t)i * r + k] * yc[(int64_t)k * nrhs + rh];
-                }
-                __syncwarp();
-            }
-        }
-        __syncthreads();
-        // 2. acc = sum_e mat_e y[span_e]  (warp per redundant row)
-        for (int64_t e = warp; e < (int64_t)r * nrhs; e += nw) {
-            const int k = (int)(e / nrhs), rh = (int)(e % nrhs);
-            double acc = 0.0;
-            for (int64_t ei = C.edge_begin; ei < C.edge_end; ++ei) {
-                const SolveEdge E = edges[ei];
-                const double* mk = E.mat + (int64_t)k * E.ld;
-                for (int j = lane; j < E.w; j += 32) acc += mk[j] * y[(E.lo + j) * nrhs + rh];
-            }
-            acc = warp_sum(acc);
-            if (lane == 0) t[e] = acc;
-        }
-        __syncthreads();
-        for (int64_t e = threadIdx.x; e < (int64_t)r * nrhs; e += ST) yc[e] += t[e];
-        __syncthreads();
-    }
-    // 3. y_c = Q y_c (warp per row)
-    for (int64_t e = warp; e < (int64_t)s * nrhs; e += nw) {
-        const int i = (int)(e / nrhs), rh = (int)(e % nrhs);
-        const double* qi = C.q + (int64_t)i * s;
-        double acc = 0.0;
-        for (int j = lane; j < s; j += 32) acc += qi[j] * yc[(int64_t)j * nrhs + rh];
-        acc = warp_sum(acc);
-        if (lane == 0) t[e] = acc;
-    }
-    __syncthreads();
-    for (int64_t e = threadIdx.x; e < (int64_t)s * nrhs; e += ST) yc[e] = t[e];
 }
 
 __global__ void gather_rows_kernel(const double* __restrict__ src, const int64_t* __restrict__ idx,
@@ -149,39 +202,6 @@ __global__ void scatter_rows_kernel(const double* __restrict__ src, const int64_
     if (e >= n * nrhs) return;
     const int64_t i = e / nrhs, rh = e % nrhs;
     dst[idx[i] * nrhs + rh] = src[e];
-}
-
-// dense LU solve (lu_solve semantics) by one CTA; x is n x nrhs
-__global__ void __launch_bounds__(1024)
-top_solve_kernel(const double* __restrict__ lu, const int* __restrict__ piv, int n,
-                 double* __restrict__ x, int nrhs) {
-    for (int k = 0; k < n; ++k) {
-        const int p = piv[k];
-        if (p != k)
-            for (int rh = threadIdx.x; rh < nrhs; rh += blockDim.x) {
-                const double a = x[(int64_t)k * nrhs + rh];
-                x[(int64_t)k * nrhs + rh] = x[(int64_t)p * nrhs + rh];
-                x[(int64_t)p * nrhs + rh] = a;
-            }
-        __syncthreads();
-    }
-    for (int k = 0; k < n; ++k) {
-        for (int64_t e = threadIdx.x; e < (int64_t)(n - k - 1) * nrhs; e += blockDim.x) {
-            const int i = k + 1 + (int)(e / nrhs), rh = (int)(e % nrhs);
-            x[(int64_t)i * nrhs + rh] -= lu[(int64_t)i * n + k] * x[(int64_t)k * nrhs + rh];
-        }
-        __syncthreads();
-    }
-    for (int k = n - 1; k >= 0; --k) {
-        const double ukk = lu[(int64_t)k * n + k];
-        for (int rh = threadIdx.x; rh < nrhs; rh += blockDim.x) x[(int64_t)k * nrhs + rh] /= ukk;
-        __syncthreads();
-        for (int64_t e = threadIdx.x; e < (int64_t)k * nrhs; e += blockDim.x) {
-            const int i = (int)(e / nrhs), rh = (int)(e % nrhs);
-            x[(int64_t)i * nrhs + rh] -= lu[(int64_t)i * n + k] * x[(int64_t)k * nrhs + rh];
-        }
-        __syncthreads();
-    }
 }
 
 __global__ void __launch_bounds__(128)
@@ -248,16 +268,18 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
 
-void launch_fwd_clusters(const SolveCluster* d_cl, int32_t ncl, const SolveEdge* d_edges, double* y,
-                         double* scratch, int32_t nrhs, double* work, cudaStream_t st) {
-    if (ncl <= 0) return;
+void launch_solve_tasks(const SolveTask* d_tasks, int32_t ntasks, const SolveCluster* d_cl,
+                        const SolveEdge* d_edges, double* y, double* scratch, double* work, int32_t nrhs,
+                        cudaStream_t st) {
+    if (ntasks <= 0) return;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(fwd_clusters_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             6144 * 8);
+        cudaFuncSetAttribute(solve_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SOLVE_SMEM_VEC * 8);
         configured = true;
     }
-    fwd_clusters_kernel<<<ncl, ST, 6144 * sizeof(double), st>>>(d_cl, d_edges, y, scratch, nrhs, work);
+    solve_tasks_kernel<<<ntasks, ST, SOLVE_SMEM_VEC * sizeof(double), st>>>(d_tasks, d_cl, d_edges, y, scratch,
+                                                                            work, nrhs);
     count_launch();
 }
 
@@ -265,19 +287,6 @@ void launch_fwd_scatter(const ScatterGroup* d_groups, int32_t ngroups, const int
                         const double* scratch, double* y, int32_t nrhs, cudaStream_t st) {
     if (ngroups <= 0) return;
     fwd_scatter_kernel<<<ngroups, ST, 0, st>>>(d_groups, d_list, scratch, y, nrhs);
-    count_launch();
-}
-
-void launch_bwd_clusters(const SolveCluster* d_cl, int32_t ncl, const SolveEdge* d_edges, double* y,
-                         int32_t nrhs, double* work, cudaStream_t st) {
-    if (ncl <= 0) return;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(bwd_clusters_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             6144 * 8);
-        configured = true;
-    }
-    bwd_clusters_kernel<<<ncl, ST, 6144 * sizeof(double), st>>>(d_cl, d_edges, y, nrhs, work);
     count_launch();
 }
 
@@ -292,14 +301,6 @@ void launch_scatter_rows(const double* src, const int64_t* idx, int64_t n, int32
                          cudaStream_t st) {
     if (n <= 0) return;
     scatter_rows_kernel<<<nblk(n * nrhs, 256), 256, 0, st>>>(src, idx, n, nrhs, dst);
-    count_launch();
-}
-
-void launch_top_solve(const double* lu, const int32_t* piv, int32_t n, double* x, int32_t nrhs,
-                      double* work, cudaStream_t st) {
-    (void)work;
-    if (n <= 0) return;
-    top_solve_kernel<<<1, 1024, 0, st>>>(lu, piv, n, x, nrhs);
     count_launch();
 }
 

@@ -151,10 +151,13 @@ struct SolveCluster {
     const double* q;     // s x s
     const double* lu;    // r x r
     const int32_t* piv;
+    const double* mw;    // r x W eliminators (-W), row-major ld W; edges are column slices
     int64_t off;         // offset in the level vector
     int32_t s, r;
+    int64_t W;
     int64_t edge_begin, edge_end;
-    int64_t woff;        // work slot (s * nrhs doubles) when it exceeds shared memory
+    int64_t woff;        // work slot: 2 * s * nrhs doubles (rotated vector, gathered products)
+    int64_t soff;        // forward products of column j of mw go to scratch row soff + j
 };
 
 struct SolveEdge {
@@ -165,6 +168,23 @@ struct SolveEdge {
     int32_t w;
     int32_t pad_;
 };
+
+// one CTA of a batched substitution launch (k_solve.cu)
+enum SolveTaskKind : int32_t {
+    ST_ROT_T = 0,  // work[j] = (Q^T y_c)[j], j in [begin, end)            forward
+    ST_PROD,       // scratch[soff + j] = (mw^T work_R)[j], j in [begin,end)  forward
+    ST_LSOLVE,     // y_c = [L^-1 P work_R ; work_S]                          forward
+    ST_USOLVE,     // work = [U^-1 y_R ; y_S]                                 backward
+    ST_GATHER,     // tbuf[k] = sum_e (mat_e y[span_e])[k], k in [begin,end)  backward
+    ST_ROT,        // y_c[i] = (Q (work + [tbuf; 0]))[i], i in [begin, end)   backward
+};
+struct SolveTask {
+    int32_t cl, kind, begin, end;
+};
+constexpr int SOLVE_ROT_T_COLS = 64;
+constexpr int SOLVE_PROD_COLS = 256;
+constexpr int SOLVE_ROW_SLICE = 16;
+constexpr int SOLVE_SMEM_VEC = 8192;  // doubles of shared vector space per solve CTA
 
 struct ScatterGroup {    // y[lo : lo+w] += sum of scratch rows listed in [begin,end)
     int64_t lo;
@@ -220,24 +240,39 @@ void launch_row_swaps(double* A, int64_t lda, int32_t ncols_total, int32_t k0, i
                       const int32_t* piv, int32_t skip_c0, int32_t skip_c1, cudaStream_t st);
 void launch_trsm_unit_lower_rows(const double* A, int64_t lda, int32_t k0, int32_t nb,
                                  int32_t c0, int32_t ncols, cudaStream_t st);
+// cooperative panel LU of the dense top (k_top.cu); false if the panel does
+// not fit (caller falls back to launch_panel_lu)
+constexpr int TOP_PANEL_NB = 64;
+constexpr size_t TOP_PANEL_SMEM = 200 * 1024;
+struct TopPanelScratch {
+    double* val;     // 2 * grid
+    int* idx;        // 2 * grid
+    double* rows;    // 2 * grid * TOP_PANEL_NB
+    double* rowk;    // 2 * TOP_PANEL_NB
+    unsigned* bar;   // 2
+};
+int top_panel_grid(int m);
+bool launch_coop_panel_lu(double* A, int64_t lda, int32_t n, int32_t k0, int32_t nb, int32_t* piv,
+                          TopPanelScratch S, cudaStream_t st);
 void launch_absmax(const double* A, int64_t lda, int32_t rows, int32_t cols, double* out,
                    cudaStream_t st);
 void launch_diag_absmin(const double* A, int64_t lda, int32_t n, double* out, cudaStream_t st);
 
 // solve
-void launch_fwd_clusters(const SolveCluster* d_cl, int32_t ncl, const SolveEdge* d_edges,
-                         double* y, double* scratch, int32_t nrhs, double* work,
-                         cudaStream_t st);
+void launch_solve_tasks(const SolveTask* d_tasks, int32_t ntasks, const SolveCluster* d_cl,
+                        const SolveEdge* d_edges, double* y, double* scratch, double* work, int32_t nrhs,
+                        cudaStream_t st);
 void launch_fwd_scatter(const ScatterGroup* d_groups, int32_t ngroups, const int64_t* d_list,
                         const double* scratch, double* y, int32_t nrhs, cudaStream_t st);
-void launch_bwd_clusters(const SolveCluster* d_cl, int32_t ncl, const SolveEdge* d_edges,
-                         double* y, int32_t nrhs, double* work, cudaStream_t st);
 void launch_gather_rows(const double* src, const int64_t* idx, int64_t n, int32_t nrhs,
                         double* dst, cudaStream_t st);
 void launch_scatter_rows(const double* src, const int64_t* idx, int64_t n, int32_t nrhs,
                          double* dst, cudaStream_t st);
-void launch_top_solve(const double* lu, const int32_t* piv, int32_t n, double* x, int32_t nrhs,
-                      double* work, cudaStream_t st);
+// dense top solve: x <- (LU)^-1 P x through tmp (n x nrhs); sync holds
+// 1 + ceil(n/64) ints; perm from launch_top_perm (k_top.cu)
+void launch_top_perm(const int32_t* piv, int32_t n, int32_t* perm, cudaStream_t st);
+void launch_top_solve(const double* lu, const int32_t* perm, int32_t n, double* x, int32_t nrhs,
+                      double* tmp, int32_t* sync, cudaStream_t st);
 
 // matvec / vectors
 void launch_gemv_tasks(const GemvTask* d_tasks, int32_t ntasks, const GemvContrib* d_contribs,

@@ -21,6 +21,10 @@ struct SolvePlan {
         ScatterGroup* groups = nullptr;
         int32_t ngroups = 0;
         int64_t* list = nullptr;
+        // task lists: forward rotation, forward products + L solves,
+        // backward U solves + gathers, backward rotation
+        SolveTask* tk[4] = {};
+        int32_t ntk[4] = {};
         double fwd_flops = 0, fwd_bytes = 0, sc_bytes = 0;
     };
     struct Level {
@@ -33,6 +37,9 @@ struct SolvePlan {
     std::vector<Level> levels;
     std::vector<double*> yv;   // per record level vectors
     double* ytop = nullptr;
+    double* ttop = nullptr;   // top solve temporary
+    int32_t* top_perm = nullptr;
+    int32_t* top_sync = nullptr;
     double* scratch = nullptr;
     double* work = nullptr;
     Region mem{size_t(16) << 20};
@@ -69,6 +76,7 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
             std::vector<int64_t> group_order;
             int64_t soff = 0, woff = 0;
             double flops_b = 0, bytes_b = 0;
+            std::vector<SolveTask> tk[4];
             for (int c : batch) {
                 const ClusterFactor& cf = rec.factors[rec.pos.at(c)];
                 SolveCluster sc{};
@@ -78,14 +86,24 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
                 sc.off = cf.offset;
                 sc.s = cf.s;
                 sc.r = cf.r;
+                sc.mw = cf.edges.empty() ? nullptr : cf.edges[0].mat;
+                sc.W = 0;
+                for (auto& e : cf.edges) sc.W += e.w;
+                sc.soff = soff;
                 sc.edge_begin = int64_t(edges.size());
                 sc.woff = woff;
-                woff += int64_t(cf.s) * nrhs;
+                woff += 2 * int64_t(cf.s) * nrhs;
+                if (cf.s + 256 > SOLVE_SMEM_VEC)
+                    throw Error(H2F_E_INTERNAL, "assertion: cluster too large for the solve kernels");
+                int64_t col = 0;
                 for (auto& e : cf.edges) {
                     SolveEdge se{};
                     se.mat = e.mat;
                     se.ld = e.ld;
                     se.w = e.w;
+                    if (e.mat != sc.mw + col || e.ld != sc.W)
+                        throw Error(H2F_E_INTERNAL, "assertion: eliminator edges are not contiguous");
+                    col += e.w;
                     // target span (solve.py:80-87)
                     if (e.kind == EDGE_SELF) {
                         se.lo = cf.offset + cf.r;
@@ -106,9 +124,25 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
                     edges.push_back(se);
                 }
                 sc.edge_end = int64_t(edges.size());
+                const int ci = int(cls.size());
                 cls.push_back(sc);
-                double ew = 0;
-                for (auto& e : cf.edges) ew += double(e.w);
+                for (int j = 0; j < cf.s; j += SOLVE_ROT_T_COLS)
+                    tk[0].push_back({ci, ST_ROT_T, j, std::min(cf.s, j + SOLVE_ROT_T_COLS)});
+                for (int i = 0; i < cf.s; i += SOLVE_ROW_SLICE)
+                    tk[3].push_back({ci, ST_ROT, i, std::min(cf.s, i + SOLVE_ROW_SLICE)});
+                if (cf.r > 0) {
+                    tk[1].push_back({ci, ST_LSOLVE, 0, cf.r});
+                    for (int64_t j = 0; j < sc.W; j += SOLVE_PROD_COLS)
+                        tk[1].push_back({ci, ST_PROD, int32_t(j), int32_t(std::min<int64_t>(sc.W, j + SOLVE_PROD_COLS))});
+                    tk[2].push_back({ci, ST_USOLVE, 0, cf.r});
+                    for (int i = 0; i < cf.r; i += SOLVE_ROW_SLICE)
+                        tk[2].push_back({ci, ST_GATHER, i, std::min(cf.r, i + SOLVE_ROW_SLICE)});
+                } else {
+                    // nothing eliminated: the rotated vector passes through
+                    tk[1].push_back({ci, ST_LSOLVE, 0, 0});
+                    tk[2].push_back({ci, ST_USOLVE, 0, 0});
+                }
+                double ew = double(sc.W);
                 flops_b += (2.0 * cf.s * cf.s + 2.0 * cf.r * ew + double(cf.r) * cf.r) * nrhs;
                 bytes_b += 8.0 * (double(cf.s) * cf.s + double(cf.r) * cf.r + cf.r * ew) +
                            16.0 * (cf.s + ew) * nrhs;
@@ -132,6 +166,10 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
             B.ngroups = int32_t(gs.size());
             B.groups = to_dev(P.mem, gs);
             B.list = to_dev(P.mem, list);
+            for (int q = 0; q < 4; ++q) {
+                B.tk[q] = to_dev(P.mem, tk[q]);
+                B.ntk[q] = int32_t(tk[q].size());
+            }
             B.fwd_flops = flops_b;
             B.fwd_bytes = bytes_b;
             B.sc_bytes = 16.0 * double(soff) * nrhs;
@@ -143,6 +181,10 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
     }
     for (auto& L : P.levels) P.yv.push_back(P.mem.alloc_n<double>(L.total * nrhs));
     P.ytop = P.mem.alloc_n<double>(std::max<int64_t>(f.top_size, 1) * nrhs);
+    P.ttop = P.mem.alloc_n<double>(std::max<int64_t>(f.top_size, 1) * nrhs);
+    P.top_perm = P.mem.alloc_n<int32_t>(std::max<int64_t>(f.top_size, 1));
+    P.top_sync = P.mem.alloc_n<int32_t>(f.top_size / 64 + 2);
+    launch_top_perm(f.top_piv, int32_t(f.top_size), P.top_perm, ctx().stream);
     P.scratch = P.mem.alloc_n<double>(std::max<int64_t>(scratch_rows, 1) * nrhs);
     P.work = P.mem.alloc_n<double>(std::max<int64_t>(work_max, 1));
     ctx().sync();
@@ -160,7 +202,7 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
     if (f.recs.empty()) {
         // solve.py:46-47
         H2F_CUDA(cudaMemcpyAsync(P.ytop, b_dev, nb, cudaMemcpyDeviceToDevice, st));
-        launch_top_solve(f.top_lu, f.top_piv, int(f.top_size), P.ytop, nrhs, P.work, st);
+        launch_top_solve(f.top_lu, P.top_perm, int(f.top_size), P.ytop, nrhs, P.ttop, P.top_sync, st);
         H2F_CUDA(cudaMemcpyAsync(x_dev, P.ytop, nb, cudaMemcpyDeviceToDevice, st));
         return;
     }
@@ -171,7 +213,8 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
         for (auto& B : L.batches) {
             {
                 ProfScope ps(K_SOLVE_FWD, B.fwd_flops, B.fwd_bytes);
-                launch_fwd_clusters(B.cl, B.ncl, B.edges, P.yv[li], P.scratch, nrhs, P.work, st);
+                launch_solve_tasks(B.tk[0], B.ntk[0], B.cl, B.edges, P.yv[li], P.scratch, P.work, nrhs, st);
+                launch_solve_tasks(B.tk[1], B.ntk[1], B.cl, B.edges, P.yv[li], P.scratch, P.work, nrhs, st);
             }
             ProfScope ps(K_SOLVE_SCATTER, 0.0, B.sc_bytes);
             launch_fwd_scatter(B.groups, B.ngroups, B.list, P.scratch, P.yv[li], nrhs, st);
@@ -182,7 +225,7 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
     {
         const double nt = double(f.top_size);
         ProfScope ps(K_SOLVE_TOP, 2.0 * nt * nt * nrhs, 8.0 * nt * nt);
-        launch_top_solve(f.top_lu, f.top_piv, int(f.top_size), P.ytop, nrhs, P.work, st);
+        launch_top_solve(f.top_lu, P.top_perm, int(f.top_size), P.ytop, nrhs, P.ttop, P.top_sync, st);
     }
     for (size_t li = R; li-- > 0;) {
         auto& L = P.levels[li];
@@ -191,7 +234,8 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
         for (size_t bi = L.batches.size(); bi-- > 0;) {
             auto& B = L.batches[bi];
             ProfScope ps(K_SOLVE_BWD, B.fwd_flops, B.fwd_bytes);
-            launch_bwd_clusters(B.cl, B.ncl, B.edges, P.yv[li], nrhs, P.work, st);
+            launch_solve_tasks(B.tk[2], B.ntk[2], B.cl, B.edges, P.yv[li], P.scratch, P.work, nrhs, st);
+            launch_solve_tasks(B.tk[3], B.ntk[3], B.cl, B.edges, P.yv[li], P.scratch, P.work, nrhs, st);
         }
     }
     H2F_CUDA(cudaMemcpyAsync(x_dev, P.yv[0], nb, cudaMemcpyDeviceToDevice, st));

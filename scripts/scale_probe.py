@@ -28,9 +28,11 @@ for item in cases:
     t0 = time.perf_counter()
     x = H.refined_solve(h2, fac2, b)
     ts = time.perf_counter() - t0
+    _lib.profile_enable(True); _lib.profile_reset()
     t0 = time.perf_counter()
     x = H.refined_solve(h2, fac2, b)
     ts2 = time.perf_counter() - t0
+    sprof = _lib.profile_get(); _lib.profile_enable(False)
     eb = np.linalg.norm(H.matvec(h2, x) - b) / np.linalg.norm(b)
     print(json.dumps({"case": f"{name}_{n}", "over": over, "build_s": round(tb, 2), "fact_s_first": round(tf, 4),
         "fact_s": round(tf2, 4), "solve_s_first": round(ts, 4), "solve_s": round(ts2, 4), "e_b": eb,
@@ -40,4 +42,6 @@ for item in cases:
         "levels": [(r.level, round(r.time_s, 4), r.nbatches, r.max_rank) for r in fac2.records],
         "mem": _lib.memory_stats(),
         "kernels": {k: [round(v["seconds"], 4), v["launches"], round(v["flops"] / max(v["seconds"], 1e-12) / 1e9, 1)]
-                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["seconds"])}}), flush=True)
+                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["seconds"])},
+        "solve_kernels": {k: [round(v["seconds"], 4), v["launches"], round(v["bytes"] / max(v["seconds"], 1e-12) / 1e9, 1)]
+                    for k, v in sorted(sprof.items(), key=lambda kv: -kv[1]["seconds"])}}), flush=True)
