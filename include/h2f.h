@@ -133,6 +133,24 @@ int h2f_profile_get(int32_t kid, h2f_kernel_profile* out);   /* syncs the stream
 /* FP64 DMMA (m8n8k4) throughput probe: all SMs, iters MMAs per warp chain */
 int h2f_bench_dmma(int64_t iters, double* tflops);
 
+/* ---- per-cluster dense kernels (test / micro-benchmark hooks) -------------
+ * Host pointers, row-major.  `path` selects the implementation the
+ * factorization dispatches to by size, so each can be checked on any size:
+ *   svd:        0 shared-memory Jacobi (one CTA), 1 block-cyclic multi-CTA,
+ *               2 pairwise multi-CTA.  R is m x n; U receives the kept
+ *               rows (kept x n, sorted by sigma desc); sweeps = -1 if unknown.
+ *               augment_basis's SVD step, factorization.py:79-81
+ *   qr_r:       0 shared-memory TSQR, 1 blocked Householder (cooperative
+ *               panels).  Y is n x wf (QR of Y^T), R is min(n,wf) x n.
+ *               factorization.py:78
+ *   complement: 0 one CTA, 1 blocked Householder.  BT is kt x s (columns of
+ *               b_aug), Q is s x s = [complement | b_aug].  factorization.py:88-99
+ * ms = device time of the kernels. */
+int h2f_dense_svd(const double* R, int32_t m, int32_t n, double thresh, int32_t path, double* U, int32_t* kept,
+                  int32_t* sweeps, double* ms);
+int h2f_dense_qr_r(const double* Y, int32_t n, int32_t wf, int32_t path, double* R, double* ms);
+int h2f_dense_complement(const double* BT, int32_t s, int32_t kt, int32_t path, double* Q, double* ms);
+
 /* ---- H2 matrix ----------------------------------------------------------- */
 int h2f_matrix_create(const h2f_matrix_desc* desc, const double* vals, h2f_matrix* out);
 int h2f_matrix_destroy(h2f_matrix m);

@@ -77,6 +77,9 @@ _SIGS = {
     "h2f_profile_count": (C.c_int, [i32p]),
     "h2f_profile_get": (C.c_int, [C.c_int32, C.POINTER(KernelProfile)]),
     "h2f_bench_dmma": (C.c_int, [C.c_int64, f64p]),
+    "h2f_dense_svd": (C.c_int, [f64p, C.c_int32, C.c_int32, C.c_double, C.c_int32, f64p, i32p, i32p, f64p]),
+    "h2f_dense_qr_r": (C.c_int, [f64p, C.c_int32, C.c_int32, C.c_int32, f64p, f64p]),
+    "h2f_dense_complement": (C.c_int, [f64p, C.c_int32, C.c_int32, C.c_int32, f64p, f64p]),
     "h2f_matrix_create": (C.c_int, [C.POINTER(MatrixDesc), f64p, C.POINTER(C.c_void_p)]),
     "h2f_matrix_destroy": (C.c_int, [C.c_void_p]),
     "h2f_matrix_nbytes": (C.c_int, [C.c_void_p, i64p]),
@@ -215,3 +218,36 @@ def bench_dmma(iters=20000):
     v = C.c_double()
     check(ensure_init().h2f_bench_dmma(int(iters), C.byref(v)))
     return v.value
+
+
+# ---- per-cluster dense kernels (test / micro-benchmark hooks) ---------------
+
+def dense_svd(R, thresh, path):
+    """(U_kept, kept, sweeps, ms): one-sided Jacobi on the rows of R (m x n)."""
+    R = as_f64(R)
+    m, n = R.shape
+    U = np.zeros((n, n))
+    kept, sweeps, ms = C.c_int32(), C.c_int32(), C.c_double()
+    check(ensure_init().h2f_dense_svd(ptr(R), m, n, float(thresh), int(path), ptr(U), C.byref(kept),
+                                      C.byref(sweeps), C.byref(ms)))
+    return U[:kept.value].copy(), kept.value, sweeps.value, ms.value
+
+
+def dense_qr_r(Y, path):
+    """(R, ms): R factor of the QR of Y^T (Y is n x wf)."""
+    Y = as_f64(Y)
+    n, wf = Y.shape
+    R = np.zeros((min(n, wf), n))
+    ms = C.c_double()
+    check(ensure_init().h2f_dense_qr_r(ptr(Y), n, wf, int(path), ptr(R), C.byref(ms)))
+    return R, ms.value
+
+
+def dense_complement(BT, path):
+    """(Q, ms): [orthonormal complement | b_aug] from BT = b_aug^T (kt x s)."""
+    BT = as_f64(BT)
+    kt, s = BT.shape
+    Q = np.zeros((s, s))
+    ms = C.c_double()
+    check(ensure_init().h2f_dense_complement(ptr(BT), s, kt, int(path), ptr(Q), C.byref(ms)))
+    return Q, ms.value

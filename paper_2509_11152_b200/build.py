@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-Wno-deprecated-gpu-targets", "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-I", CSRC,
           "-I", os.path.join(os.path.dirname(HERE), "include")]
-SOURCES = ["k_gemm.cu", "k_dense.cu", "k_solve.cu", "k_top.cu", "runtime.cpp", "h2mat.cpp", "factor.cpp",
+SOURCES = ["k_gemm.cu", "k_dense.cu", "k_hh.cu", "dense.cpp", "k_solve.cu", "k_top.cu", "runtime.cpp", "h2mat.cpp", "factor.cpp",
            "solve.cpp", "api.cpp"]
 
 

@@ -5,6 +5,8 @@
 #include <string>
 #include <vector>
 
+#include "builders.h"
+#include "dense.h"
 #include "factor.h"
 
 using namespace h2f;
@@ -121,6 +123,104 @@ int h2f_profile_get(int32_t kid, h2f_kernel_profile* out) {
 
 int h2f_bench_dmma(int64_t iters, double* tflops) {
     return guard([&] { *tflops = bench_dmma(iters, ctx().stream); });
+}
+
+namespace {
+
+// events around a device section on the library stream
+struct DevTimer {
+    cudaEvent_t a, b;
+    DevTimer() {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, ctx().stream);
+    }
+    double stop() {
+        cudaEventRecord(b, ctx().stream);
+        H2F_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        return ms;
+    }
+};
+
+void h2d(void* dst, const void* src, size_t bytes) {
+    if (bytes) H2F_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx().stream));
+}
+
+}  // namespace
+
+int h2f_dense_svd(const double* R, int32_t m, int32_t n, double thresh, int32_t path, double* U, int32_t* kept,
+                  int32_t* sweeps, double* ms) {
+    return guard([&] {
+        if (m < 0 || n <= 0 || m > n || path < 0 || path > 2) throw Error(H2F_E_ARG, "bad svd arguments");
+        Region scr(size_t(64) << 20);
+        double* dR = scr.alloc_n<double>(int64_t(m) * n);
+        double* dU = scr.alloc_n<double>(int64_t(n) * n);
+        int32_t* dk = scr.alloc_n<int32_t>(1);
+        h2d(dR, R, sizeof(double) * m * n);
+        std::vector<SvdTask> t{SvdTask{dR, dU, m, n, dk, 0}};
+        std::vector<int32_t*> flags;
+        DevTimer tm;
+        if (path == 0) {
+            if (n > SMEM_DENSE_MAX_N) throw Error(H2F_E_ARG, "shared-memory Jacobi needs n <= 144");
+            launch_jacobi_smem(upload(t), 1, n, thresh, ctx().stream);
+        } else {
+            jacobi_multi_cta(t, thresh, scr, path == 2, &flags);
+        }
+        *ms = tm.stop();
+        int32_t k = 0, sw = -1;
+        d2h(&k, dk, sizeof(int32_t));
+        if (path != 0) d2h(&sw, flags[0] + 63, sizeof(int32_t));
+        ctx().sync();
+        d2h(U, dU, sizeof(double) * int64_t(k) * n);
+        ctx().sync();
+        *kept = k;
+        *sweeps = sw;
+    });
+}
+
+int h2f_dense_qr_r(const double* Y, int32_t n, int32_t wf, int32_t path, double* R, double* ms) {
+    return guard([&] {
+        if (n <= 0 || wf <= 0 || path < 0 || path > 1) throw Error(H2F_E_ARG, "bad qr arguments");
+        if (path == 0 && n > SMEM_DENSE_MAX_N) throw Error(H2F_E_ARG, "shared-memory TSQR needs n <= 144");
+        Region scr(size_t(64) << 20);
+        double* dY = scr.alloc_n<double>(int64_t(n) * wf);
+        const int m = std::min(n, wf);
+        double* dR = scr.alloc_n<double>(int64_t(n) * n);
+        h2d(dY, Y, sizeof(double) * int64_t(n) * wf);
+        DevTimer tm;
+        if (path == 0) {
+            std::vector<QrTask> t{QrTask{dY, dR, wf, n, wf, 0, wf, 0}};
+            launch_qr_r_smem(upload(t), 1, n, ctx().stream);
+        } else {
+            qr_r_blocked({QrTask{dY, dR, wf, n, wf, 0, wf, 0}}, scr);
+        }
+        *ms = tm.stop();
+        d2h(R, dR, sizeof(double) * int64_t(m) * n);
+        ctx().sync();
+    });
+}
+
+int h2f_dense_complement(const double* BT, int32_t s, int32_t kt, int32_t path, double* Q, double* ms) {
+    return guard([&] {
+        if (s <= 0 || kt < 0 || kt > s || path < 0 || path > 1) throw Error(H2F_E_ARG, "bad complement arguments");
+        Region scr(size_t(64) << 20);
+        double* dB = scr.alloc_n<double>(int64_t(std::max(kt, 1)) * s);
+        double* dW = scr.alloc_n<double>(int64_t(std::max(kt, 1)) * s);
+        double* dQ = scr.alloc_n<double>(int64_t(s) * s);
+        double* cs = scr.alloc_n<double>(int64_t(16) * s);
+        h2d(dB, BT, sizeof(double) * int64_t(kt) * s);
+        std::vector<ComplementTask> t{ComplementTask{dB, dW, dQ, cs, s, kt}};
+        DevTimer tm;
+        if (path == 0) launch_complement(upload(t), 1, ctx().stream);
+        else complement_blocked(t, scr);
+        *ms = tm.stop();
+        d2h(Q, dQ, sizeof(double) * int64_t(s) * s);
+        ctx().sync();
+    });
 }
 
 int h2f_matrix_create(const h2f_matrix_desc* desc, const double* vals, h2f_matrix* out) {

@@ -1,0 +1,118 @@
+// Host-side builders of the batched task lists (GEMM, copy) shared by the
+// factorization driver and the dense per-cluster orchestration.
+#pragma once
+#include <vector>
+
+#include "kernels.h"
+#include "runtime.h"
+
+namespace h2f {
+
+struct GemmBuild {
+    std::vector<GemmTask> tasks;
+    std::vector<GemmContrib> contribs;
+    std::vector<int64_t> tile_start{0};
+    int64_t norm_tiles = 0;
+    double flops = 0, bytes = 0;  // algorithmic work of the launch (profiler)
+
+    static int64_t tiles(int M, int N) { return cdiv(M, GEMM_TILE) * cdiv(N, GEMM_TILE); }
+    // returns the task's norm base (mode NORM) or -1
+    int64_t add(double* C, int64_t ldc, int M, int N, int mode, const GemmContrib* cs, size_t nc) {
+        if (M <= 0 || N <= 0) return -1;
+        GemmTask t{};
+        t.C = C;
+        t.ldc = ldc;
+        t.M = M;
+        t.N = N;
+        t.mode = mode;
+        t.tiles_n = int(cdiv(N, GEMM_TILE));
+        t.contrib_begin = int64_t(contribs.size());
+        for (size_t i = 1; i < nc; ++i)  // the kernel applies alpha once per task
+            if (cs[i].alpha != cs[0].alpha) throw Error(H2F_E_INTERNAL, "assertion: mixed alpha in one GEMM task");
+        contribs.insert(contribs.end(), cs, cs + nc);
+        t.contrib_end = int64_t(contribs.size());
+        for (size_t i = 0; i < nc; ++i) {
+            flops += 2.0 * M * N * cs[i].K;
+            bytes += 8.0 * (double(M) * cs[i].K + double(cs[i].K) * N);
+        }
+        bytes += mode == GEMM_ADD ? 16.0 * M * N : (mode == GEMM_STORE ? 8.0 * M * N : 0.0);
+        t.norm_base = -1;
+        const int64_t nt = tiles(M, N);
+        if (mode == GEMM_NORM) {
+            t.norm_base = norm_tiles;
+            norm_tiles += nt;
+        }
+        tasks.push_back(t);
+        tile_start.push_back(tile_start.back() + nt);
+        return t.norm_base;
+    }
+    int64_t add1(double* C, int64_t ldc, int M, int N, int mode, const GemmContrib& c) {
+        return add(C, ldc, M, N, mode, &c, 1);
+    }
+    void launch(int kid, double* norms = nullptr, double bytes_override = -1.0) {
+        if (tasks.empty()) return;
+        Context& X = ctx();
+        auto* dt = X.up.put(tasks);
+        auto* dc = X.up.put(contribs);
+        auto* ds = X.up.put(tile_start);
+        X.up.flush(X.stream);
+        ProfScope ps(kid, flops, bytes_override >= 0 ? bytes_override : bytes);
+        launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), tile_start.back(), norms, X.stream);
+    }
+};
+
+inline GemmContrib contrib(const double* A, int64_t lda, int transA, const double* B, int64_t ldb,
+                           int transB, int K, double alpha = 1.0) {
+    GemmContrib c{};
+    c.A = A;
+    c.lda = lda;
+    c.transA = transA;
+    c.B = B;
+    c.ldb = ldb;
+    c.transB = transB;
+    c.K = K;
+    c.alpha = alpha;
+    return c;
+}
+
+struct CopyBuild {
+    std::vector<CopyTask> tasks;
+    std::vector<int64_t> tile_start{0};
+    double bytes = 0;
+    void add(double* dst, int64_t ldd, int rows, int cols, const double* src, int64_t lds, int trans,
+             int mode, double alpha = 1.0) {
+        if (rows <= 0 || cols <= 0) return;
+        CopyTask t{};
+        t.dst = dst;
+        t.ldd = ldd;
+        t.rows = rows;
+        t.cols = cols;
+        t.src = src;
+        t.lds = lds;
+        t.trans = trans;
+        t.mode = mode;
+        t.alpha = alpha;
+        tasks.push_back(t);
+        tile_start.push_back(tile_start.back() + cdiv(rows, COPY_TILE) * cdiv(cols, COPY_TILE));
+        bytes += double(rows) * cols * (mode == COPY_ZERO ? 8.0 : (mode == COPY_ADD ? 24.0 : 16.0));
+    }
+    void zero(double* dst, int64_t ldd, int rows, int cols) { add(dst, ldd, rows, cols, nullptr, 0, 0, COPY_ZERO); }
+    void launch() {
+        if (tasks.empty()) return;
+        Context& X = ctx();
+        auto* dt = X.up.put(tasks);
+        auto* ds = X.up.put(tile_start);
+        X.up.flush(X.stream);
+        ProfScope ps(K_COPY, 0.0, bytes);
+        launch_copy_tasks(dt, ds, int32_t(tasks.size()), tile_start.back(), X.stream);
+    }
+};
+
+template <class T> inline T* upload(const std::vector<T>& v) {
+    Context& X = ctx();
+    T* d = X.up.put(v);
+    X.up.flush(X.stream);
+    return d;
+}
+
+}  // namespace h2f

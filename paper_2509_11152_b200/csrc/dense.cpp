@@ -1,0 +1,323 @@
+// Batched blocked Householder QR / complement / Jacobi orchestration.
+//
+// Every panel step advances all clusters of a batch together: one
+// cooperative panel launch (k_hh.cu, the clusters' CTA groups side by side,
+// in waves if they do not fit co-resident), then the trailing update
+// A -= V T^T (V^T A) as a split-K DMMA GEMM, a T multiply and a DMMA GEMM.
+#include "dense.h"
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "builders.h"
+
+namespace h2f {
+
+namespace {
+
+int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return sms;
+}
+
+constexpr int KCH = 1024;  // split-K chunk of the V^T A product
+
+struct PanelPlan {
+    int job, j0, nbp, Lp, ncta, chunk;
+};
+
+// CTA allocation of one wave: at least ceil(Lp / HH_CHUNK_MAX) CTAs per
+// job, spare CTAs to the jobs with the most rows per CTA
+void size_wave(std::vector<PanelPlan>& w, int cap) {
+    int total = 0;
+    for (auto& p : w) {
+        p.ncta = int(cdiv(p.Lp, HH_CHUNK_MAX));
+        total += p.ncta;
+    }
+    for (;;) {
+        PanelPlan* best = nullptr;
+        double most = 0;
+        for (auto& p : w) {
+            const double per = double(p.Lp) / p.ncta;
+            if (per >= 2.0 * 64 && per > most) {  // keep >= 64 rows per CTA
+                most = per;
+                best = &p;
+            }
+        }
+        if (!best || total >= cap) break;
+        ++best->ncta;
+        ++total;
+    }
+    for (auto& p : w) {
+        int ch = int(cdiv(p.Lp, p.ncta));
+        ch = std::max(HH_NB, (ch + 3) & ~3);
+        p.chunk = ch;
+        p.ncta = int(cdiv(p.Lp, ch));
+    }
+}
+
+}  // namespace
+
+void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
+    cudaStream_t st = ctx().stream;
+    const int cap = hh_panel_capacity(HH_CHUNK_MAX);
+    if (cap < 1) throw Error(H2F_E_INTERNAL, "assertion: Householder panel kernel cannot be resident");
+    int maxp = 0;
+    std::vector<double*> vbuf(jobs.size(), nullptr);
+    for (size_t i = 0; i < jobs.size(); ++i) {
+        maxp = std::max<int>(maxp, int(cdiv(jobs[i].nfac, HH_NB)));
+        jobs[i].Vt.clear();
+        jobs[i].T.clear();
+        if (!keep && jobs[i].nfac > 0) vbuf[i] = scr.alloc_n<double>(int64_t(HH_NB) * jobs[i].L);
+    }
+    for (int p = 0; p < maxp; ++p) {
+        const int j0 = p * HH_NB;
+        std::vector<PanelPlan> all;
+        for (size_t i = 0; i < jobs.size(); ++i) {
+            const HhJob& J = jobs[i];
+            if (j0 >= J.nfac) continue;
+            all.push_back({int(i), j0, std::min(HH_NB, J.nfac - j0), J.L - j0, 0, 0});
+        }
+        if (all.empty()) break;
+        // waves of co-resident CTA groups
+        std::vector<std::vector<PanelPlan>> waves(1);
+        int used = 0;
+        for (auto& pp : all) {
+            const int need = int(cdiv(pp.Lp, HH_CHUNK_MAX));
+            if (need > cap) throw Error(H2F_E_INTERNAL, "assertion: Householder panel taller than the device");
+            if (used + need > cap) {
+                waves.emplace_back();
+                used = 0;
+            }
+            waves.back().push_back(pp);
+            used += need;
+        }
+        GemmBuild gk, gu;
+        std::vector<HhTmulTask> tm;
+        int max_trail = 0;
+        for (auto& w : waves) {
+            size_wave(w, cap);
+            std::vector<HhPanelTask> tasks;
+            std::vector<int32_t> owner;
+            int cta0 = 0, max_chunk = HH_NB;
+            uint32_t* bars = scr.alloc_n<uint32_t>(2 * int64_t(w.size()));
+            H2F_CUDA(cudaMemsetAsync(bars, 0, sizeof(uint32_t) * 2 * w.size(), st));
+            for (size_t t = 0; t < w.size(); ++t) {
+                const PanelPlan& pp = w[t];
+                HhJob& J = jobs[pp.job];
+                HhPanelTask k{};
+                k.M = J.M;
+                k.ldm = J.ldm;
+                k.Vt = keep ? scr.alloc_n<double>(int64_t(HH_NB) * pp.Lp) : vbuf[pp.job];
+                k.T = scr.alloc_n<double>(HH_NB * HH_NB);
+                k.part = scr.alloc_n<double>(int64_t(pp.ncta + 1) * (HH_NB + 2));
+                k.gram = scr.alloc_n<double>(int64_t(pp.ncta) * HH_NB * HH_NB);
+                k.bar = bars + 2 * t;
+                k.L = J.L;
+                k.j0 = pp.j0;
+                k.nbp = pp.nbp;
+                k.chunk = pp.chunk;
+                k.cta0 = cta0;
+                k.ncta = pp.ncta;
+                tasks.push_back(k);
+                for (int c = 0; c < pp.ncta; ++c) owner.push_back(int32_t(t));
+                cta0 += pp.ncta;
+                max_chunk = std::max(max_chunk, pp.chunk);
+                J.Vt.push_back(k.Vt);
+                J.T.push_back(k.T);
+                // trailing update of columns [j0 + nbp, ntot), rows [j0, L)
+                const int ntrail = J.ntot - (pp.j0 + pp.nbp);
+                if (ntrail <= 0) continue;
+                const int L = pp.Lp, nch = int(cdiv(L, KCH));
+                double* At = J.M + int64_t(pp.j0 + pp.nbp) * J.ldm + pp.j0;  // ntrail x L, ld ldm
+                double* P = scr.alloc_n<double>(int64_t(nch) * pp.nbp * ntrail);
+                double* W2 = scr.alloc_n<double>(int64_t(pp.nbp) * ntrail);
+                for (int c = 0; c < nch; ++c) {
+                    const int kk = std::min(KCH, L - c * KCH);
+                    gk.add1(P + int64_t(c) * pp.nbp * ntrail, ntrail, pp.nbp, ntrail, GEMM_STORE,
+                            contrib(k.Vt + int64_t(c) * KCH, L, 0, At + int64_t(c) * KCH, J.ldm, 1, kk));
+                }
+                tm.push_back(HhTmulTask{P, k.T, W2, nch, pp.nbp, ntrail, 1});
+                max_trail = std::max(max_trail, ntrail);
+                gu.add1(At, J.ldm, ntrail, L, GEMM_ADD, contrib(W2, ntrail, 1, k.Vt, L, 0, pp.nbp, -1.0));
+            }
+            cudaError_t e = launch_hh_panel(upload(tasks), upload(owner), int32_t(owner.size()), max_chunk, st);
+            if (e != cudaSuccess)
+                throw Error(H2F_E_CUDA, std::string("cooperative Householder panel launch: ") + cudaGetErrorString(e));
+        }
+        gk.launch(-1);
+        if (!tm.empty()) launch_hh_tmul(upload(tm), int32_t(tm.size()), max_trail, st);
+        gu.launch(-1);
+    }
+}
+
+void hh_apply_q(const std::vector<HhJob>& jobs, const std::vector<HhApply>& xs, Region& scr) {
+    cudaStream_t st = ctx().stream;
+    int maxp = 0;
+    for (auto& J : jobs) maxp = std::max<int>(maxp, int(J.Vt.size()));
+    for (int p = maxp - 1; p >= 0; --p) {
+        GemmBuild g1, g2;
+        std::vector<HhTmulTask> tm;
+        int max_cols = 0;
+        for (size_t i = 0; i < jobs.size(); ++i) {
+            const HhJob& J = jobs[i];
+            const HhApply& X = xs[i];
+            if (p >= int(J.Vt.size()) || X.nx <= 0) continue;
+            const int j0 = p * HH_NB, nbp = std::min(HH_NB, J.nfac - j0), L = J.L - j0;
+            double* Xp = X.X + int64_t(j0) * X.ldx;  // L x nx
+            double* P = scr.alloc_n<double>(int64_t(nbp) * X.nx);
+            double* W = scr.alloc_n<double>(int64_t(nbp) * X.nx);
+            g1.add1(P, X.nx, nbp, X.nx, GEMM_STORE, contrib(J.Vt[p], L, 0, Xp, X.ldx, 0, L));
+            tm.push_back(HhTmulTask{P, J.T[p], W, 1, nbp, X.nx, 0});
+            max_cols = std::max(max_cols, X.nx);
+            g2.add1(Xp, X.ldx, L, X.nx, GEMM_ADD, contrib(J.Vt[p], L, 1, W, X.nx, 0, nbp, -1.0));
+        }
+        g1.launch(-1);
+        if (!tm.empty()) launch_hh_tmul(upload(tm), int32_t(tm.size()), max_cols, st);
+        g2.launch(-1);
+    }
+}
+
+void qr_r_blocked(const std::vector<QrTask>& tasks, Region& scr) {
+    std::vector<HhJob> jobs;
+    std::vector<RExtractTask> ex;
+    int maxn = 0;
+    for (auto& t : tasks) {
+        HhJob J;
+        J.M = t.Y;
+        J.ldm = t.ldy;
+        J.L = t.wf;
+        J.ntot = t.s;
+        J.nfac = std::min(t.s, t.wf);
+        jobs.push_back(J);
+        ex.push_back(RExtractTask{t.Y, t.R, t.ldy, J.nfac, t.s});
+        maxn = std::max(maxn, t.s);
+    }
+    hh_factor(jobs, scr, false);
+    launch_r_extract(upload(ex), int32_t(ex.size()), maxn, ctx().stream);
+}
+
+void complement_blocked(const std::vector<ComplementTask>& tasks, Region& scr) {
+    cudaStream_t st = ctx().stream;
+    std::vector<HhJob> jobs;
+    std::vector<HhApply> xs;
+    std::vector<EyeTask> eye;
+    CopyBuild cp, zero;
+    int maxr = 0;
+    for (auto& t : tasks) {
+        const int s = t.s, kt = t.kt, r = s - kt;
+        HhJob J;
+        J.M = t.W;
+        J.ldm = s;
+        J.L = s;
+        J.ntot = kt;
+        J.nfac = kt;
+        jobs.push_back(J);
+        cp.add(t.W, s, kt, s, t.BT, s, 0, COPY_SET);     // the QR works on a copy of b_aug
+        cp.add(t.Q + r, s, s, kt, t.BT, s, 1, COPY_SET);  // trailing columns: b_aug itself
+        zero.zero(t.Q, s, s, r);
+        if (r > 0) eye.push_back(EyeTask{t.Q, s, kt, r});
+        xs.push_back(HhApply{t.Q, s, r});
+        maxr = std::max(maxr, r);
+    }
+    zero.launch();
+    cp.launch();
+    launch_set_eye(upload(eye), int32_t(eye.size()), maxr, st);
+    hh_factor(jobs, scr, true);
+    hh_apply_q(jobs, xs, scr);
+}
+
+namespace {
+
+// one cooperative launch over `idx` tasks; block-cyclic unless forced pairwise
+void jacobi_wave(const std::vector<SvdTask>& tasks, const std::vector<size_t>& idx, bool pairwise, double thresh,
+                 Region& scr, std::vector<int32_t*>* flags_out) {
+    cudaStream_t st = ctx().stream;
+    int max_n = 1, max_m = 1;
+    for (size_t i : idx) {
+        max_n = std::max(max_n, tasks[i].n);
+        max_m = std::max(max_m, tasks[i].m);
+    }
+    const int jb = jacobi_block_rows(max_n);
+    const int cap = pairwise ? jacobi_coop_capacity(max_n, max_m) : jacobi_block_capacity(max_n, max_m);
+    constexpr int WARPS = 8;  // pairs per CTA and step (pairwise version)
+    std::vector<int> want;
+    int total = 0;
+    for (size_t i : idx) {
+        const int m = tasks[i].m;
+        want.push_back(std::max<int>(1, int(pairwise ? cdiv((m + 1) / 2, WARPS) : cdiv(m, 2 * jb))));
+        total += want.back();
+    }
+    while (pairwise && total > cap) {  // the pairwise version loops over pairs: shrink to fit
+        auto it = std::max_element(want.begin(), want.end());
+        if (*it <= 1) break;
+        --*it;
+        --total;
+    }
+    if (total > cap) throw Error(H2F_E_INTERNAL, "assertion: too many clusters for the co-resident Jacobi");
+    uint32_t* bars = scr.alloc_n<uint32_t>(2 * idx.size());
+    int32_t* flags = scr.alloc_n<int32_t>(64 * idx.size());
+    H2F_CUDA(cudaMemsetAsync(bars, 0, sizeof(uint32_t) * 2 * idx.size(), st));
+    H2F_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * 64 * idx.size(), st));
+    std::vector<CoopSvdTask> ct;
+    std::vector<int32_t> owner;
+    int cta0 = 0;
+    for (size_t w = 0; w < idx.size(); ++w) {
+        const SvdTask& t = tasks[idx[w]];
+        ct.push_back(CoopSvdTask{t, cta0, want[w], bars + 2 * w, flags + 64 * w, scr.alloc_n<double>(std::max(t.m, 1))});
+        for (int c = 0; c < want[w]; ++c) owner.push_back(int32_t(w));
+        cta0 += want[w];
+        if (flags_out) (*flags_out)[idx[w]] = flags + 64 * w;
+    }
+    cudaError_t e = pairwise ? launch_jacobi_coop(upload(ct), int32_t(owner.size()), upload(owner), max_n, max_m,
+                                                  thresh, st)
+                             : launch_jacobi_block(upload(ct), int32_t(owner.size()), upload(owner), max_n, max_m,
+                                                   thresh, st);
+    if (e != cudaSuccess) throw Error(H2F_E_CUDA, std::string("cooperative Jacobi launch: ") + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+void jacobi_multi_cta(const std::vector<SvdTask>& tasks, double thresh, Region& scr, bool pairwise,
+                      std::vector<int32_t*>* flags_out) {
+    static const bool env_pairwise = std::getenv("H2F_JACOBI_PAIRWISE") != nullptr;
+    if (flags_out) flags_out->assign(tasks.size(), nullptr);
+    if (pairwise || env_pairwise) {
+        std::vector<size_t> all(tasks.size());
+        for (size_t i = 0; i < tasks.size(); ++i) all[i] = i;
+        jacobi_wave(tasks, all, true, thresh, scr, flags_out);
+        return;
+    }
+    int max_n = 1, max_m = 1;
+    for (auto& t : tasks) {
+        max_n = std::max(max_n, t.n);
+        max_m = std::max(max_m, t.m);
+    }
+    const int jb = jacobi_block_rows(max_n);
+    const int cap = jacobi_block_capacity(max_n, max_m);
+    // waves of co-resident clusters; a cluster wider than the device runs pairwise
+    std::vector<size_t> wave;
+    int used = 0;
+    for (size_t i = 0; i < tasks.size(); ++i) {
+        const int need = std::max<int>(1, int(cdiv(tasks[i].m, 2 * jb)));
+        if (need > cap) {
+            jacobi_wave(tasks, {i}, true, thresh, scr, flags_out);
+            continue;
+        }
+        if (used + need > cap) {
+            jacobi_wave(tasks, wave, false, thresh, scr, flags_out);
+            wave.clear();
+            used = 0;
+        }
+        wave.push_back(i);
+        used += need;
+    }
+    if (!wave.empty()) jacobi_wave(tasks, wave, false, thresh, scr, flags_out);
+}
+
+}  // namespace h2f

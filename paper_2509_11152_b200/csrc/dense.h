@@ -1,0 +1,46 @@
+// Batched per-cluster dense linear algebra, host orchestration (the large-n
+// paths of the augmentation, factorization.py:62-99).
+#pragma once
+#include <vector>
+
+#include "kernels.h"
+#include "runtime.h"
+
+namespace h2f {
+
+// One matrix of a batched blocked Householder QR.  Column j lives at
+// M + j*ldm with its L rows contiguous (e.g. the rows of a row-major Z are
+// the columns of Z^T).  Columns [0, nfac) are factored; the trailing
+// updates reach columns [0, ntot).  With keep=true the per-panel Vt / T are
+// retained for hh_apply_q.
+struct HhJob {
+    double* M = nullptr;
+    int64_t ldm = 0;
+    int L = 0, ntot = 0, nfac = 0;
+    std::vector<double*> Vt, T;  // per panel (keep=true)
+};
+
+void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep);
+
+// X <- Q X with Q = H_0 ... H_{nfac-1} of job i; X_i is L x nx, row-major ld ldx
+struct HhApply {
+    double* X;
+    int64_t ldx;
+    int nx;
+};
+void hh_apply_q(const std::vector<HhJob>& jobs, const std::vector<HhApply>& xs, Region& scr);
+
+// R (min(n,wf) x n, row-major ld n) of the QR of Y^T for the QrTasks (Y is n x wf,
+// row-major; overwritten)
+void qr_r_blocked(const std::vector<QrTask>& tasks, Region& scr);
+
+// Q~ = [complement | b_aug] for each task (factorization.py:88-99), blocked
+void complement_blocked(const std::vector<ComplementTask>& tasks, Region& scr);
+
+// one-sided Jacobi SVD of large R's with several co-resident CTAs per cluster
+// (block-cyclic; pairwise = one group barrier per round-robin step).  With
+// flags_out, flags_out[i][63] receives the sweep count of task i (device).
+void jacobi_multi_cta(const std::vector<SvdTask>& tasks, double thresh, Region& scr, bool pairwise = false,
+                      std::vector<int32_t*>* flags_out = nullptr);
+
+}  // namespace h2f

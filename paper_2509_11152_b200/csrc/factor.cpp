@@ -24,6 +24,8 @@
 #include <numeric>
 #include <set>
 
+#include "builders.h"
+#include "dense.h"
 #include "factor.h"
 
 namespace h2f {
@@ -137,112 +139,6 @@ struct Lvl {
     }
 };
 
-// ---- launch builders -----------------------------------------------------------
-struct GemmBuild {
-    std::vector<GemmTask> tasks;
-    std::vector<GemmContrib> contribs;
-    std::vector<int64_t> tile_start{0};
-    int64_t norm_tiles = 0;
-    double flops = 0, bytes = 0;  // algorithmic work of the launch (profiler)
-
-    static int64_t tiles(int M, int N) { return cdiv(M, GEMM_TILE) * cdiv(N, GEMM_TILE); }
-    // returns the task's norm base (mode NORM) or -1
-    int64_t add(double* C, int64_t ldc, int M, int N, int mode, const GemmContrib* cs, size_t nc) {
-        if (M <= 0 || N <= 0) return -1;
-        GemmTask t{};
-        t.C = C;
-        t.ldc = ldc;
-        t.M = M;
-        t.N = N;
-        t.mode = mode;
-        t.tiles_n = int(cdiv(N, GEMM_TILE));
-        t.contrib_begin = int64_t(contribs.size());
-        contribs.insert(contribs.end(), cs, cs + nc);
-        t.contrib_end = int64_t(contribs.size());
-        for (size_t i = 0; i < nc; ++i) {
-            flops += 2.0 * M * N * cs[i].K;
-            bytes += 8.0 * (double(M) * cs[i].K + double(cs[i].K) * N);
-        }
-        bytes += mode == GEMM_ADD ? 16.0 * M * N : (mode == GEMM_STORE ? 8.0 * M * N : 0.0);
-        t.norm_base = -1;
-        const int64_t nt = tiles(M, N);
-        if (mode == GEMM_NORM) {
-            t.norm_base = norm_tiles;
-            norm_tiles += nt;
-        }
-        tasks.push_back(t);
-        tile_start.push_back(tile_start.back() + nt);
-        return t.norm_base;
-    }
-    int64_t add1(double* C, int64_t ldc, int M, int N, int mode, const GemmContrib& c) {
-        return add(C, ldc, M, N, mode, &c, 1);
-    }
-    void launch(int kid, double* norms = nullptr, double bytes_override = -1.0) {
-        if (tasks.empty()) return;
-        Context& X = ctx();
-        auto* dt = X.up.put(tasks);
-        auto* dc = X.up.put(contribs);
-        auto* ds = X.up.put(tile_start);
-        X.up.flush(X.stream);
-        ProfScope ps(kid, flops, bytes_override >= 0 ? bytes_override : bytes);
-        launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), tile_start.back(), norms, X.stream);
-    }
-};
-
-inline GemmContrib contrib(const double* A, int64_t lda, int transA, const double* B, int64_t ldb,
-                           int transB, int K, double alpha = 1.0) {
-    GemmContrib c{};
-    c.A = A;
-    c.lda = lda;
-    c.transA = transA;
-    c.B = B;
-    c.ldb = ldb;
-    c.transB = transB;
-    c.K = K;
-    c.alpha = alpha;
-    return c;
-}
-
-struct CopyBuild {
-    std::vector<CopyTask> tasks;
-    std::vector<int64_t> tile_start{0};
-    double bytes = 0;
-    void add(double* dst, int64_t ldd, int rows, int cols, const double* src, int64_t lds, int trans,
-             int mode, double alpha = 1.0) {
-        if (rows <= 0 || cols <= 0) return;
-        CopyTask t{};
-        t.dst = dst;
-        t.ldd = ldd;
-        t.rows = rows;
-        t.cols = cols;
-        t.src = src;
-        t.lds = lds;
-        t.trans = trans;
-        t.mode = mode;
-        t.alpha = alpha;
-        tasks.push_back(t);
-        tile_start.push_back(tile_start.back() + cdiv(rows, COPY_TILE) * cdiv(cols, COPY_TILE));
-        bytes += double(rows) * cols * (mode == COPY_ZERO ? 8.0 : (mode == COPY_ADD ? 24.0 : 16.0));
-    }
-    void zero(double* dst, int64_t ldd, int rows, int cols) { add(dst, ldd, rows, cols, nullptr, 0, 0, COPY_ZERO); }
-    void launch() {
-        if (tasks.empty()) return;
-        Context& X = ctx();
-        auto* dt = X.up.put(tasks);
-        auto* ds = X.up.put(tile_start);
-        X.up.flush(X.stream);
-        ProfScope ps(K_COPY, 0.0, bytes);
-        launch_copy_tasks(dt, ds, int32_t(tasks.size()), tile_start.back(), X.stream);
-    }
-};
-
-template <class T> T* upload(const std::vector<T>& v) {
-    Context& X = ctx();
-    T* d = X.up.put(v);
-    X.up.flush(X.stream);
-    return d;
-}
-
 // phase accounting from CUDA events (sums to the device-side wall time)
 class PhaseClock {
   public:
@@ -271,6 +167,23 @@ class PhaseClock {
     std::vector<std::pair<cudaEvent_t, int>> marks_;
 };
 
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
+// Q~ for a set of clusters: one CTA per cluster up to H2F_HH_MIN_S rows,
+// the blocked Householder with cooperative panels above
+void complement(const std::vector<ComplementTask>& tasks, Region& scr) {
+    static const int min_s = env_int("H2F_HH_MIN_S", 128);
+    int lim = min_s;
+    if (const char* env = std::getenv("H2F_SMALL_N_MAX")) lim = std::min(lim, std::atoi(env));
+    std::vector<ComplementTask> small, big;
+    for (auto& t : tasks) (t.s > lim && t.kt > 0 ? big : small).push_back(t);
+    if (!small.empty()) launch_complement(upload(small), int32_t(small.size()), ctx().stream);
+    if (!big.empty()) complement_blocked(big, scr);
+}
+
 class Factorizer {
   public:
     Factorizer(H2Mat& m, Factorization& f) : M(m), F(f) {}
@@ -293,8 +206,6 @@ class Factorizer {
     std::chrono::steady_clock::time_point level_t0;
     void dump_level_profile(int level);
 
-    void blocked_qr(const std::vector<QrTask>& tasks, Region& scr);
-    void jacobi_multi_cta(const std::vector<SvdTask>& tasks, Region& scr);
     std::unique_ptr<Lvl> leaf_level(int level);
     void attach_couplings(Lvl& L);
     void process_batch(Lvl& L, const std::vector<int>& batch);
@@ -305,108 +216,6 @@ class Factorizer {
     std::vector<std::pair<int, int>> dense_pairs(int level) const;
 };
 
-
-// R of QR(Z^T) for large n: blocked Householder, panels of BQR_NB columns
-// (bqr_panel) + split-K V^T M_trail (DMMA) + T^T reduction + trailing update
-// M_trail -= V W2 (DMMA).  All clusters of the batch advance together.
-void Factorizer::blocked_qr(const std::vector<QrTask>& tasks, Region& scr) {
-    cudaStream_t st = ctx().stream;
-    constexpr int KCH = 1024;
-    struct Q_ {
-        QrTask t;
-        int nref;
-        double *V, *T, *P, *W2;
-    };
-    std::vector<Q_> q;
-    int maxp = 0;
-    for (auto& t : tasks) {
-        Q_ x;
-        x.t = t;
-        x.nref = std::min(t.s, t.wf);
-        x.V = scr.alloc_n<double>(int64_t(BQR_NB) * t.wf);
-        x.T = scr.alloc_n<double>(BQR_NB * BQR_NB);
-        x.P = scr.alloc_n<double>(cdiv(t.wf, KCH) * BQR_NB * int64_t(t.s));
-        x.W2 = scr.alloc_n<double>(int64_t(BQR_NB) * t.s);
-        maxp = std::max<int>(maxp, int(cdiv(x.nref, BQR_NB)));
-        q.push_back(x);
-    }
-    for (int p = 0; p < maxp; ++p) {
-        std::vector<BqrPanelTask> pan;
-        std::vector<BqrReduceTask> red;
-        GemmBuild gk, gu;
-        int max_trail = 0;
-        for (auto& x : q) {
-            const int j0 = p * BQR_NB;
-            if (j0 >= x.nref) continue;
-            const int nbp = std::min(BQR_NB, x.nref - j0);
-            const int n = x.t.s, wf = x.t.wf, L = wf - j0;
-            pan.push_back(BqrPanelTask{x.t.Y, x.V, x.T, x.t.ldy, wf, j0, nbp, 0});
-            const int ntrail = n - (j0 + nbp);
-            if (ntrail <= 0) continue;
-            const int nch = int(cdiv(L, KCH));
-            double* Zt = x.t.Y + int64_t(j0 + nbp) * x.t.ldy + j0;
-            for (int ch = 0; ch < nch; ++ch) {
-                const int k = std::min(KCH, L - ch * KCH);
-                gk.add1(x.P + int64_t(ch) * BQR_NB * ntrail, ntrail, BQR_NB, ntrail, GEMM_STORE,
-                        contrib(x.V + int64_t(ch) * KCH, L, 0, Zt + int64_t(ch) * KCH, x.t.ldy, 1, k));
-            }
-            red.push_back(BqrReduceTask{x.P, x.T, x.W2, nch, ntrail});
-            max_trail = std::max(max_trail, ntrail);
-            gu.add1(Zt, x.t.ldy, ntrail, L, GEMM_ADD, contrib(x.W2, ntrail, 1, x.V, L, 0, nbp, -1.0));
-        }
-        if (pan.empty()) break;
-        launch_bqr_panel(upload(pan), int32_t(pan.size()), st);
-        gk.launch(-1);
-        if (!red.empty()) launch_bqr_reduce(upload(red), int32_t(red.size()), max_trail, st);
-        gu.launch(-1);
-    }
-    std::vector<RExtractTask> ex;
-    int maxn = 0;
-    for (auto& x : q) {
-        ex.push_back(RExtractTask{x.t.Y, x.t.R, x.t.ldy, x.nref, x.t.s});
-        maxn = std::max(maxn, x.t.s);
-    }
-    launch_r_extract(upload(ex), int32_t(ex.size()), maxn, st);
-}
-
-// Jacobi SVD for large n: several co-resident CTAs per cluster
-void Factorizer::jacobi_multi_cta(const std::vector<SvdTask>& tasks, Region& scr) {
-    cudaStream_t st = ctx().stream;
-    int sms = 148;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    std::vector<int> want(tasks.size());
-    int total = 0;
-    for (size_t i = 0; i < tasks.size(); ++i) {
-        want[i] = std::max<int>(1, int(cdiv((tasks[i].m + 1) / 2, 16)));
-        total += want[i];
-    }
-    while (total > sms) {  // shrink the largest allocations until co-resident
-        auto it = std::max_element(want.begin(), want.end());
-        if (*it <= 1) break;
-        --*it;
-        --total;
-    }
-    if (total > sms) throw Error(H2F_E_INTERNAL, "assertion: too many clusters for the co-resident Jacobi");
-    uint32_t* bars = scr.alloc_n<uint32_t>(2 * tasks.size());
-    int32_t* flags = scr.alloc_n<int32_t>(64 * tasks.size());
-    H2F_CUDA(cudaMemsetAsync(bars, 0, sizeof(uint32_t) * 2 * tasks.size(), st));
-    H2F_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * 64 * tasks.size(), st));
-    std::vector<CoopSvdTask> ct;
-    std::vector<int32_t> owner;
-    int cta0 = 0;
-    for (size_t i = 0; i < tasks.size(); ++i) {
-        ct.push_back(CoopSvdTask{tasks[i], cta0, want[i], bars + 2 * i, flags + 64 * i});
-        for (int c = 0; c < want[i]; ++c) owner.push_back(int32_t(i));
-        cta0 += want[i];
-    }
-    auto* dct = upload(ct);
-    auto* down = upload(owner);
-    launch_jacobi_coop(dct, int32_t(owner.size()), down, drop, st);
-}
 
 std::vector<std::pair<int, int>> Factorizer::dense_pairs(int level) const {
     std::vector<std::pair<int, int>> out(M.inner[level]);
@@ -512,6 +321,9 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         int small_n_max = SMEM_DENSE_MAX_N;
         if (const char* env = std::getenv("H2F_SMALL_N_MAX"))
             small_n_max = std::min(SMEM_DENSE_MAX_N, std::atoi(env));
+        // the shared-memory TSQR serves n <= hh_min_n; above, the blocked
+        // Householder with cooperative panels (dense.cpp)
+        const int hh_min_n = std::min(small_n_max, env_int("H2F_HH_MIN_N", 32));
         H2F_CUDA(cudaMemsetAsync(kept_d, 0, sizeof(int) * nb, st));
         for (int bi = 0; bi < nb; ++bi) {
             const int c = batch[bi], ci = L.at(c);
@@ -554,7 +366,9 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             A.U = scr.alloc_n<double>(int64_t(n) * n);
             const int m = std::min(n, wf);
             SvdTask sv{R, A.U, m, n, kept_d + bi, 0};
-            if (n <= small_n_max) {
+            if (n > hh_min_n) {
+                qr_big.push_back(QrTask{Z, R, wf, n, wf, 0, wf, 0});
+            } else {
                 // two-level TSQR: segments of <= seg columns fold into
                 // their own R (written transposed side by side), then one
                 // CTA folds the stacked R's
@@ -569,10 +383,11 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 } else {
                     qr_small.push_back(QrTask{Z, R, wf, n, wf, 0, wf, 0});
                 }
+            }
+            if (n <= small_n_max) {
                 svd_small.push_back(sv);
                 max_n_small = std::max(max_n_small, n);
             } else {
-                qr_big.push_back(QrTask{Z, R, wf, n, wf, 0, wf, 0});
                 svd_big.push_back(sv);
             }
         }
@@ -583,33 +398,47 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             cb += 16.0 * double(t.s) * t.s;
         }
         {
-            ProfScope ps(K_COMPLEMENT, cf, cb);
-            launch_complement(upload(cmpV), int32_t(cmpV.size()), st);
+            ProfScope ps(K_COMPLEMENT_V, cf, cb);
+            complement(cmpV, scr);
         }
         gz.launch(K_GEMM_AUG);
-        double qf = 0, qb = 0, jf = 0, jb = 0;
-        for (auto* v : {&qr_small, &qr_big})
-            for (auto& t : *v) {
+        auto qr_work = [](const std::vector<QrTask>& v, double& f, double& b) {
+            for (auto& t : v) {
                 const double n = t.s, w = t.wf;
-                qf += 2.0 * w * n * n - (w >= n ? 2.0 / 3.0 * n * n * n : 0.0);
-                qb += 8.0 * n * w + 8.0 * n * n;
+                f += 2.0 * w * n * n - (w >= n ? 2.0 / 3.0 * n * n * n : 0.0);
+                b += 8.0 * n * w + 8.0 * n * n;
             }
-        for (auto* v : {&svd_small, &svd_big})
-            for (auto& t : *v) {
-                jf += 22.0 * double(t.m) * t.m * t.n;  // c_svd = 22 convention
-                jb += 16.0 * double(t.m) * t.n;
+        };
+        auto svd_work = [](const std::vector<SvdTask>& v, double& f, double& b) {
+            for (auto& t : v) {
+                f += 22.0 * double(t.m) * t.m * t.n;  // c_svd = 22 convention
+                b += 16.0 * double(t.m) * t.n;
             }
-        {
-            ProfScope ps(K_QR, qf, qb);
+        };
+        if (!qr_small.empty()) {
+            double f = 0, b = 0;
+            qr_work(qr_small, f, b);
+            ProfScope ps(K_QR, f, b);
             if (!qr_seg.empty()) launch_qr_r_smem(upload(qr_seg), int32_t(qr_seg.size()), max_n_small, st);
-            if (!qr_small.empty()) launch_qr_r_smem(upload(qr_small), int32_t(qr_small.size()), max_n_small, st);
-            if (!qr_big.empty()) blocked_qr(qr_big, scr);
+            launch_qr_r_smem(upload(qr_small), int32_t(qr_small.size()), max_n_small, st);
         }
-        {
-            ProfScope ps(K_JACOBI, jf, jb);
-            if (!svd_small.empty())
-                launch_jacobi_smem(upload(svd_small), int32_t(svd_small.size()), max_n_small, drop, st);
-            if (!svd_big.empty()) jacobi_multi_cta(svd_big, scr);
+        if (!qr_big.empty()) {
+            double f = 0, b = 0;
+            qr_work(qr_big, f, b);
+            ProfScope ps(K_QR_BIG, f, b);
+            qr_r_blocked(qr_big, scr);
+        }
+        if (!svd_small.empty()) {
+            double f = 0, b = 0;
+            svd_work(svd_small, f, b);
+            ProfScope ps(K_JACOBI, f, b);
+            launch_jacobi_smem(upload(svd_small), int32_t(svd_small.size()), max_n_small, drop, st);
+        }
+        if (!svd_big.empty()) {
+            double f = 0, b = 0;
+            svd_work(svd_big, f, b);
+            ProfScope ps(K_JACOBI_BIG, f, b);
+            jacobi_multi_cta(svd_big, drop, scr);
         }
     }
     int* kept_h = static_cast<int*>(X.pinned_buf(sizeof(int) * nb));
@@ -652,7 +481,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         {
             ProfScope ps(K_COMPLEMENT, rf + cf, cb);
             if (!ro.empty()) launch_reorth(upload(ro), int32_t(ro.size()), st);
-            if (!cmp.empty()) launch_complement(upload(cmp), int32_t(cmp.size()), st);
+            if (!cmp.empty()) complement(cmp, scr);
         }
     }
     for (int bi = 0; bi < nb; ++bi) {

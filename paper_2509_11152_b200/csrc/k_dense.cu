@@ -1,6 +1,6 @@
 // Per-cluster dense linear algebra, batched: one CTA per cluster of a batch.
 //
-//   qr_r        R of the reduced Householder QR of Y^T (Y = fill residual)   factorization.py:78
+//   qr_r_smem   R of the reduced Householder QR of Y^T (Y = fill residual)   factorization.py:78
 //   jacobi      one-sided Jacobi SVD of R^T, kept count, re-orthogonalised
 //               new directions -> b_aug^T                                     factorization.py:79-84
 //   complement  complete Householder QR of b_aug -> Q~ = [complement|b_aug]   factorization.py:88-99
@@ -11,6 +11,7 @@
 // Working matrices live in global memory (L1/L2 resident at these sizes) and
 // are updated with CTA-wide barriers; reductions use a fixed order so the
 // results are run-to-run deterministic.
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -34,46 +35,6 @@ __device__ __forceinline__ void reflector(double alpha, double ss, double& beta,
         beta = -copysign(hypot(alpha, xnorm), alpha);
         tau = (beta - alpha) / beta;
         scal = 1.0 / (alpha - beta);
-    }
-}
-
-__global__ void __launch_bounds__(DT) qr_r_kernel(const QrTask* __restrict__ tasks) {
-    const QrTask T = tasks[blockIdx.x];
-    __shared__ double sh[DT / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = DT / 32;
-    const int s = T.s, wf = T.wf;
-    const int nref = s < wf ? s : wf;
-    for (int j = 0; j < nref; ++j) {
-        double* yj = T.Y + (int64_t)j * T.ldy;
-        double ss = 0.0;
-        for (int i = j + 1 + threadIdx.x; i < wf; i += DT) ss += yj[i] * yj[i];
-        ss = block_sum(ss, sh);
-        const double alpha = yj[j];
-        double beta, tau, scal;
-        reflector(alpha, ss, beta, tau, scal);
-        if (tau != 0.0)
-            for (int i = j + 1 + threadIdx.x; i < wf; i += DT) yj[i] *= scal;
-        if (threadIdx.x == 0) {
-            double* rj = T.R + (int64_t)j * s;
-            rj[j] = beta;
-            for (int c = 0; c < j; ++c) rj[c] = 0.0;
-        }
-        __syncthreads();
-        for (int c = j + 1 + warp; c < s; c += nw) {
-            double* yc = T.Y + (int64_t)c * T.ldy;
-            double d = 0.0;
-            for (int i = j + 1 + lane; i < wf; i += 32) d += yj[i] * yc[i];
-            d = warp_sum(d) + yc[j];
-            if (tau != 0.0) {
-                d *= tau;
-                for (int i = j + 1 + lane; i < wf; i += 32) yc[i] -= d * yj[i];
-                __syncwarp();
-                if (lane == 0) yc[j] -= d;
-            }
-            __syncwarp();
-            if (lane == 0) T.R[(int64_t)j * s + c] = yc[j];
-        }
-        __syncthreads();
     }
 }
 
@@ -222,18 +183,6 @@ __device__ void jacobi_finish(const double* A, int m, int n, double thresh, doub
     }
 }
 
-__global__ void __launch_bounds__(DT) jacobi_kernel(const SvdTask* __restrict__ tasks, double thresh) {
-    const SvdTask T = tasks[blockIdx.x];
-    extern __shared__ double dsh[];  // sig[m] then rank (int) [m]
-    __shared__ int flag, kept_s;
-    if (T.m == 0) {
-        if (threadIdx.x == 0) *T.kept_out = 0;
-        return;
-    }
-    jacobi_sweeps(T.R, T.m, T.n, &flag);
-    jacobi_finish(T.R, T.m, T.n, thresh, dsh, reinterpret_cast<int*>(dsh + T.m), &kept_s, T.U, T.kept_out);
-}
-
 __global__ void __launch_bounds__(DT) jacobi_smem_kernel(const SvdTask* __restrict__ tasks, double thresh) {
     const SvdTask T = tasks[blockIdx.x];
     extern __shared__ double dsh[];  // A[m*n], sig[m], rank[m]
@@ -344,115 +293,6 @@ __global__ void __launch_bounds__(DT) complement_kernel(const ComplementTask* __
     }
 }
 
-// ---- blocked Householder QR (large n) --------------------------------------
-// Panel: factor columns j0..j0+nbp-1 of M = Z^T (rows of Z) in place, then
-// write the explicit reflectors V (unit lower, BQR_NB x L) and the compact-WY
-// factor T (LAPACK dlarft, forward/columnwise).  The trailing update
-// M_trail -= V (T^T (V^T M_trail)) runs on the DMMA tile GEMM.
-__global__ void __launch_bounds__(DT) bqr_panel_kernel(const BqrPanelTask* __restrict__ tasks) {
-    const BqrPanelTask T = tasks[blockIdx.x];
-    __shared__ double sh[DT / 32];
-    __shared__ double taus[BQR_NB];
-    __shared__ double G[BQR_NB][BQR_NB];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = DT / 32;
-    const int wf = T.wf, j0 = T.j0, nbp = T.nbp, L = wf - j0;
-    for (int jj = 0; jj < nbp; ++jj) {
-        const int j = j0 + jj;
-        double* zj = T.Z + (int64_t)j * T.ldz;
-        double ss = 0.0;
-        for (int i = j + 1 + threadIdx.x; i < wf; i += DT) ss += zj[i] * zj[i];
-        ss = block_sum(ss, sh);
-        double beta, tau, scal;
-        reflector(zj[j], ss, beta, tau, scal);
-        if (tau != 0.0)
-            for (int i = j + 1 + threadIdx.x; i < wf; i += DT) zj[i] *= scal;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            zj[j] = beta;
-            taus[jj] = tau;
-        }
-        if (tau != 0.0)
-            for (int c = jj + 1 + warp; c < nbp; c += nw) {
-                double* zc = T.Z + (int64_t)(j0 + c) * T.ldz;
-                double d = 0.0;
-                for (int i = j + 1 + lane; i < wf; i += 32) d += zj[i] * zc[i];
-                d = (warp_sum(d) + zc[j]) * tau;
-                for (int i = j + 1 + lane; i < wf; i += 32) zc[i] -= d * zj[i];
-                __syncwarp();
-                if (lane == 0) zc[j] -= d;
-            }
-        __syncthreads();
-    }
-    // explicit V
-    for (int64_t e = threadIdx.x; e < (int64_t)BQR_NB * L; e += DT) {
-        const int jj = (int)(e / L), ip = (int)(e % L);
-        const int i = j0 + ip, j = j0 + jj;
-        double v = 0.0;
-        if (jj < nbp) v = (i < j) ? 0.0 : (i == j ? 1.0 : T.Z[(int64_t)j * T.ldz + i]);
-        T.V[e] = v;
-    }
-    __syncthreads();
-    // Gram V V^T (warp a computes row a)
-    if (warp < BQR_NB) {
-        const int a = warp;
-        double acc[BQR_NB];
-#pragma unroll
-        for (int b = 0; b < BQR_NB; ++b) acc[b] = 0.0;
-        const double* va = T.V + (int64_t)a * L;
-        for (int ip = lane; ip < L; ip += 32) {
-            const double x = va[ip];
-#pragma unroll
-            for (int b = 0; b < BQR_NB; ++b) acc[b] += x * T.V[(int64_t)b * L + ip];
-        }
-#pragma unroll
-        for (int b = 0; b < BQR_NB; ++b) {
-            const double g = warp_sum(acc[b]);
-            if (lane == 0) G[a][b] = g;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double Tm[BQR_NB][BQR_NB];
-        for (int a = 0; a < BQR_NB; ++a)
-            for (int b = 0; b < BQR_NB; ++b) Tm[a][b] = 0.0;
-        for (int jj = 0; jj < nbp; ++jj) {
-            const double tau = taus[jj];
-            double tmp[BQR_NB];
-            for (int a = 0; a < jj; ++a) tmp[a] = -tau * G[a][jj];
-            for (int a = 0; a < jj; ++a) {
-                double acc = 0.0;
-                for (int b = a; b < jj; ++b) acc += Tm[a][b] * tmp[b];
-                Tm[a][jj] = acc;
-            }
-            Tm[jj][jj] = tau;
-        }
-        for (int a = 0; a < BQR_NB; ++a)
-            for (int b = 0; b < BQR_NB; ++b) T.T[a * BQR_NB + b] = Tm[a][b];
-    }
-}
-
-// W2[a][c] = sum_b T[b][a] * (sum_chunks P[chunk][b][c])
-__global__ void bqr_reduce_kernel(const BqrReduceTask* __restrict__ tasks) {
-    const BqrReduceTask R = tasks[blockIdx.y];
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= R.ntrail) return;
-    double S[BQR_NB];
-#pragma unroll
-    for (int b = 0; b < BQR_NB; ++b) S[b] = 0.0;
-    for (int ch = 0; ch < R.nchunks; ++ch) {
-        const double* P = R.P + (int64_t)ch * BQR_NB * R.ntrail;
-#pragma unroll
-        for (int b = 0; b < BQR_NB; ++b) S[b] += P[(int64_t)b * R.ntrail + c];
-    }
-#pragma unroll
-    for (int a = 0; a < BQR_NB; ++a) {
-        double acc = 0.0;
-#pragma unroll
-        for (int b = 0; b <= a; ++b) acc += R.T[b * BQR_NB + a] * S[b];
-        R.W2[(int64_t)a * R.ntrail + c] = acc;
-    }
-}
-
 __global__ void r_extract_kernel(const RExtractTask* __restrict__ tasks) {
     const RExtractTask X = tasks[blockIdx.y];
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -463,8 +303,12 @@ __global__ void r_extract_kernel(const RExtractTask* __restrict__ tasks) {
 
 // ---- multi-CTA Jacobi (large n) ---------------------------------------------
 // CTAs [cta0, cta0+ncta) of the grid own one cluster; each round-robin step's
-// pairs are spread over all their warps, with a global-memory barrier between
-// steps.  Loads/stores bypass L1 (other SMs write the rows).
+// pairs are spread over all their warps (one pair per warp), with a group
+// barrier between steps.  A warp holds its pair's two rows in registers
+// (NPL doubles per lane, all loads issued at once), so a rotation costs one
+// L2 round trip; loads/stores bypass L1 (other SMs write the rows).  The
+// arithmetic (lane-strided partial sums, butterfly reduction) is the same as
+// the shared-memory kernel's.
 __device__ __forceinline__ void cta_group_barrier(uint32_t* bar, int nct) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -476,21 +320,107 @@ __device__ __forceinline__ void cta_group_barrier(uint32_t* bar, int nct) {
             __threadfence();
             atomicAdd(bar + 1, 1u);
         } else {
-            while (*gen == g) __nanosleep(64);
+            while (*gen == g) __nanosleep(20);
         }
         __threadfence();
     }
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(DT) jacobi_coop_kernel(const CoopSvdTask* __restrict__ tasks,
-                                                        const int* __restrict__ cta_task, double thresh) {
+constexpr int JT = 256;  // threads per CTA of the multi-CTA Jacobi
+
+__device__ __forceinline__ bool jac_pair_loop(double* __restrict__ rp, double* __restrict__ rq, int n, double tol) {
+    const int lane = threadIdx.x & 31;
+    double a = 0.0, b = 0.0, g = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        const double x = __ldcg(rp + i), y = __ldcg(rq + i);
+        a += x * x;
+        b += y * y;
+        g += x * y;
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    g = warp_sum(g);
+    if (!(g != 0.0 && a > 0.0 && b > 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b))) return false;
+    const double zeta = (b - a) / (2.0 * g);
+    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+    const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+    for (int i = lane; i < n; i += 32) {
+        const double x = __ldcg(rp + i), y = __ldcg(rq + i);
+        __stcg(rp + i, c * x - sn * y);
+        __stcg(rq + i, sn * x + c * y);
+    }
+    return true;
+}
+
+template <int NPL>
+__device__ __forceinline__ bool jac_pair_reg(double* __restrict__ rp, double* __restrict__ rq, int n, double tol) {
+    if constexpr (NPL == 0) return jac_pair_loop(rp, rq, n, tol);
+    const int lane = threadIdx.x & 31;
+    double x[NPL > 0 ? NPL : 1], y[NPL > 0 ? NPL : 1];
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+        const int i = lane + 32 * k;
+        x[k] = i < n ? __ldcg(rp + i) : 0.0;
+        y[k] = i < n ? __ldcg(rq + i) : 0.0;
+    }
+    double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+        a += x[k] * x[k];
+        b += y[k] * y[k];
+        g += x[k] * y[k];
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    g = warp_sum(g);
+    if (!(g != 0.0 && a > 0.0 && b > 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b))) return false;
+    const double zeta = (b - a) / (2.0 * g);
+    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+    const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+        const int i = lane + 32 * k;
+        if (i < n) {
+            __stcg(rp + i, c * x[k] - sn * y[k]);
+            __stcg(rq + i, sn * x[k] + c * y[k]);
+        }
+    }
+    return true;
+}
+
+template <int NPL>
+__device__ __forceinline__ double row_norm_reg(const double* __restrict__ r, int n) {
+    const int lane = threadIdx.x & 31;
+    if constexpr (NPL == 0) {
+        double a = 0.0;
+        for (int i = lane; i < n; i += 32) {
+            const double x = __ldcg(r + i);
+            a += x * x;
+        }
+        return sqrt(warp_sum(a));
+    }
+    double x[NPL > 0 ? NPL : 1];
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+        const int i = lane + 32 * k;
+        x[k] = i < n ? __ldcg(r + i) : 0.0;
+    }
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) a += x[k] * x[k];
+    return sqrt(warp_sum(a));
+}
+
+template <int NPL>
+__global__ void __launch_bounds__(JT, 1) jacobi_coop_kernel(const CoopSvdTask* __restrict__ tasks,
+                                                           const int* __restrict__ cta_task, double thresh) {
     const CoopSvdTask CT = tasks[cta_task[blockIdx.x]];
     const int rank = blockIdx.x - CT.cta0, nct = CT.ncta;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = DT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = JT / 32;
     const int m = CT.t.m, n = CT.t.n;
     double* A = CT.t.R;
-    extern __shared__ double dsh[];
+    extern __shared__ double dsh[];  // sig[m]
     __shared__ int kept_s;
     if (m == 0) {
         if (rank == 0 && threadIdx.x == 0) *CT.t.kept_out = 0;
@@ -500,71 +430,183 @@ __global__ void __launch_bounds__(DT) jacobi_coop_kernel(const CoopSvdTask* __re
     const int mm = m + (m & 1);
     const int gw = rank * nw + warp, gnw = nct * nw;
     for (int sweep = 0; sweep < 60; ++sweep) {
+        bool rotated = false;
         for (int st = 0; st < mm - 1; ++st) {
             for (int pi = gw; pi < mm / 2; pi += gnw) {
                 int p, q;
                 rr_pair(pi, st, mm, p, q);
                 if (p >= m || q >= m) continue;
-                double* rp = A + (int64_t)p * n;
-                double* rq = A + (int64_t)q * n;
-                double a = 0.0, b = 0.0, g = 0.0;
-                for (int i = lane; i < n; i += 32) {
-                    const double x = __ldcg(rp + i), y = __ldcg(rq + i);
-                    a += x * x;
-                    b += y * y;
-                    g += x * y;
-                }
-                a = warp_sum(a);
-                b = warp_sum(b);
-                g = warp_sum(g);
-                if (g != 0.0 && a > 0.0 && b > 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b)) {
-                    const double zeta = (b - a) / (2.0 * g);
-                    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
-                    for (int i = lane; i < n; i += 32) {
-                        const double x = __ldcg(rp + i), y = __ldcg(rq + i);
-                        __stcg(rp + i, c * x - sn * y);
-                        __stcg(rq + i, sn * x + c * y);
-                    }
-                    if (lane == 0) CT.flags[sweep] = 1;
-                }
+                rotated |= jac_pair_reg<NPL>(A + (int64_t)p * n, A + (int64_t)q * n, n, tol);
             }
             cta_group_barrier(CT.bar, nct);
         }
-        const int any = *(volatile int*)(CT.flags + sweep);
+        if (rotated && lane == 0) CT.flags[sweep] = 1;
+        cta_group_barrier(CT.bar, nct);
+        const int any = __ldcg(CT.flags + sweep);
+        if (rank == 0 && threadIdx.x == 0) CT.flags[63] = sweep + 1;
         if (!any) break;
     }
-    if (rank != 0) return;
-    double* sig = dsh;
-    int* rnk = reinterpret_cast<int*>(dsh + m);
-    for (int i = warp; i < m; i += nw) {
-        const double* ri = A + (int64_t)i * n;
-        double a = 0.0;
-        for (int c = lane; c < n; c += 32) {
-            const double x = __ldcg(ri + c);
-            a += x * x;
-        }
-        a = warp_sum(a);
-        if (lane == 0) sig[i] = sqrt(a);
+    // sigma (row norms) of this CTA's rows, shared through global memory
+    for (int i = gw; i < m; i += gnw) {
+        const double sg = row_norm_reg<NPL>(A + (int64_t)i * n, n);
+        if (lane == 0) CT.sig[i] = sg;
     }
+    cta_group_barrier(CT.bar, nct);
+    for (int i = threadIdx.x; i < m; i += JT) dsh[i] = __ldcg(CT.sig + i);
     if (threadIdx.x == 0) kept_s = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < m; i += DT) {
-        int r = 0;
-        const double si = sig[i];
-        for (int j = 0; j < m; ++j) r += (sig[j] > si) || (sig[j] == si && j < i);
-        rnk[i] = r;
-        if (si >= thresh) atomicAdd(&kept_s, 1);
-    }
+    int cnt = 0;
+    for (int i = threadIdx.x; i < m; i += JT) cnt += dsh[i] >= thresh;
+    atomicAdd(&kept_s, cnt);
     __syncthreads();
     const int kept = kept_s;
-    if (threadIdx.x == 0) *CT.t.kept_out = kept;
-    for (int i = warp; i < m; i += nw) {
-        const int j = rnk[i];
-        if (j >= kept) continue;
-        const double inv = 1.0 / sig[i];
+    if (rank == 0 && threadIdx.x == 0) *CT.t.kept_out = kept;
+    // kept rows, normalised, in descending sigma order (first index wins ties)
+    for (int i = gw; i < m; i += gnw) {
+        const double si = dsh[i];
+        int r = 0;
+        for (int j = lane; j < m; j += 32) r += (dsh[j] > si) || (dsh[j] == si && j < i);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+        if (r >= kept) continue;
+        const double inv = 1.0 / si;
         const double* ri = A + (int64_t)i * n;
-        for (int c = lane; c < n; c += 32) CT.t.U[(int64_t)j * n + c] = __ldcg(ri + c) * inv;
+        for (int c = lane; c < n; c += 32) CT.t.U[(int64_t)r * n + c] = __ldcg(ri + c) * inv;
+    }
+}
+
+// ---- block-cyclic multi-CTA Jacobi ----------------------------------------------
+// The m rows are cut into 2P blocks of JB rows; P co-resident CTAs play a
+// round-robin tournament over the blocks.  In one block step a CTA stages its
+// two blocks in shared memory and applies all JB x JB cross rotations (JB
+// inner steps of JB disjoint pairs, one warp per pair, __syncthreads between
+// inner steps), plus, at the first block step of a sweep, the rotations
+// inside each of its blocks; then the blocks go back to global memory and
+// the CTAs meet at one group barrier.  Every pair of rows is visited once
+// per sweep (a block-cyclic ordering), with one group barrier per JB^2
+// rotations instead of one per row pair.
+__device__ __forceinline__ bool jac_rotate_smem(double* __restrict__ x, double* __restrict__ y, int n, double tol) {
+    const int lane = threadIdx.x & 31;
+    double a = 0.0, b = 0.0, g = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        const double u = x[i], v = y[i];
+        a += u * u;
+        b += v * v;
+        g += u * v;
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    g = warp_sum(g);
+    if (!(g != 0.0 && a > 0.0 && b > 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b))) return false;
+    const double zeta = (b - a) / (2.0 * g);
+    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+    const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+    for (int i = lane; i < n; i += 32) {
+        const double u = x[i], v = y[i];
+        x[i] = c * u - sn * v;
+        y[i] = sn * u + c * v;
+    }
+    return true;
+}
+
+template <int JB>
+__global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* __restrict__ tasks,
+                                                            const int* __restrict__ cta_task, double thresh) {
+    const CoopSvdTask CT = tasks[cta_task[blockIdx.x]];
+    const int rank = blockIdx.x - CT.cta0, P = CT.ncta, NB2 = 2 * CT.ncta;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = JT / 32;
+    const int m = CT.t.m, n = CT.t.n;
+    double* A = CT.t.R;
+    extern __shared__ double bsm[];  // 2*JB rows of n; after the sweeps: sig[m]
+    __shared__ int kept_s;
+    __shared__ int rot_s;
+    if (m == 0) {
+        if (rank == 0 && threadIdx.x == 0) *CT.t.kept_out = 0;
+        return;
+    }
+    const double tol = 2.220446049250313e-16 * sqrt((double)n);
+    // rows of block j: [j*JB, min((j+1)*JB, m)); smem row r (0..2JB) <-> block (r < JB ? bp : bq)
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        if (threadIdx.x == 0) rot_s = 0;
+        bool rotated = false;
+        for (int st = 0; st < NB2 - 1; ++st) {
+            int bp, bq;
+            rr_pair(rank, st, NB2, bp, bq);
+            const int p0 = bp * JB, q0 = bq * JB;
+            const int np = max(0, min(JB, m - p0)), nq = max(0, min(JB, m - q0));
+            // stage (rows beyond m are zero and never rotate)
+            for (int e = threadIdx.x; e < 2 * JB * n; e += JT) {
+                const int r = e / n, i = e % n;
+                const int row = r < JB ? p0 + r : q0 + r - JB;
+                const bool v = r < JB ? r < np : r - JB < nq;
+                bsm[e] = v ? __ldcg(A + (int64_t)row * n + i) : 0.0;
+            }
+            __syncthreads();
+            if (st == 0) {
+                // rotations inside each block: round robin on JB rows, warps
+                // [0, nw/2) on block p, [nw/2, nw) on block q
+                const int half = nw / 2, blk = warp / half, wi = warp % half;
+                const int jbe = JB + (JB & 1);
+                for (int is = 0; is < jbe - 1; ++is) {
+                    for (int pi = wi; pi < jbe / 2; pi += half) {
+                        int a, b;
+                        rr_pair(pi, is, jbe, a, b);
+                        if (a >= JB || b >= JB) continue;
+                        rotated |= jac_rotate_smem(bsm + (int64_t)(blk * JB + a) * n, bsm + (int64_t)(blk * JB + b) * n,
+                                                   n, tol);
+                    }
+                    __syncthreads();
+                }
+            }
+            // cross rotations: inner step s pairs p-row i with q-row (i + s) % JB
+            for (int s = 0; s < JB; ++s) {
+                for (int i = warp; i < JB; i += nw)
+                    rotated |= jac_rotate_smem(bsm + (int64_t)i * n, bsm + (int64_t)(JB + (i + s) % JB) * n, n, tol);
+                __syncthreads();
+            }
+            for (int e = threadIdx.x; e < 2 * JB * n; e += JT) {
+                const int r = e / n, i = e % n;
+                const int row = r < JB ? p0 + r : q0 + r - JB;
+                const bool v = r < JB ? r < np : r - JB < nq;
+                if (v) __stcg(A + (int64_t)row * n + i, bsm[e]);
+            }
+            cta_group_barrier(CT.bar, P);
+        }
+        if (rotated && lane == 0) rot_s = 1;
+        __syncthreads();
+        if (rot_s && threadIdx.x == 0) CT.flags[sweep] = 1;
+        cta_group_barrier(CT.bar, P);
+        const int any = __ldcg(CT.flags + sweep);
+        if (rank == 0 && threadIdx.x == 0) CT.flags[63] = sweep + 1;
+        if (!any) break;
+    }
+    // sigma, kept count, sorted normalised rows (as jacobi_coop_kernel)
+    const int gw = rank * nw + warp, gnw = P * nw;
+    for (int i = gw; i < m; i += gnw) {
+        const double sg = row_norm_reg<0>(A + (int64_t)i * n, n);
+        if (lane == 0) CT.sig[i] = sg;
+    }
+    cta_group_barrier(CT.bar, P);
+    double* dsh = bsm;
+    for (int i = threadIdx.x; i < m; i += JT) dsh[i] = __ldcg(CT.sig + i);
+    if (threadIdx.x == 0) kept_s = 0;
+    __syncthreads();
+    int cnt = 0;
+    for (int i = threadIdx.x; i < m; i += JT) cnt += dsh[i] >= thresh;
+    atomicAdd(&kept_s, cnt);
+    __syncthreads();
+    const int kept = kept_s;
+    if (rank == 0 && threadIdx.x == 0) *CT.t.kept_out = kept;
+    for (int i = gw; i < m; i += gnw) {
+        const double si = dsh[i];
+        int r = 0;
+        for (int j = lane; j < m; j += 32) r += (dsh[j] > si) || (dsh[j] == si && j < i);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+        if (r >= kept) continue;
+        const double inv = 1.0 / si;
+        const double* ri = A + (int64_t)i * n;
+        for (int c = lane; c < n; c += 32) CT.t.U[(int64_t)r * n + c] = __ldcg(ri + c) * inv;
     }
 }
 
@@ -774,25 +816,11 @@ __global__ void diag_absmin_kernel(const double* A, int64_t lda, int n, double* 
 
 }  // namespace
 
-void launch_qr_r(const QrTask* d_tasks, int32_t ntasks, cudaStream_t st) {
-    if (ntasks <= 0) return;
-    qr_r_kernel<<<ntasks, DT, 0, st>>>(d_tasks);
-    count_launch();
-}
-
 void launch_qr_r_smem(const QrTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st) {
     if (ntasks <= 0) return;
     const size_t smem = sizeof(double) * (size_t(max_n) * max_n + size_t(max_n) * QB + 8);
     cudaFuncSetAttribute(qr_r_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     qr_r_smem_kernel<<<ntasks, DT, smem, st>>>(d_tasks);
-    count_launch();
-}
-
-void launch_jacobi(const SvdTask* d_tasks, int32_t ntasks, double thresh, cudaStream_t st) {
-    if (ntasks <= 0) return;
-    const size_t smem = 4096 * (sizeof(double) + sizeof(int));  // sig + rank, m <= 4096
-    cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    jacobi_kernel<<<ntasks, DT, smem, st>>>(d_tasks, thresh);
     count_launch();
 }
 
@@ -811,19 +839,6 @@ void launch_reorth(const ReorthTask* d_tasks, int32_t ntasks, cudaStream_t st) {
     count_launch();
 }
 
-void launch_bqr_panel(const BqrPanelTask* d_tasks, int32_t ntasks, cudaStream_t st) {
-    if (ntasks <= 0) return;
-    bqr_panel_kernel<<<ntasks, DT, 0, st>>>(d_tasks);
-    count_launch();
-}
-
-void launch_bqr_reduce(const BqrReduceTask* d_tasks, int32_t ntasks, int32_t max_ntrail, cudaStream_t st) {
-    if (ntasks <= 0 || max_ntrail <= 0) return;
-    dim3 grid((max_ntrail + 127) / 128, ntasks);
-    bqr_reduce_kernel<<<grid, 128, 0, st>>>(d_tasks);
-    count_launch();
-}
-
 void launch_r_extract(const RExtractTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st) {
     if (ntasks <= 0) return;
     dim3 grid((unsigned)(((int64_t)max_n * max_n + 255) / 256), ntasks);
@@ -831,16 +846,97 @@ void launch_r_extract(const RExtractTask* d_tasks, int32_t ntasks, int32_t max_n
     count_launch();
 }
 
-void launch_jacobi_coop(const CoopSvdTask* d_tasks, int32_t total_ctas, const int32_t* d_cta_task,
-                        double thresh, cudaStream_t st) {
-    if (total_ctas <= 0) return;
-    const size_t smem = 4096 * (sizeof(double) + sizeof(int));
-    cudaFuncSetAttribute(jacobi_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+int jacobi_coop_npl(int n) {
+    const int npl = (n + 31) / 32;
+    for (int c : {2, 4, 8, 12, 16, 20, 24, 32, 40, 48})
+        if (npl <= c) return c;
+    return 0;  // generic loop version
+}
+
+template <int NPL>
+static cudaError_t launch_jc(const CoopSvdTask* d_tasks, int32_t total_ctas, const int32_t* d_cta_task,
+                             double thresh, size_t smem, cudaStream_t st) {
+    cudaFuncSetAttribute(jacobi_coop_kernel<NPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {(void*)&d_tasks, (void*)&d_cta_task, (void*)&thresh};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)jacobi_coop_kernel, dim3(total_ctas), dim3(DT),
-                                                args, smem, st);
-    if (e != cudaSuccess) jacobi_coop_kernel<<<total_ctas, DT, smem, st>>>(d_tasks, d_cta_task, thresh);
+    return cudaLaunchCooperativeKernel((const void*)jacobi_coop_kernel<NPL>, dim3(total_ctas), dim3(JT), args,
+                                       smem, st);
+}
+
+cudaError_t launch_jacobi_coop(const CoopSvdTask* d_tasks, int32_t total_ctas, const int32_t* d_cta_task,
+                               int32_t max_n, int32_t max_m, double thresh, cudaStream_t st) {
+    if (total_ctas <= 0) return cudaSuccess;
+    const size_t smem = sizeof(double) * size_t(std::max(max_m, 1));
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (jacobi_coop_npl(max_n)) {
+    case 2: e = launch_jc<2>(d_tasks, total_ctas, d_cta_task, thresh, smem, st); break;
+    case 4: e = launch_jc<4>(d_tasks, total_ctas, d_cta_task, thresh, smem, st); break;
+    case 8: e = launch_jc<8>(d_tasks, total_ctas, d_cta_task, thresh, smem, st); break;
+    case 12: e = launch_jc<12>(d_tasks, total_ctas, d_cta_task, thresh, smem, st); break;
+    case 16: e = launch_jc<16>(d_tasks, total_ctas, d_cta_task, thresh, smem, st); break;
+    case 20: e = launch_jc<20>(d_tasks, total_ctas, d_cta_task, thresh, smem, st); break;
+    case 24: e = launch_jc<24>(d_tasks, total_ctas, d_cta_task, thresh, smem, st); break;
+    case 32: e = launch_jc<32>(d_tasks, total_ctas, d_cta_task, thresh, smem, st); break;
+    case 40: e = launch_jc<40>(d_tasks, total_ctas, d_cta_task, thresh, smem, st); break;
+    case 48: e = launch_jc<48>(d_tasks, total_ctas, d_cta_task, thresh, smem, st); break;
+    default: e = launch_jc<0>(d_tasks, total_ctas, d_cta_task, thresh, smem, st); break;
+    }
     count_launch();
+    return e;
+}
+
+int jacobi_coop_capacity(int max_n, int max_m) {
+    const size_t smem = sizeof(double) * size_t(std::max(max_m, 1));
+    int per_sm = 0, dev = 0, sms = 0;
+    const void* fn = nullptr;
+    switch (jacobi_coop_npl(max_n)) {
+    case 2: fn = (const void*)jacobi_coop_kernel<2>; break;
+    case 4: fn = (const void*)jacobi_coop_kernel<4>; break;
+    case 8: fn = (const void*)jacobi_coop_kernel<8>; break;
+    case 12: fn = (const void*)jacobi_coop_kernel<12>; break;
+    case 16: fn = (const void*)jacobi_coop_kernel<16>; break;
+    case 20: fn = (const void*)jacobi_coop_kernel<20>; break;
+    case 24: fn = (const void*)jacobi_coop_kernel<24>; break;
+    case 32: fn = (const void*)jacobi_coop_kernel<32>; break;
+    case 40: fn = (const void*)jacobi_coop_kernel<40>; break;
+    case 48: fn = (const void*)jacobi_coop_kernel<48>; break;
+    default: fn = (const void*)jacobi_coop_kernel<0>; break;
+    }
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, JT, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return per_sm * sms;
+}
+
+
+int jacobi_block_rows(int n) { return (size_t(16) * n * 8 <= size_t(200) * 1024) ? 8 : 4; }
+
+size_t jacobi_block_smem(int max_n, int max_m) {
+    const int jb = jacobi_block_rows(max_n);
+    return sizeof(double) * std::max<size_t>(size_t(2) * jb * max_n, size_t(max_m));
+}
+
+int jacobi_block_capacity(int max_n, int max_m) {
+    const size_t smem = jacobi_block_smem(max_n, max_m);
+    const void* fn = jacobi_block_rows(max_n) == 8 ? (const void*)jacobi_block_kernel<8> : (const void*)jacobi_block_kernel<4>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, JT, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return per_sm * sms;
+}
+
+cudaError_t launch_jacobi_block(const CoopSvdTask* d_tasks, int32_t total_ctas, const int32_t* d_cta_task,
+                                int32_t max_n, int32_t max_m, double thresh, cudaStream_t st) {
+    if (total_ctas <= 0) return cudaSuccess;
+    const size_t smem = jacobi_block_smem(max_n, max_m);
+    const void* fn = jacobi_block_rows(max_n) == 8 ? (const void*)jacobi_block_kernel<8> : (const void*)jacobi_block_kernel<4>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    void* args[] = {(void*)&d_tasks, (void*)&d_cta_task, (void*)&thresh};
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(total_ctas), dim3(JT), args, smem, st);
+    count_launch();
+    return e;
 }
 
 void launch_complement(const ComplementTask* d_tasks, int32_t ntasks, cudaStream_t st) {

@@ -1,0 +1,273 @@
+// Blocked Householder QR with a cooperative multi-CTA panel (LAPACK geqrf
+// conventions: dlarfg reflectors, dlarft forward/columnwise T).
+//
+// Used for the two tall QRs of the augmentation (factorization.py:78 and the
+// complete QR of b_aug, :98) once the clusters outgrow one CTA.  One panel of
+// HH_NB columns is spread over `ncta` co-resident CTAs, each holding a
+// contiguous slice of the panel's rows in shared memory; every column costs
+// two group barriers (norm, then the dots with the rest of the panel) and the
+// partial sums are reduced in a fixed order, so the factor is bitwise
+// reproducible.  The trailing update A -= V T^T (V^T A) runs on the DMMA tile
+// GEMM (k_gemm.cu) between panels.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace h2f {
+
+namespace {
+
+constexpr int HT = 256;
+constexpr int HW = HT / 32;
+
+// LAPACK dlarfg-style reflector for x = [alpha, rest]; ss = ||rest||^2.
+__device__ __forceinline__ void hh_reflector(double alpha, double ss, double& beta, double& tau, double& scal) {
+    if (ss == 0.0) {
+        beta = alpha;
+        tau = 0.0;
+        scal = 0.0;
+    } else {
+        beta = -copysign(hypot(alpha, sqrt(ss)), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+    }
+}
+
+// barrier over the `n` CTAs of one task (generation counter in bar[1])
+__device__ __forceinline__ void group_barrier(uint32_t* bar, int n) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile uint32_t* gen = bar + 1;
+        const uint32_t g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == uint32_t(n - 1)) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(HT, 1)
+hh_panel_kernel(const HhPanelTask* __restrict__ tasks, const int32_t* __restrict__ cta_task) {
+    const HhPanelTask T = tasks[cta_task[blockIdx.x]];
+    const int g = blockIdx.x - T.cta0, G = T.ncta;
+    const int nbp = T.nbp, lds = T.chunk + 4;
+    const int64_t Lp = (int64_t)T.L - T.j0;
+    const int64_t r0 = (int64_t)g * T.chunk;
+    const int rows = (int)min((int64_t)T.chunk, Lp - r0);
+    const int rows4 = (rows + 3) & ~3;
+    extern __shared__ double S[];  // column jj of the slice at S[jj * lds]
+    __shared__ double taus[HH_NB];
+    __shared__ double red[HW];
+    __shared__ double dsh[HH_NB + 2];
+    __shared__ double Tm[HH_NB][HH_NB + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* M0 = T.M + (int64_t)T.j0 * T.ldm + T.j0 + r0;
+
+    for (int jj = 0; jj < HH_NB; ++jj)
+        for (int i = threadIdx.x; i < lds; i += HT)
+            S[jj * lds + i] = (jj < nbp && i < rows) ? M0[(int64_t)jj * T.ldm + i] : 0.0;
+    __syncthreads();
+
+    // pa: [G + 1] partial norms + alpha, double-buffered by column parity (a
+    // column with tau == 0 skips the second barrier); pb: [(G + 1) * HH_NB]
+    // partial dots + heads
+    double* pb = T.part + 2 * (G + 1);
+    for (int jj = 0; jj < nbp; ++jj) {
+        double* pa = T.part + (jj & 1) * (G + 1);
+        const int lo = (int)max((int64_t)0, (int64_t)(jj + 1) - r0);  // local rows strictly below the diagonal
+        double ss = 0.0;
+        for (int i = lo + threadIdx.x; i < rows; i += HT) {
+            const double x = S[jj * lds + i];
+            ss += x * x;
+        }
+        ss = block_sum(ss, red);
+        if (threadIdx.x == 0) {
+            pa[g] = ss;
+            if (g == 0) pa[G] = S[jj * lds + jj];
+        }
+        group_barrier(T.bar, G);
+        if (warp == 0) {
+            double v = 0.0;
+            for (int q = lane; q < G; q += 32) v += __ldcg(pa + q);
+            v = warp_sum(v);
+            if (lane == 0) {
+                dsh[HH_NB] = v;
+                dsh[HH_NB + 1] = __ldcg(pa + G);
+            }
+        }
+        __syncthreads();
+        double beta, tau, scal;
+        hh_reflector(dsh[HH_NB + 1], dsh[HH_NB], beta, tau, scal);
+        if (tau != 0.0)
+            for (int i = lo + threadIdx.x; i < rows; i += HT) S[jj * lds + i] *= scal;
+        if (threadIdx.x == 0) {
+            taus[jj] = tau;
+            if (g == 0) S[jj * lds + jj] = beta;
+        }
+        __syncthreads();
+        if (tau == 0.0 || jj + 1 >= nbp) continue;  // tau is identical in every CTA
+        for (int c = jj + 1 + warp; c < nbp; c += HW) {
+            double d = 0.0;
+            for (int i = lo + lane; i < rows; i += 32) d += S[jj * lds + i] * S[c * lds + i];
+            d = warp_sum(d);
+            if (lane == 0) {
+                pb[(int64_t)g * HH_NB + c] = d;
+                if (g == 0) pb[(int64_t)G * HH_NB + c] = S[c * lds + jj];
+            }
+        }
+        group_barrier(T.bar, G);
+        for (int c = jj + 1 + warp; c < nbp; c += HW) {
+            double v = 0.0;
+            for (int q = lane; q < G; q += 32) v += __ldcg(pb + (int64_t)q * HH_NB + c);
+            v = warp_sum(v);
+            if (lane == 0) dsh[c] = (v + __ldcg(pb + (int64_t)G * HH_NB + c)) * tau;
+        }
+        __syncthreads();
+        const int w = nbp - jj - 1;
+        for (int e = threadIdx.x; e < w * rows; e += HT) {
+            const int c = jj + 1 + e / rows, i = e % rows;
+            if (i >= lo) S[c * lds + i] -= dsh[c] * S[jj * lds + i];
+        }
+        if (g == 0)
+            for (int c = jj + 1 + threadIdx.x; c < nbp; c += HT) S[c * lds + jj] -= dsh[c];
+        __syncthreads();
+    }
+
+    // write back (R on/above the diagonal, reflectors below) and the explicit
+    // unit-lower V^T (HH_NB x Lp); S becomes the explicit V for the Gram
+    for (int jj = 0; jj < nbp; ++jj)
+        for (int i = threadIdx.x; i < rows; i += HT) {
+            const double x = S[jj * lds + i];
+            M0[(int64_t)jj * T.ldm + i] = x;
+            const int64_t gi = r0 + i;
+            const double v = gi < jj ? 0.0 : (gi == jj ? 1.0 : x);
+            T.Vt[(int64_t)jj * Lp + gi] = v;
+            S[jj * lds + i] = v;
+        }
+    __syncthreads();
+    // partial Gram V^T V over the slice: 16 8x8 DMMA tiles, 2 per warp
+    {
+        const int gq = lane >> 2, t = lane & 3;
+        double* gp = T.gram + (int64_t)g * HH_NB * HH_NB;
+        for (int tile = warp; tile < 16; tile += HW) {
+            const int ti = tile >> 2, tj = tile & 3;
+            double c0 = 0.0, c1 = 0.0;
+            const double* A = S + (ti * 8 + gq) * lds;
+            const double* B = S + (tj * 8 + gq) * lds;
+            for (int k0 = 0; k0 < rows4; k0 += 4) dmma_8x8x4(c0, c1, A[k0 + t], B[k0 + t]);
+            gp[(ti * 8 + gq) * HH_NB + tj * 8 + 2 * t] = c0;
+            gp[(ti * 8 + gq) * HH_NB + tj * 8 + 2 * t + 1] = c1;
+        }
+    }
+    group_barrier(T.bar, G);
+    if (g != 0) return;
+    // CTA 0: Gram (fixed-order sum over the slices), then dlarft
+    double* Gm = S;  // HH_NB x HH_NB, reuses the slice buffer
+    for (int e = threadIdx.x; e < HH_NB * HH_NB; e += HT) {
+        const int a = e / HH_NB, b = e % HH_NB;
+        double v = 0.0;
+        if (a < b && b < nbp)
+            for (int q = 0; q < G; ++q) v += __ldcg(T.gram + (int64_t)q * HH_NB * HH_NB + e);
+        Gm[e] = v;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        for (int j = 0; j < HH_NB; ++j) {
+            const double tj = j < nbp ? taus[j] : 0.0;
+            double acc = 0.0;
+            if (lane < j)
+                for (int k = lane; k < j; ++k) acc += Tm[lane][k] * (-tj * Gm[k * HH_NB + j]);
+            __syncwarp();
+            Tm[lane][j] = lane < j ? acc : (lane == j ? tj : 0.0);
+            __syncwarp();
+        }
+        for (int j = 0; j < HH_NB; ++j) T.T[lane * HH_NB + j] = Tm[lane][j];
+    }
+}
+
+// out[a][c] = sum_b op(T)[a][b] * (sum_ch P[ch][b][c]),  op(T) = T^T (trans) or T
+__global__ void hh_tmul_kernel(const HhTmulTask* __restrict__ tasks) {
+    const HhTmulTask R = tasks[blockIdx.y];
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= R.ncols) return;
+    double S[HH_NB];
+#pragma unroll
+    for (int b = 0; b < HH_NB; ++b) S[b] = 0.0;
+    for (int ch = 0; ch < R.nchunks; ++ch) {
+        const double* P = R.P + (int64_t)ch * R.nrows * R.ncols;
+#pragma unroll
+        for (int b = 0; b < HH_NB; ++b)
+            if (b < R.nrows) S[b] += P[(int64_t)b * R.ncols + c];
+    }
+#pragma unroll
+    for (int a = 0; a < HH_NB; ++a) {
+        if (a >= R.nrows) break;
+        double acc = 0.0;
+        if (R.trans) {
+#pragma unroll
+            for (int b = 0; b <= a; ++b) acc += R.T[b * HH_NB + a] * S[b];
+        } else {
+#pragma unroll
+            for (int b = a; b < HH_NB; ++b) acc += R.T[a * HH_NB + b] * S[b];
+        }
+        R.out[(int64_t)a * R.ncols + c] = acc;
+    }
+}
+
+// X[kt + i][i] = 1 (the [0; I] seed of the complement columns); X pre-zeroed
+__global__ void set_eye_kernel(const EyeTask* __restrict__ tasks) {
+    const EyeTask E = tasks[blockIdx.y];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < E.n) E.X[(int64_t)(E.row0 + i) * E.ldx + i] = 1.0;
+}
+
+}  // namespace
+
+size_t hh_panel_smem(int chunk) { return sizeof(double) * size_t(HH_NB) * (chunk + 4); }
+
+int hh_panel_capacity(int chunk) {
+    static int cached_chunk = -1, cached = 0;
+    if (chunk == cached_chunk) return cached;
+    const size_t smem = hh_panel_smem(chunk);
+    cudaFuncSetAttribute(hh_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hh_panel_kernel, HT, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cached_chunk = chunk;
+    cached = per_sm * sms;
+    return cached;
+}
+
+cudaError_t launch_hh_panel(const HhPanelTask* d_tasks, const int32_t* d_cta_task, int32_t total_ctas,
+                            int32_t max_chunk, cudaStream_t st) {
+    if (total_ctas <= 0) return cudaSuccess;
+    const size_t smem = hh_panel_smem(max_chunk);
+    cudaFuncSetAttribute(hh_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    void* args[] = {(void*)&d_tasks, (void*)&d_cta_task};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)hh_panel_kernel, dim3(total_ctas), dim3(HT), args,
+                                                smem, st);
+    count_launch();
+    return e;  // never falls back to a plain launch: the group barriers need co-residency
+}
+
+void launch_hh_tmul(const HhTmulTask* d_tasks, int32_t ntasks, int32_t max_cols, cudaStream_t st) {
+    if (ntasks <= 0 || max_cols <= 0) return;
+    dim3 grid((max_cols + 127) / 128, ntasks);
+    hh_tmul_kernel<<<grid, 128, 0, st>>>(d_tasks);
+    count_launch();
+}
+
+void launch_set_eye(const EyeTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st) {
+    if (ntasks <= 0 || max_n <= 0) return;
+    dim3 grid((max_n + 127) / 128, ntasks);
+    set_eye_kernel<<<grid, 128, 0, st>>>(d_tasks);
+    count_launch();
+}
+
+}  // namespace h2f

@@ -79,8 +79,8 @@ solve_tasks_kernel(const SolveTask* __restrict__ tasks, const SolveCluster* __re
     const int s = C.s, r = C.r;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* yc = y + C.off * nrhs;
-    double* wk = work + C.woff;             // s x nrhs
-    double* tb = work + C.woff + (int64_t)s * nrhs;  // r x nrhs
+    double* wk = work + C.woff;                      // s x nrhs
+    double* tb = work + C.woff + (int64_t)s * nrhs;  // nch x r x nrhs gather partials
     switch (T.kind) {
     case ST_ROT_T: {
         // 64 columns x 4 row groups, partial sums reduced through shared memory
@@ -144,24 +144,36 @@ solve_tasks_kernel(const SolveTask* __restrict__ tasks, const SolveCluster* __re
         break;
     }
     case ST_GATHER: {
+        // columns [c0, c1) of the eliminators: the edges are consecutive
+        // column slices of mw (edge e starts at column soff_e - C.soff)
+        const int ch = T.c0 / SOLVE_GATHER_COLS;
+        double* part = tb + (int64_t)ch * r * nrhs;
         for (int k = T.begin + warp; k < T.end; k += STW)
             for (int rh = 0; rh < nrhs; ++rh) {
                 double acc = 0.0;
                 for (int64_t ei = C.edge_begin; ei < C.edge_end; ++ei) {
                     const SolveEdge E = edges[ei];
-                    const double* mk = E.mat + (int64_t)k * E.ld;
-                    const double* ys = y + E.lo * nrhs + rh;
-                    for (int j = lane; j < E.w; j += 32) acc += mk[j] * ys[(int64_t)j * nrhs];
+                    const int e0 = (int)(E.soff - C.soff);
+                    const int lo = max(e0, T.c0), hi = min(e0 + E.w, T.c1);
+                    if (lo >= hi) continue;
+                    const double* mk = E.mat + (int64_t)k * E.ld - e0;
+                    const double* ys = y + (E.lo - e0) * nrhs + rh;
+#pragma unroll 8
+                    for (int j = lo + lane; j < hi; j += 32) acc += mk[j] * ys[(int64_t)j * nrhs];
                 }
                 acc = warp_sum(acc);
-                if (lane == 0) tb[(int64_t)k * nrhs + rh] = acc;
+                if (lane == 0) part[(int64_t)k * nrhs + rh] = acc;
             }
         break;
     }
     case ST_ROT: {
         for (int rh = 0; rh < nrhs; ++rh) {
-            for (int j = threadIdx.x; j < s; j += ST)
-                sv[j] = wk[(int64_t)j * nrhs + rh] + (j < r ? tb[(int64_t)j * nrhs + rh] : 0.0);
+            for (int j = threadIdx.x; j < s; j += ST) {
+                double t = 0.0;
+                if (j < r)
+                    for (int ch = 0; ch < C.nch; ++ch) t += tb[((int64_t)ch * r + j) * nrhs + rh];
+                sv[j] = wk[(int64_t)j * nrhs + rh] + t;
+            }
             __syncthreads();
             for (int i = T.begin + warp; i < T.end; i += STW) {
                 const double* qi = C.q + (int64_t)i * s;

@@ -92,25 +92,6 @@ struct ComplementTask {  // Q~ = [complement | b_aug] from BT (kt x s rows = col
     int32_t s, kt;
 };
 
-// blocked Householder QR of M = Z^T (Z is n x wf row-major), panel of BQR_NB
-// columns = BQR_NB rows of Z.  The panel kernel factors the panel in place and
-// writes V (explicit unit-lower, nbp x L, L = wf - j0) and T (BQR_NB^2, upper).
-constexpr int BQR_NB = 16;
-struct BqrPanelTask {
-    double* Z;           // n x wf, ld = ldz
-    double* V;           // BQR_NB x L (ld L)
-    double* T;           // BQR_NB x BQR_NB
-    int64_t ldz;
-    int32_t wf, j0, nbp, pad_;
-};
-
-struct BqrReduceTask {   // W2 = T^T * sum_c P_c  (BQR_NB x ntrail)
-    const double* P;     // nchunks x (BQR_NB x ntrail)
-    const double* T;
-    double* W2;
-    int32_t nchunks, ntrail;
-};
-
 struct RExtractTask {    // R[j][c] = c >= j ? Z[c][j] : 0  (j < m, c < n)
     const double* Z;
     double* R;           // n x n
@@ -123,6 +104,7 @@ struct CoopSvdTask {     // multi-CTA Jacobi: CTAs [cta0, cta0+ncta) own one clu
     int32_t cta0, ncta;
     uint32_t* bar;       // [2] barrier counter + generation
     int32_t* flags;      // [64] per-sweep rotation flags (zeroed)
+    double* sig;         // [m] singular values (scratch)
 };
 
 struct LuTask {          // partial-pivot LU of the r x r view of D_cc
@@ -146,6 +128,37 @@ struct TrsmTask {        // MW = -(U^-1 L^-1 P G) column block
     int32_t pad_;
 };
 
+// ---- blocked Householder QR with a cooperative panel (k_hh.cu) ---------------------
+// Matrix column j at M + j*ldm (rows contiguous).  One task = one panel of
+// nbp <= HH_NB columns starting at column/row j0, spread over CTAs
+// [cta0, cta0+ncta) of the grid, `chunk` rows of [j0, L) each (chunk >= HH_NB,
+// multiple of 4).  Outputs: R/reflectors in place, the explicit unit-lower
+// reflectors Vt (HH_NB x (L-j0), row-major) and T (HH_NB x HH_NB, dlarft).
+constexpr int HH_NB = 32;
+constexpr int HH_CHUNK_MAX = 512;
+struct HhPanelTask {
+    double* M;
+    int64_t ldm;
+    double* Vt;
+    double* T;
+    double* part;        // (ncta + 1) * (HH_NB + 2) doubles
+    double* gram;        // ncta * HH_NB * HH_NB doubles
+    uint32_t* bar;       // 2 words, zeroed
+    int32_t L, j0, nbp, chunk;
+    int32_t cta0, ncta;
+};
+struct HhTmulTask {      // out = op(T) * sum_ch P[ch]   (nrows x ncols each)
+    const double* P;
+    const double* T;
+    double* out;
+    int32_t nchunks, nrows, ncols, trans;
+};
+struct EyeTask {         // X[row0 + i][i] = 1, i < n
+    double* X;
+    int64_t ldx;
+    int32_t row0, n;
+};
+
 // ---- solve -----------------------------------------------------------------------
 struct SolveCluster {
     const double* q;     // s x s
@@ -156,7 +169,9 @@ struct SolveCluster {
     int32_t s, r;
     int64_t W;
     int64_t edge_begin, edge_end;
-    int64_t woff;        // work slot: 2 * s * nrhs doubles (rotated vector, gathered products)
+    int64_t woff;        // work slot: (s + nch * r) * nrhs doubles (rotated vector, gather partials)
+    int32_t nch;         // column chunks of the backward gather
+    int32_t pad2_;
     int64_t soff;        // forward products of column j of mw go to scratch row soff + j
 };
 
@@ -175,12 +190,15 @@ enum SolveTaskKind : int32_t {
     ST_PROD,       // scratch[soff + j] = (mw^T work_R)[j], j in [begin,end)  forward
     ST_LSOLVE,     // y_c = [L^-1 P work_R ; work_S]                          forward
     ST_USOLVE,     // work = [U^-1 y_R ; y_S]                                 backward
-    ST_GATHER,     // tbuf[k] = sum_e (mat_e y[span_e])[k], k in [begin,end)  backward
-    ST_ROT,        // y_c[i] = (Q (work + [tbuf; 0]))[i], i in [begin, end)   backward
+    ST_GATHER,     // part[ch][k] = sum_e (mat_e y[span_e])[k] over columns [c0,c1) = chunk ch,
+                   // k in [begin,end)                                         backward
+    ST_ROT,        // y_c[i] = (Q (work + [sum_ch part[ch]; 0]))[i], i in [begin, end)  backward
 };
 struct SolveTask {
     int32_t cl, kind, begin, end;
+    int32_t c0, c1;      // ST_GATHER: eliminator column range [c0, c1)
 };
+constexpr int SOLVE_GATHER_COLS = 2048;  // column chunk of one ST_GATHER task
 constexpr int SOLVE_ROT_T_COLS = 64;
 constexpr int SOLVE_PROD_COLS = 256;
 constexpr int SOLVE_ROW_SLICE = 16;
@@ -216,22 +234,33 @@ void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
                        double* d_norms, cudaStream_t st);
 void launch_copy_tasks(const CopyTask* d_tasks, const int64_t* d_tile_start, int32_t ntasks,
                        int64_t ntiles, cudaStream_t st);
-void launch_qr_r(const QrTask* d_tasks, int32_t ntasks, cudaStream_t st);
 void launch_qr_r_smem(const QrTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st);
-void launch_jacobi(const SvdTask* d_tasks, int32_t ntasks, double thresh, cudaStream_t st);
 void launch_jacobi_smem(const SvdTask* d_tasks, int32_t ntasks, int32_t max_n, double thresh, cudaStream_t st);
 void launch_reorth(const ReorthTask* d_tasks, int32_t ntasks, cudaStream_t st);
-void launch_bqr_panel(const BqrPanelTask* d_tasks, int32_t ntasks, cudaStream_t st);
-void launch_bqr_reduce(const BqrReduceTask* d_tasks, int32_t ntasks, int32_t max_ntrail, cudaStream_t st);
 void launch_r_extract(const RExtractTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st);
-void launch_jacobi_coop(const CoopSvdTask* d_tasks, int32_t total_ctas, const int32_t* d_cta_task,
-                        double thresh, cudaStream_t st);
+// block-cyclic multi-CTA Jacobi: JB-row blocks (jacobi_block_rows), 2 blocks per CTA
+int jacobi_block_rows(int n);
+int jacobi_block_capacity(int max_n, int max_m);
+cudaError_t launch_jacobi_block(const CoopSvdTask* d_tasks, int32_t total_ctas, const int32_t* d_cta_task,
+                                int32_t max_n, int32_t max_m, double thresh, cudaStream_t st);
+// multi-CTA Jacobi for n <= 32 * 48 (jacobi_coop_npl(n) > 0); cooperative launch
+int jacobi_coop_npl(int n);
+int jacobi_coop_capacity(int max_n, int max_m);  // co-resident CTAs
+cudaError_t launch_jacobi_coop(const CoopSvdTask* d_tasks, int32_t total_ctas, const int32_t* d_cta_task,
+                               int32_t max_n, int32_t max_m, double thresh, cudaStream_t st);
 constexpr int SMEM_DENSE_MAX_N = 144;  // n x n doubles resident in shared memory
 void launch_complement(const ComplementTask* d_tasks, int32_t ntasks, cudaStream_t st);
 void launch_lu(const LuTask* d_tasks, int32_t ntasks, cudaStream_t st);
 void launch_trsm(const TrsmTask* d_tasks, int32_t ntasks, cudaStream_t st);
 void launch_sumsq_reduce(const double* d_parts, const int64_t* d_seg, int32_t nseg,
                          double* d_out, cudaStream_t st);
+
+size_t hh_panel_smem(int chunk);
+int hh_panel_capacity(int chunk);  // co-resident CTAs of the panel kernel at this chunk
+cudaError_t launch_hh_panel(const HhPanelTask* d_tasks, const int32_t* d_cta_task, int32_t total_ctas,
+                            int32_t max_chunk, cudaStream_t st);
+void launch_hh_tmul(const HhTmulTask* d_tasks, int32_t ntasks, int32_t max_cols, cudaStream_t st);
+void launch_set_eye(const EyeTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st);
 
 // top (dense) LU pieces
 void launch_panel_lu(double* A, int64_t lda, int32_t n, int32_t k0, int32_t nb, int32_t* piv,

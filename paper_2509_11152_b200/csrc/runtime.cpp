@@ -172,7 +172,7 @@ const char* kernel_name(int kid) {
         "gemm_augment", "gemm_project", "gemm_schur", "gemm_fill_create", "gemm_top_update", "copy_tasks",
         "qr_r", "jacobi_svd", "complement", "lu_redundant", "trsm_eliminator", "norm_reduce", "top_panel_lu",
         "top_misc", "solve_fwd_clusters", "solve_fwd_scatter", "solve_bwd_clusters", "solve_top",
-        "solve_misc", "matvec_gemv", "vector_ops"};
+        "solve_misc", "matvec_gemv", "vector_ops", "qr_r_blocked", "jacobi_svd_coop", "complement_v"};
     return (kid >= 0 && kid < K_COUNT) ? names[kid] : "?";
 }
 

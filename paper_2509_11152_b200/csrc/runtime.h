@@ -100,7 +100,8 @@ class Uploader {
 enum KernelId : int {
     K_GEMM_AUG = 0, K_GEMM_PROJECT, K_GEMM_SCHUR, K_GEMM_CREATE, K_GEMM_TOP, K_COPY, K_QR, K_JACOBI,
     K_COMPLEMENT, K_LU, K_TRSM, K_REDUCE, K_TOP_PANEL, K_TOP_MISC, K_SOLVE_FWD, K_SOLVE_SCATTER,
-    K_SOLVE_BWD, K_SOLVE_TOP, K_SOLVE_MISC, K_MATVEC, K_VECTOR, K_COUNT
+    K_SOLVE_BWD, K_SOLVE_TOP, K_SOLVE_MISC, K_MATVEC, K_VECTOR, K_QR_BIG, K_JACOBI_BIG, K_COMPLEMENT_V,
+    K_COUNT
 };
 const char* kernel_name(int kid);
 

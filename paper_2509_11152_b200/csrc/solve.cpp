@@ -92,7 +92,6 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
                 sc.soff = soff;
                 sc.edge_begin = int64_t(edges.size());
                 sc.woff = woff;
-                woff += 2 * int64_t(cf.s) * nrhs;
                 if (cf.s + 256 > SOLVE_SMEM_VEC)
                     throw Error(H2F_E_INTERNAL, "assertion: cluster too large for the solve kernels");
                 int64_t col = 0;
@@ -124,23 +123,28 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
                     edges.push_back(se);
                 }
                 sc.edge_end = int64_t(edges.size());
+                sc.nch = cf.r > 0 ? int32_t(cdiv(std::max<int64_t>(sc.W, 1), SOLVE_GATHER_COLS)) : 0;
+                woff += (int64_t(cf.s) + int64_t(sc.nch) * cf.r) * nrhs;
                 const int ci = int(cls.size());
                 cls.push_back(sc);
                 for (int j = 0; j < cf.s; j += SOLVE_ROT_T_COLS)
-                    tk[0].push_back({ci, ST_ROT_T, j, std::min(cf.s, j + SOLVE_ROT_T_COLS)});
+                    tk[0].push_back({ci, ST_ROT_T, j, std::min(cf.s, j + SOLVE_ROT_T_COLS), 0, 0});
                 for (int i = 0; i < cf.s; i += SOLVE_ROW_SLICE)
-                    tk[3].push_back({ci, ST_ROT, i, std::min(cf.s, i + SOLVE_ROW_SLICE)});
+                    tk[3].push_back({ci, ST_ROT, i, std::min(cf.s, i + SOLVE_ROW_SLICE), 0, 0});
                 if (cf.r > 0) {
-                    tk[1].push_back({ci, ST_LSOLVE, 0, cf.r});
+                    tk[1].push_back({ci, ST_LSOLVE, 0, cf.r, 0, 0});
                     for (int64_t j = 0; j < sc.W; j += SOLVE_PROD_COLS)
-                        tk[1].push_back({ci, ST_PROD, int32_t(j), int32_t(std::min<int64_t>(sc.W, j + SOLVE_PROD_COLS))});
-                    tk[2].push_back({ci, ST_USOLVE, 0, cf.r});
-                    for (int i = 0; i < cf.r; i += SOLVE_ROW_SLICE)
-                        tk[2].push_back({ci, ST_GATHER, i, std::min(cf.r, i + SOLVE_ROW_SLICE)});
+                        tk[1].push_back({ci, ST_PROD, int32_t(j), int32_t(std::min<int64_t>(sc.W, j + SOLVE_PROD_COLS)),
+                                         0, 0});
+                    tk[2].push_back({ci, ST_USOLVE, 0, cf.r, 0, 0});
+                    for (int64_t c0 = 0; c0 < std::max<int64_t>(sc.W, 1); c0 += SOLVE_GATHER_COLS)
+                        for (int i = 0; i < cf.r; i += SOLVE_ROW_SLICE)
+                            tk[2].push_back({ci, ST_GATHER, i, std::min(cf.r, i + SOLVE_ROW_SLICE), int32_t(c0),
+                                             int32_t(std::min<int64_t>(sc.W, c0 + SOLVE_GATHER_COLS))});
                 } else {
                     // nothing eliminated: the rotated vector passes through
-                    tk[1].push_back({ci, ST_LSOLVE, 0, 0});
-                    tk[2].push_back({ci, ST_USOLVE, 0, 0});
+                    tk[1].push_back({ci, ST_LSOLVE, 0, 0, 0, 0});
+                    tk[2].push_back({ci, ST_USOLVE, 0, 0, 0, 0});
                 }
                 double ew = double(sc.W);
                 flops_b += (2.0 * cf.s * cf.s + 2.0 * cf.r * ew + double(cf.r) * cf.r) * nrhs;

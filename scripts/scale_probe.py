@@ -34,8 +34,10 @@ for item in cases:
     ts2 = time.perf_counter() - t0
     sprof = _lib.profile_get(); _lib.profile_enable(False)
     eb = np.linalg.norm(H.matvec(h2, x) - b) / np.linalg.norm(b)
+    x0 = H.solve(fac2, b)
+    eb0 = np.linalg.norm(H.matvec(h2, x0) - b) / np.linalg.norm(b)
     print(json.dumps({"case": f"{name}_{n}", "over": over, "build_s": round(tb, 2), "fact_s_first": round(tf, 4),
-        "fact_s": round(tf2, 4), "solve_s_first": round(ts, 4), "solve_s": round(ts2, 4), "e_b": eb,
+        "fact_s": round(tf2, 4), "solve_s_first": round(ts, 4), "solve_s": round(ts2, 4), "e_b": eb, "e_b_raw": eb0,
         "top": fac2.top_size, "nbytes_MB": fac2.nbytes() / 1e6,
         "batches": sum(r.nbatches for r in fac2.records),
         "phases": {k: round(v, 4) for k, v in fac2.phase_seconds.items()},
