@@ -56,7 +56,7 @@ struct GemmBuild {
         auto* dc = X.up.put(contribs);
         auto* ds = X.up.put(tile_start);
         X.up.flush(X.stream);
-        ProfScope ps(kid, flops, bytes_override >= 0 ? bytes_override : bytes);
+        ProfScope ps(kid, flops, bytes_override >= 0 ? bytes_override : bytes, double(tile_start.back()));
         launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), tile_start.back(), norms, X.stream);
     }
 };

@@ -32,7 +32,9 @@ struct PanelPlan {
 };
 
 // CTA allocation of one wave: at least ceil(Lp / HH_CHUNK_MAX) CTAs per
-// job, spare CTAs to the jobs with the most rows per CTA
+// job, spare CTAs to the jobs with the most rows per CTA while a CTA keeps
+// >= 128 rows (measured: the per-column work of wide slices outweighs the
+// cost of a larger barrier group)
 void size_wave(std::vector<PanelPlan>& w, int cap) {
     int total = 0;
     for (auto& p : w) {
@@ -44,7 +46,7 @@ void size_wave(std::vector<PanelPlan>& w, int cap) {
         double most = 0;
         for (auto& p : w) {
             const double per = double(p.Lp) / p.ncta;
-            if (per >= 2.0 * 64 && per > most) {  // keep >= 64 rows per CTA
+            if (per >= 2.0 * 128 && per > most) {
                 most = per;
                 best = &p;
             }
@@ -230,6 +232,40 @@ void complement_blocked(const std::vector<ComplementTask>& tasks, Region& scr) {
     launch_set_eye(upload(eye), int32_t(eye.size()), maxr, st);
     hh_factor(jobs, scr, true);
     hh_apply_q(jobs, xs, scr);
+}
+
+void blocked_lu(double* A, int64_t n, int32_t* piv, Region& scr, double* red, int kid_panel, int kid_misc,
+                int kid_gemm) {
+    cudaStream_t st = ctx().stream;
+    if (n == 0) return;
+    launch_absmax(A, n, int(n), int(n), red, st);
+    const int nb = TOP_PANEL_NB;
+    const int g = top_panel_grid(int(n));
+    TopPanelScratch ps;
+    ps.val = scr.alloc_n<double>(2 * g);
+    ps.idx = scr.alloc_n<int>(2 * g);
+    ps.rows = scr.alloc_n<double>(int64_t(2) * g * TOP_PANEL_NB);
+    ps.rowk = scr.alloc_n<double>(2 * TOP_PANEL_NB);
+    ps.bar = scr.alloc_n<unsigned>(2);
+    for (int64_t k0 = 0; k0 < n; k0 += nb) {
+        const int w = int(std::min<int64_t>(nb, n - k0));
+        {
+            ProfScope p(kid_panel, double(n - k0) * w * w, 16.0 * double(n - k0) * w);
+            if (!launch_coop_panel_lu(A, n, int(n), int(k0), w, piv, ps, st))
+                launch_panel_lu(A, n, int(n), int(k0), w, piv, st);
+        }
+        const int64_t rest = n - k0 - w;
+        ProfScope p(kid_misc, double(rest) * w * w, 16.0 * double(n) * w + 16.0 * double(rest) * w);
+        launch_row_swaps(A, n, int(n), int(k0), w, piv, int(k0), int(k0 + w), st);
+        if (rest > 0) {
+            launch_trsm_unit_lower_rows(A, n, int(k0), w, int(k0 + w), int(rest), st);
+            GemmBuild gb;
+            gb.add1(A + (k0 + w) * n + (k0 + w), n, int(rest), int(rest), GEMM_ADD,
+                    contrib(A + (k0 + w) * n + k0, n, 0, A + k0 * n + (k0 + w), n, 0, w, -1.0));
+            gb.launch(kid_gemm);
+        }
+    }
+    launch_diag_absmin(A, n, int(n), red + 1, st);
 }
 
 namespace {

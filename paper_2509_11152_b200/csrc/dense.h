@@ -43,4 +43,10 @@ void complement_blocked(const std::vector<ComplementTask>& tasks, Region& scr);
 void jacobi_multi_cta(const std::vector<SvdTask>& tasks, double thresh, Region& scr, bool pairwise = false,
                       std::vector<int32_t*>* flags_out = nullptr);
 
+// partial-pivot LU of the n x n row-major A in place (LAPACK getrf pivots,
+// 0-based): cooperative panels + DMMA trailing updates.  red[0] = max|A|
+// before, red[1] = min|diag(U)| after (device; the vanishing-pivot test).
+void blocked_lu(double* A, int64_t n, int32_t* piv, Region& scr, double* red, int kid_panel, int kid_misc,
+                int kid_gemm);
+
 }  // namespace h2f

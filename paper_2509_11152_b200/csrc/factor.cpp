@@ -175,7 +175,7 @@ int env_int(const char* name, int dflt) {
 // Q~ for a set of clusters: one CTA per cluster up to H2F_HH_MIN_S rows,
 // the blocked Householder with cooperative panels above
 void complement(const std::vector<ComplementTask>& tasks, Region& scr) {
-    static const int min_s = env_int("H2F_HH_MIN_S", 128);
+    const int min_s = env_int("H2F_HH_MIN_S", 224);
     int lim = min_s;
     if (const char* env = std::getenv("H2F_SMALL_N_MAX")) lim = std::min(lim, std::atoi(env));
     std::vector<ComplementTask> small, big;
@@ -546,9 +546,19 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     std::vector<Elim> el;
     int* status_d = scr.alloc_n<int>(nb);
     {
-        CopyBuild panels;
+        CopyBuild panels, lu_copy;
         std::vector<LuTask> lus;
-        std::vector<TrsmTask> trs;
+        struct BigLu {
+            double* lu;
+            int32_t* piv;
+            int r;
+            int* status;
+        };
+        std::vector<BigLu> lu_big;
+        std::vector<TrsmTask> trs, trs32, trs16;
+        int max_r_dmma[2] = {1, 1};
+        const int lu_blocked_min = env_int("H2F_LU_BLOCKED_MIN", 192);
+        const int trsm_dmma_min = env_int("H2F_TRSM_DMMA_MIN", 48);
         H2F_CUDA(cudaMemsetAsync(status_d, 0, sizeof(int) * nb, st));
         for (int bi = 0; bi < nb; ++bi) {
             const int c = batch[bi], ci = L.at(c);
@@ -592,16 +602,23 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 else
                     panels.add(e.G + e.offs[i], e.W, r, B.rows, B.p, B.ld, 1, COPY_SET);
             }
-            LuTask lt{};
-            lt.D = Dcc.p;
-            lt.ldd = Dcc.ld;
-            lt.LU = cf.lu;
-            lt.piv = cf.piv;
-            lt.r = r;
-            lt.cluster = c;
-            lt.status = status_d + bi;
-            lus.push_back(lt);
-            for (int64_t c0 = 0; c0 < e.W; c0 += 128) {
+            if (r > lu_blocked_min) {
+                // large redundant blocks: cooperative-panel LU with DMMA updates
+                lu_copy.add(cf.lu, r, r, r, Dcc.p, Dcc.ld, 0, COPY_SET);
+                lu_big.push_back({cf.lu, cf.piv, r, status_d + bi});
+            } else {
+                LuTask lt{};
+                lt.D = Dcc.p;
+                lt.ldd = Dcc.ld;
+                lt.LU = cf.lu;
+                lt.piv = cf.piv;
+                lt.r = r;
+                lt.cluster = c;
+                lt.status = status_d + bi;
+                lus.push_back(lt);
+            }
+            const int nc = r >= trsm_dmma_min ? trsm_dmma_cols(r) : 0;
+            for (int64_t c0 = 0; c0 < e.W; c0 += (nc ? nc : 128)) {
                 TrsmTask tt{};
                 tt.LU = cf.lu;
                 tt.piv = cf.piv;
@@ -612,7 +629,8 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 tt.r = r;
                 tt.W = int(e.W);
                 tt.col0 = int(c0);
-                trs.push_back(tt);
+                (nc == 32 ? trs32 : nc == 16 ? trs16 : trs).push_back(tt);
+                if (nc) max_r_dmma[nc == 32 ? 0 : 1] = std::max(max_r_dmma[nc == 32 ? 0 : 1], r);
             }
             // edges (factorization.py:453-456)
             cf.edges.push_back({c, EDGE_SELF, e.MW, e.W, kt});
@@ -635,10 +653,18 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         {
             ProfScope ps(K_LU, lf, lb);
             if (!lus.empty()) launch_lu(upload(lus), int32_t(lus.size()), st);
+            lu_copy.launch();
+            for (auto& b : lu_big) {
+                double* red = scr.alloc_n<double>(2);
+                blocked_lu(b.lu, b.r, b.piv, scr, red, -1, -1, -1);
+                launch_lu_status(red, b.r, b.status, st);
+            }
         }
         {
             ProfScope ps(K_TRSM, tf, tb);
             if (!trs.empty()) launch_trsm(upload(trs), int32_t(trs.size()), st);
+            if (!trs32.empty()) launch_trsm_dmma(upload(trs32), int32_t(trs32.size()), max_r_dmma[0], 32, st);
+            if (!trs16.empty()) launch_trsm_dmma(upload(trs16), int32_t(trs16.size()), max_r_dmma[1], 16, st);
         }
     }
 
@@ -988,34 +1014,7 @@ void Factorizer::top_factor(double* A, int64_t n) {
     cudaStream_t st = X.stream;
     if (n == 0) return;
     double* red = scratch[0].alloc_n<double>(2);
-    launch_absmax(A, n, int(n), int(n), red, st);
-    const int nb = TOP_PANEL_NB;
-    const int g = top_panel_grid(int(n));
-    TopPanelScratch ps_scr;
-    ps_scr.val = scratch[0].alloc_n<double>(2 * g);
-    ps_scr.idx = scratch[0].alloc_n<int>(2 * g);
-    ps_scr.rows = scratch[0].alloc_n<double>(int64_t(2) * g * TOP_PANEL_NB);
-    ps_scr.rowk = scratch[0].alloc_n<double>(2 * TOP_PANEL_NB);
-    ps_scr.bar = scratch[0].alloc_n<unsigned>(2);
-    for (int64_t k0 = 0; k0 < n; k0 += nb) {
-        const int w = int(std::min<int64_t>(nb, n - k0));
-        {
-            ProfScope ps(K_TOP_PANEL, double(n - k0) * w * w, 16.0 * double(n - k0) * w);
-            if (!launch_coop_panel_lu(A, n, int(n), int(k0), w, F.top_piv, ps_scr, st))
-                launch_panel_lu(A, n, int(n), int(k0), w, F.top_piv, st);
-        }
-        const int64_t rest = n - k0 - w;
-        ProfScope ps(K_TOP_MISC, double(rest) * w * w, 16.0 * double(n) * w + 16.0 * double(rest) * w);
-        launch_row_swaps(A, n, int(n), int(k0), w, F.top_piv, int(k0), int(k0 + w), st);
-        if (rest > 0) {
-            launch_trsm_unit_lower_rows(A, n, int(k0), w, int(k0 + w), int(rest), st);
-            GemmBuild g;
-            g.add1(A + (k0 + w) * n + (k0 + w), n, int(rest), int(rest), GEMM_ADD,
-                   contrib(A + (k0 + w) * n + k0, n, 0, A + k0 * n + (k0 + w), n, 0, w, -1.0));
-            g.launch(K_GEMM_TOP);
-        }
-    }
-    launch_diag_absmin(A, n, int(n), red + 1, st);
+    blocked_lu(A, n, F.top_piv, scratch[0], red, K_TOP_PANEL, K_TOP_MISC, K_GEMM_TOP);
     double* h = static_cast<double*>(X.pinned_buf(16));
     H2F_CUDA(cudaMemcpyAsync(h, red, 16, cudaMemcpyDeviceToHost, st));
     X.sync();

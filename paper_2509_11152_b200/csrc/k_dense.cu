@@ -98,6 +98,20 @@ __global__ void __launch_bounds__(DT) qr_r_smem_kernel(const QrTask* __restrict_
     }
 }
 
+// Jacobi rotation annihilating the (p, q) inner product: a = |x_p|^2,
+// b = |x_q|^2, g = x_p.x_q.  Rotate iff |g| > tol sqrt(a b) (tested
+// squared); t = tan(theta) = sgn(d) 2g / (|d| + sqrt(d^2 + 4 g^2)), d = b - a
+// (the Rutishauser formula without the zeta division): one sqrt, one
+// division and one rsqrt per rotation.
+__device__ __forceinline__ bool jac_rotation(double a, double b, double g, double tol, double& c, double& sn) {
+    if (!(g != 0.0 && a > 0.0 && b > 0.0 && g * g > (tol * tol) * (a * b))) return false;
+    const double d = b - a;
+    const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(d * d + 4.0 * g * g));
+    c = rsqrt(1.0 + t * t);
+    sn = c * t;
+    return true;
+}
+
 // circle-method round robin: player list [0, rot...]; pair i of round st
 __device__ __forceinline__ void rr_pair(int i, int st, int mm, int& p, int& q) {
     auto pos = [&](int j) { return j == 0 ? 0 : 1 + ((j - 1 + st) % (mm - 1)); };
@@ -130,10 +144,8 @@ __device__ void jacobi_sweeps(double* A, int m, int n, int* flag) {
                 a = warp_sum(a);
                 b = warp_sum(b);
                 g = warp_sum(g);
-                if (g != 0.0 && a > 0.0 && b > 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b)) {
-                    const double zeta = (b - a) / (2.0 * g);
-                    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+                double c, sn;
+                if (jac_rotation(a, b, g, tol, c, sn)) {
                     for (int i = lane; i < n; i += 32) {
                         const double x = rp[i], y = rq[i];
                         rp[i] = c * x - sn * y;
@@ -341,10 +353,8 @@ __device__ __forceinline__ bool jac_pair_loop(double* __restrict__ rp, double* _
     a = warp_sum(a);
     b = warp_sum(b);
     g = warp_sum(g);
-    if (!(g != 0.0 && a > 0.0 && b > 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b))) return false;
-    const double zeta = (b - a) / (2.0 * g);
-    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-    const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+    double c, sn;
+    if (!jac_rotation(a, b, g, tol, c, sn)) return false;
     for (int i = lane; i < n; i += 32) {
         const double x = __ldcg(rp + i), y = __ldcg(rq + i);
         __stcg(rp + i, c * x - sn * y);
@@ -374,10 +384,8 @@ __device__ __forceinline__ bool jac_pair_reg(double* __restrict__ rp, double* __
     a = warp_sum(a);
     b = warp_sum(b);
     g = warp_sum(g);
-    if (!(g != 0.0 && a > 0.0 && b > 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b))) return false;
-    const double zeta = (b - a) / (2.0 * g);
-    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-    const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+    double c, sn;
+    if (!jac_rotation(a, b, g, tol, c, sn)) return false;
 #pragma unroll
     for (int k = 0; k < NPL; ++k) {
         const int i = lane + 32 * k;
@@ -497,10 +505,8 @@ __device__ __forceinline__ bool jac_rotate_smem(double* __restrict__ x, double* 
     a = warp_sum(a);
     b = warp_sum(b);
     g = warp_sum(g);
-    if (!(g != 0.0 && a > 0.0 && b > 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b))) return false;
-    const double zeta = (b - a) / (2.0 * g);
-    const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-    const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+    double c, sn;
+    if (!jac_rotation(a, b, g, tol, c, sn)) return false;
     for (int i = lane; i < n; i += 32) {
         const double u = x[i], v = y[i];
         x[i] = c * u - sn * v;
@@ -534,12 +540,30 @@ __global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* 
             rr_pair(rank, st, NB2, bp, bq);
             const int p0 = bp * JB, q0 = bq * JB;
             const int np = max(0, min(JB, m - p0)), nq = max(0, min(JB, m - q0));
-            // stage (rows beyond m are zero and never rotate)
-            for (int e = threadIdx.x; e < 2 * JB * n; e += JT) {
-                const int r = e / n, i = e % n;
-                const int row = r < JB ? p0 + r : q0 + r - JB;
-                const bool v = r < JB ? r < np : r - JB < nq;
-                bsm[e] = v ? __ldcg(A + (int64_t)row * n + i) : 0.0;
+            // stage: 16 independent L2 loads in flight per thread (rows beyond
+            // m are zero and never rotate); (r, i) advance without division
+            {
+                int r = threadIdx.x / n, i = threadIdx.x % n;
+                while (r < 2 * JB) {
+                    double v[16];
+                    int rr[16], ii[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        rr[u] = r;
+                        ii[u] = i;
+                        const int row = r < JB ? p0 + r : q0 + r - JB;
+                        const bool ok = r < 2 * JB && (r < JB ? r < np : r - JB < nq);
+                        v[u] = ok ? __ldcg(A + (int64_t)row * n + i) : 0.0;
+                        i += JT;
+                        while (i >= n) {
+                            i -= n;
+                            ++r;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u)
+                        if (rr[u] < 2 * JB) bsm[(int64_t)rr[u] * n + ii[u]] = v[u];
+                }
             }
             __syncthreads();
             if (st == 0) {
@@ -564,11 +588,13 @@ __global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* 
                     rotated |= jac_rotate_smem(bsm + (int64_t)i * n, bsm + (int64_t)(JB + (i + s) % JB) * n, n, tol);
                 __syncthreads();
             }
-            for (int e = threadIdx.x; e < 2 * JB * n; e += JT) {
-                const int r = e / n, i = e % n;
+            for (int r = 0; r < 2 * JB; ++r) {
                 const int row = r < JB ? p0 + r : q0 + r - JB;
                 const bool v = r < JB ? r < np : r - JB < nq;
-                if (v) __stcg(A + (int64_t)row * n + i, bsm[e]);
+                if (!v) continue;
+                double* dst = A + (int64_t)row * n;
+                const double* src = bsm + (int64_t)r * n;
+                for (int i = threadIdx.x; i < n; i += JT) __stcg(dst + i, src[i]);
             }
             cta_group_barrier(CT.bar, P);
         }
@@ -719,6 +745,106 @@ __global__ void __launch_bounds__(TRSM_T) trsm_kernel(const TrsmTask* __restrict
         X[(int64_t)i * ldw] = acc / ui[i];
     }
     for (int i = 0; i < r; ++i) X[(int64_t)i * ldw] = -X[(int64_t)i * ldw];
+}
+
+// ---- blocked TRSM on DMMA: MW = -(U^-1 L^-1 P G), NC columns per CTA ---------
+// The CTA keeps its NC-column slice X (r x NC) in shared memory; per 32-row
+// block the update by the already solved rows is an 8x8x4 DMMA product with
+// the L (U) block row streamed from L2, followed by a sequential in-block
+// substitution (one thread per column) against the block staged in shared
+// memory.  Same forward/backward substitution as getrs (factorization.py:120).
+template <int NC>
+__global__ void __launch_bounds__(256, 1) trsm_dmma_kernel(const TrsmTask* __restrict__ tasks) {
+    constexpr int NCP = NC + 4;          // conflict-free B fragments
+    constexpr int TN = NC / 8;           // 8x8 tiles across
+    constexpr int TPW = (4 * TN) / 8;    // tiles per warp (8 warps, 32-row blocks)
+    const TrsmTask T = tasks[blockIdx.x];
+    const int r = T.r, r4 = (r + 3) & ~3;
+    const int ncols = min(NC, T.W - T.col0);
+    extern __shared__ double X[];        // r4 x NCP
+    __shared__ double Lb[32][33];
+    int* perm = reinterpret_cast<int*>(X + (int64_t)r4 * NCP);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const double* LU = T.LU;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < r; ++i) perm[i] = i;
+        for (int k = 0; k < r; ++k) {
+            const int p = T.piv[k];
+            const int t0 = perm[k];
+            perm[k] = perm[p];
+            perm[p] = t0;
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < r4 * NC; e += 256) {
+        const int i = e / NC, c = e % NC;
+        X[i * NCP + c] = (i < r && c < ncols) ? T.G[(int64_t)perm[i] * T.ldg + T.col0 + c] : 0.0;
+    }
+    __syncthreads();
+    const int nblk = (r + 31) / 32;
+    for (int dir = 0; dir < 2; ++dir) {  // 0: unit lower, forward; 1: upper, backward
+        for (int bb = 0; bb < nblk; ++bb) {
+            const int blk = dir == 0 ? bb : nblk - 1 - bb;
+            const int b0 = blk * 32, nb = min(32, r - b0);
+            const int k_lo = dir == 0 ? 0 : b0 + nb, k_hi = dir == 0 ? b0 : r;
+            if (k_hi > k_lo) {
+                double c[TPW][2];
+#pragma unroll
+                for (int u = 0; u < TPW; ++u) c[u][0] = c[u][1] = 0.0;
+                for (int k = k_lo; k < k_hi; k += 4) {
+#pragma unroll
+                    for (int u = 0; u < TPW; ++u) {
+                        const int tid_ = warp * TPW + u, ti = tid_ / TN, tj = tid_ % TN;
+                        const int row = ti * 8 + g;
+                        const double a = (row < nb && k + t < k_hi) ? __ldg(LU + (int64_t)(b0 + row) * r + k + t) : 0.0;
+                        const double bv = X[(k + t) * NCP + tj * 8 + g];
+                        dmma_8x8x4(c[u][0], c[u][1], a, bv);
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int u = 0; u < TPW; ++u) {
+                    const int tid_ = warp * TPW + u, ti = tid_ / TN, tj = tid_ % TN;
+                    const int row = ti * 8 + g;
+                    if (row < nb) {
+                        X[(b0 + row) * NCP + tj * 8 + 2 * t] -= c[u][0];
+                        X[(b0 + row) * NCP + tj * 8 + 2 * t + 1] -= c[u][1];
+                    }
+                }
+            }
+            for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+                const int i = e >> 5, k = e & 31;
+                Lb[i][k] = (i < nb && k < nb) ? LU[(int64_t)(b0 + i) * r + b0 + k] : 0.0;
+            }
+            __syncthreads();
+            if (threadIdx.x < NC) {
+                double* xc = X + (int64_t)b0 * NCP + threadIdx.x;
+                if (dir == 0) {
+                    for (int i = 1; i < nb; ++i) {
+                        double acc = xc[i * NCP];
+                        for (int k = 0; k < i; ++k) acc -= Lb[i][k] * xc[k * NCP];
+                        xc[i * NCP] = acc;
+                    }
+                } else {
+                    for (int i = nb - 1; i >= 0; --i) {
+                        double acc = xc[i * NCP];
+                        for (int k = i + 1; k < nb; ++k) acc -= Lb[i][k] * xc[k * NCP];
+                        xc[i * NCP] = acc / Lb[i][i];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int e = threadIdx.x; e < r * NC; e += 256) {
+        const int i = e / NC, c = e % NC;
+        if (c < ncols) T.MW[(int64_t)i * T.ldw + T.col0 + c] = -X[i * NCP + c];
+    }
+}
+
+__global__ void lu_status_kernel(const double* red, int r, int* status) {
+    *status = (r > 0 && red[1] <= 1e-14 * fmax(red[0], 1e-300)) ? 1 : 0;
 }
 
 // ---- dense top LU pieces --------------------------------------------------------
@@ -937,6 +1063,33 @@ cudaError_t launch_jacobi_block(const CoopSvdTask* d_tasks, int32_t total_ctas, 
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(total_ctas), dim3(JT), args, smem, st);
     count_launch();
     return e;
+}
+
+
+int trsm_dmma_cols(int r) {
+    if (size_t(r + 4) * 36 * 8 + size_t(r) * 4 <= size_t(200) * 1024) return 32;
+    if (size_t(r + 4) * 20 * 8 + size_t(r) * 4 <= size_t(200) * 1024) return 16;
+    return 0;
+}
+
+void launch_trsm_dmma(const TrsmTask* d_tasks, int32_t ntasks, int32_t max_r, int32_t nc, cudaStream_t st) {
+    if (ntasks <= 0) return;
+    const int r4 = (max_r + 3) & ~3;
+    if (nc == 32) {
+        const size_t smem = size_t(r4) * 36 * 8 + size_t(max_r) * 4 + 16;
+        cudaFuncSetAttribute(trsm_dmma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        trsm_dmma_kernel<32><<<ntasks, 256, smem, st>>>(d_tasks);
+    } else {
+        const size_t smem = size_t(r4) * 20 * 8 + size_t(max_r) * 4 + 16;
+        cudaFuncSetAttribute(trsm_dmma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        trsm_dmma_kernel<16><<<ntasks, 256, smem, st>>>(d_tasks);
+    }
+    count_launch();
+}
+
+void launch_lu_status(const double* red, int32_t r, int32_t* status, cudaStream_t st) {
+    lu_status_kernel<<<1, 1, 0, st>>>(red, r, status);
+    count_launch();
 }
 
 void launch_complement(const ComplementTask* d_tasks, int32_t ntasks, cudaStream_t st) {

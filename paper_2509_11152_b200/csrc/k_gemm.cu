@@ -20,148 +20,9 @@ namespace h2f {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, PADS = 8, LDS = BM + PADS;
+constexpr int BM = 64, BN = 64;
 constexpr int GEMM_THREADS = 128;
 
-struct Frag {
-    double a[8];
-    double b[8];
-};
-
-__device__ __forceinline__ void load_tile(const GemmContrib& P, int M, int N, int m0, int n0,
-                                          int k0, Frag& f) {
-    const int tid = threadIdx.x;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int e = tid + GEMM_THREADS * i;
-        int k, m;
-        if (P.transA) { k = e >> 6; m = e & 63; } else { k = e & 15; m = e >> 4; }
-        const int gk = k0 + k, gm = m0 + m;
-        double v = 0.0;
-        if (gk < P.K && gm < M)
-            v = P.transA ? __ldg(P.A + (int64_t)gk * P.lda + gm) : __ldg(P.A + (int64_t)gm * P.lda + gk);
-        f.a[i] = v * P.alpha;
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int e = tid + GEMM_THREADS * i;
-        int k, n;
-        if (P.transB) { k = e & 15; n = e >> 4; } else { k = e >> 6; n = e & 63; }
-        const int gk = k0 + k, gn = n0 + n;
-        double v = 0.0;
-        if (gk < P.K && gn < N)
-            v = P.transB ? __ldg(P.B + (int64_t)gn * P.ldb + gk) : __ldg(P.B + (int64_t)gk * P.ldb + gn);
-        f.b[i] = v;
-    }
-}
-
-__device__ __forceinline__ void store_tile(const GemmContrib& P, const Frag& f,
-                                           double (*As)[LDS], double (*Bs)[LDS]) {
-    const int tid = threadIdx.x;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int e = tid + GEMM_THREADS * i;
-        int k, m;
-        if (P.transA) { k = e >> 6; m = e & 63; } else { k = e & 15; m = e >> 4; }
-        As[k][m] = f.a[i];
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int e = tid + GEMM_THREADS * i;
-        int k, n;
-        if (P.transB) { k = e & 15; n = e >> 4; } else { k = e >> 6; n = e & 63; }
-        Bs[k][n] = f.b[i];
-    }
-}
-
-__global__ void __launch_bounds__(GEMM_THREADS)
-gemm_tasks_v1_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restrict__ contribs,
-                     const int64_t* __restrict__ tile_start, int ntasks, int64_t ntiles,
-                     double* __restrict__ norms) {
-    __shared__ __align__(16) double As[2][BK][LDS];
-    __shared__ __align__(16) double Bs[2][BK][LDS];
-    __shared__ double red[GEMM_THREADS / 32];
-
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, t = lane & 3;
-    const int wm = warp >> 1, wn = warp & 1;
-
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int ti = find_segment(tile_start, ntasks, tile);
-        const GemmTask T = tasks[ti];
-        const int64_t local = tile - tile_start[ti];
-        const int m0 = (int)(local / T.tiles_n) * BM;
-        const int n0 = (int)(local % T.tiles_n) * BN;
-
-        double acc[4][4][2];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-        for (int64_t ci = T.contrib_begin; ci < T.contrib_end; ++ci) {
-            const GemmContrib P = contribs[ci];
-            const int nk = (P.K + BK - 1) / BK;
-            if (nk == 0) continue;
-            Frag f;
-            load_tile(P, T.M, T.N, m0, n0, 0, f);
-            store_tile(P, f, As[0], Bs[0]);
-            __syncthreads();
-            for (int kc = 0; kc < nk; ++kc) {
-                const int cur = kc & 1;
-                if (kc + 1 < nk) load_tile(P, T.M, T.N, m0, n0, (kc + 1) * BK, f);
-#pragma unroll
-                for (int kk = 0; kk < BK; kk += 4) {
-                    double a[4], b[4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) a[i] = As[cur][kk + t][wm * 32 + i * 8 + g];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) b[j] = Bs[cur][kk + t][wn * 32 + j * 8 + g];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-                }
-                if (kc + 1 < nk) store_tile(P, f, As[cur ^ 1], Bs[cur ^ 1]);
-                __syncthreads();
-            }
-        }
-
-        if (T.mode == GEMM_NORM) {
-            double ss = 0.0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const int row = m0 + wm * 32 + i * 8 + g;
-                        const int col = n0 + wn * 32 + j * 8 + 2 * t + q;
-                        if (row < T.M && col < T.N) ss += acc[i][j][q] * acc[i][j][q];
-                    }
-            ss = block_sum(ss, red);
-            if (threadIdx.x == 0) norms[T.norm_base + local] = ss;
-        } else {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int row = m0 + wm * 32 + i * 8 + g;
-                if (row >= T.M) continue;
-                double* crow = T.C + (int64_t)row * T.ldc;
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const int col = n0 + wn * 32 + j * 8 + 2 * t + q;
-                        if (col < T.N) {
-                            if (T.mode == GEMM_ADD) crow[col] += acc[i][j][q];
-                            else crow[col] = acc[i][j][q];
-                        }
-                    }
-            }
-        }
-        __syncthreads();
-    }
-}
 
 // ---- v2: cp.async multi-stage pipeline over the concatenated K of all
 // contributions of a tile (no pipeline restart between contributions); the
@@ -238,84 +99,112 @@ __device__ __forceinline__ void mma_chunk(const double* __restrict__ As, const d
     }
 }
 
+// One CTA walks a contiguous range of tiles as a single stream of K chunks
+// (tile -> contributions in order -> BK2 chunks): the producer issues cp.async
+// STAGES-1 chunks ahead across contribution and tile boundaries, so the
+// descriptor loads and the next tile's operand loads overlap the current
+// tile's math and epilogue.  Per-stage metadata (contribution, tile origin,
+// last-chunk-of-tile flag) travels with the stage through shared memory.
+struct ChunkMeta {
+    int contrib;  // global contribution index; -1: stream ended; -2: tile without contributions
+    int ti;       // task
+    int m0, n0;
+    int last;     // last chunk of its tile: run the epilogue after it
+    int pad_;
+    int64_t local;  // tile index within the task
+};
+
 __global__ void __launch_bounds__(GEMM_THREADS, 2)
 gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restrict__ contribs,
                   const int64_t* __restrict__ tile_start, int ntasks, int64_t ntiles,
                   double* __restrict__ norms) {
     extern __shared__ __align__(16) double gsm[];
     __shared__ double red[GEMM_THREADS / 32];
-    __shared__ int chunk_contrib[STAGES], chunk_k0[STAGES];
+    __shared__ ChunkMeta meta[STAGES];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm = warp >> 1, wn = warp & 1;
 
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int ti = find_segment(tile_start, ntasks, tile);
-        const GemmTask T = tasks[ti];
-        const int64_t local = tile - tile_start[ti];
-        const int m0 = (int)(local / T.tiles_n) * BM;
-        const int n0 = (int)(local % T.tiles_n) * BN;
+    const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const int64_t t_begin = (int64_t)blockIdx.x * per, t_end = min(ntiles, t_begin + per);
+    if (t_begin >= t_end) return;
 
-        double acc[4][4][2];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-        // producer cursor over (contribution, k0) chunks
-        int64_t pc = T.contrib_begin;
-        int pk = 0;
-        auto advance = [&]() {
-            pk += BK2;
-            if (pk >= contribs[pc].K) {
-                pk = 0;
-                ++pc;
-                while (pc < T.contrib_end && contribs[pc].K <= 0) ++pc;
+    // ---- producer cursor (uniform across the CTA) ----
+    int64_t p_tile = t_begin;
+    int p_ti = find_segment(tile_start, ntasks, t_begin);
+    int64_t p_pc = 0, p_end = 0;
+    int p_pk = 0, p_m0 = 0, p_n0 = 0, p_M = 0, p_N = 0;
+    int64_t p_local = 0;
+    auto open_tile = [&]() {
+        while (p_ti + 1 < ntasks && p_tile >= tile_start[p_ti + 1]) ++p_ti;
+        const GemmTask& T = tasks[p_ti];
+        p_local = p_tile - tile_start[p_ti];
+        p_m0 = (int)(p_local / T.tiles_n) * BM;
+        p_n0 = (int)(p_local % T.tiles_n) * BN;
+        p_M = T.M;
+        p_N = T.N;
+        p_pc = T.contrib_begin;
+        p_end = T.contrib_end;
+        p_pk = 0;
+        while (p_pc < p_end && contribs[p_pc].K <= 0) ++p_pc;
+    };
+    open_tile();
+    auto issue = [&](int stage) {
+        ChunkMeta m{};
+        if (p_tile >= t_end) {
+            m.contrib = -1;
+        } else if (p_pc >= p_end) {  // tile without contributions: epilogue only
+            m.contrib = -2;
+            m.ti = p_ti;
+            m.m0 = p_m0;
+            m.n0 = p_n0;
+            m.local = p_local;
+            m.last = 1;
+            ++p_tile;
+            if (p_tile < t_end) open_tile();
+        } else {
+            const GemmContrib P = contribs[p_pc];
+            double* As = gsm + (2 * stage) * STAGE_ELEMS;
+            stage_chunk(P, p_M, p_N, p_m0, p_n0, p_pk, As, As + STAGE_ELEMS);
+            m.contrib = (int)p_pc;
+            m.ti = p_ti;
+            m.m0 = p_m0;
+            m.n0 = p_n0;
+            m.local = p_local;
+            p_pk += BK2;
+            if (p_pk >= P.K) {
+                p_pk = 0;
+                ++p_pc;
+                while (p_pc < p_end && contribs[p_pc].K <= 0) ++p_pc;
             }
-        };
-        while (pc < T.contrib_end && contribs[pc].K <= 0) ++pc;
-        // prologue: STAGES - 1 chunks in flight
-#pragma unroll
-        for (int s = 0; s < STAGES - 1; ++s) {
-            if (pc < T.contrib_end) {
-                const GemmContrib P = contribs[pc];
-                double* As = gsm + (2 * s) * STAGE_ELEMS;
-                stage_chunk(P, T.M, T.N, m0, n0, pk, As, As + STAGE_ELEMS);
-                if (threadIdx.x == 0) {
-                    chunk_contrib[s] = (int)(pc - T.contrib_begin);
-                    chunk_k0[s] = pk;
-                }
-                advance();
-            } else if (threadIdx.x == 0) {
-                chunk_contrib[s] = -1;
+            m.last = p_pc >= p_end;
+            if (m.last) {
+                ++p_tile;
+                if (p_tile < t_end) open_tile();
             }
-            cp_async_commit();
         }
-        for (int it = 0;; ++it) {
-            const int cur = it % STAGES;
-            cp_async_wait<STAGES - 2>();
-            __syncthreads();
-            const int cc = chunk_contrib[cur];
-            if (cc < 0) break;
-            // refill the stage consumed last iteration
-            {
-                const int nxt = (it + STAGES - 1) % STAGES;
-                if (pc < T.contrib_end) {
-                    const GemmContrib P = contribs[pc];
-                    double* As = gsm + (2 * nxt) * STAGE_ELEMS;
-                    stage_chunk(P, T.M, T.N, m0, n0, pk, As, As + STAGE_ELEMS);
-                    if (threadIdx.x == 0) {
-                        chunk_contrib[nxt] = (int)(pc - T.contrib_begin);
-                        chunk_k0[nxt] = pk;
-                    }
-                    advance();
-                } else if (threadIdx.x == 0) {
-                    chunk_contrib[nxt] = -1;
-                }
-                cp_async_commit();
-            }
-            const GemmContrib P = contribs[T.contrib_begin + cc];
+        if (threadIdx.x == 0) meta[stage] = m;
+        cp_async_commit();
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int st = 0; st < STAGES - 1; ++st) issue(st);
+    for (int it = 0;; ++it) {
+        const int cur = it % STAGES;
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        const ChunkMeta m = meta[cur];
+        if (m.contrib == -1) break;
+        issue((it + STAGES - 1) % STAGES);  // refills the stage consumed last iteration
+        if (m.contrib >= 0) {
+            const GemmContrib P = contribs[m.contrib];
             const double* As = gsm + (2 * cur) * STAGE_ELEMS;
             const double* Bs = As + STAGE_ELEMS;
             // zero-filled tails add exact zeros: no k bound inside the chunk
@@ -326,9 +215,10 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
             default: mma_chunk<true, true>(As, Bs, acc, wm, wn, g, t); break;
             }
         }
-        cp_async_wait<0>();
+        if (!m.last) continue;
+        // ---- epilogue of tile m ----
+        const GemmTask T = tasks[m.ti];
         const double alpha = (T.contrib_end > T.contrib_begin) ? contribs[T.contrib_begin].alpha : 1.0;
-
         if (T.mode == GEMM_NORM) {
             double ss = 0.0;
 #pragma unroll
@@ -337,33 +227,56 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
                 for (int j = 0; j < 4; ++j)
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
-                        const int row = m0 + wm * 32 + i * 8 + g;
-                        const int col = n0 + wn * 32 + j * 8 + 2 * t + q;
+                        const int row = m.m0 + wm * 32 + i * 8 + g;
+                        const int col = m.n0 + wn * 32 + j * 8 + 2 * t + q;
                         const double v = alpha * acc[i][j][q];
                         if (row < T.M && col < T.N) ss += v * v;
                     }
+            // block_sum's barriers are uniform: every thread reaches this epilogue
             ss = block_sum(ss, red);
-            if (threadIdx.x == 0) norms[T.norm_base + local] = ss;
+            if (threadIdx.x == 0) norms[T.norm_base + m.local] = ss;
         } else {
+            // all loads of the tile's C first (one memory round trip), then
+            // the stores: the compiler cannot hoist loads over possibly
+            // aliasing stores on its own
+            double cv[4][4][2];
+            if (T.mode == GEMM_ADD) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int row = m.m0 + wm * 32 + i * 8 + g;
+                    const double* crow = T.C + (int64_t)row * T.ldc;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const int col = m.n0 + wn * 32 + j * 8 + 2 * t + q;
+                            cv[i][j][q] = (row < T.M && col < T.N) ? crow[col] : 0.0;
+                        }
+                }
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int row = m0 + wm * 32 + i * 8 + g;
+                const int row = m.m0 + wm * 32 + i * 8 + g;
                 if (row >= T.M) continue;
                 double* crow = T.C + (int64_t)row * T.ldc;
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
-                        const int col = n0 + wn * 32 + j * 8 + 2 * t + q;
+                        const int col = m.n0 + wn * 32 + j * 8 + 2 * t + q;
                         if (col < T.N) {
                             const double v = alpha * acc[i][j][q];
-                            if (T.mode == GEMM_ADD) crow[col] += v; else crow[col] = v;
+                            crow[col] = T.mode == GEMM_ADD ? cv[i][j][q] + v : v;
                         }
                     }
             }
         }
-        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     }
+    cp_async_wait<0>();
 }
 
 constexpr int CT = 32;  // copy tile
@@ -452,19 +365,13 @@ void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
                        const int64_t* d_tile_start, int32_t ntasks, int64_t ntiles,
                        double* d_norms, cudaStream_t st) {
     if (ntiles <= 0) return;
-    static const bool v1 = std::getenv("H2F_GEMM_V1") != nullptr;
-    if (v1) {
-        gemm_tasks_v1_kernel<<<grid_for(ntiles, 8), GEMM_THREADS, 0, st>>>(d_tasks, d_contribs, d_tile_start,
-                                                                          ntasks, ntiles, d_norms);
-    } else {
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(gemm_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM2_SMEM);
-            configured = true;
-        }
-        gemm_tasks_kernel<<<grid_for(ntiles, 2), GEMM_THREADS, GEMM2_SMEM, st>>>(d_tasks, d_contribs, d_tile_start,
-                                                                                 ntasks, ntiles, d_norms);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(gemm_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM2_SMEM);
+        configured = true;
     }
+    gemm_tasks_kernel<<<grid_for(ntiles, 2), GEMM_THREADS, GEMM2_SMEM, st>>>(d_tasks, d_contribs, d_tile_start,
+                                                                             ntasks, ntiles, d_norms);
     count_launch();
 }
 

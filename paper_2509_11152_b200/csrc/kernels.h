@@ -135,7 +135,7 @@ struct TrsmTask {        // MW = -(U^-1 L^-1 P G) column block
 // multiple of 4).  Outputs: R/reflectors in place, the explicit unit-lower
 // reflectors Vt (HH_NB x (L-j0), row-major) and T (HH_NB x HH_NB, dlarft).
 constexpr int HH_NB = 32;
-constexpr int HH_CHUNK_MAX = 512;
+constexpr int HH_CHUNK_MAX = 840;  // rows per CTA: 32 x 844 doubles of shared memory
 struct HhPanelTask {
     double* M;
     int64_t ldm;
@@ -252,6 +252,11 @@ constexpr int SMEM_DENSE_MAX_N = 144;  // n x n doubles resident in shared memor
 void launch_complement(const ComplementTask* d_tasks, int32_t ntasks, cudaStream_t st);
 void launch_lu(const LuTask* d_tasks, int32_t ntasks, cudaStream_t st);
 void launch_trsm(const TrsmTask* d_tasks, int32_t ntasks, cudaStream_t st);
+// blocked DMMA TRSM, nc (= trsm_dmma_cols(r), 0: too large) columns per task
+int trsm_dmma_cols(int r);
+void launch_trsm_dmma(const TrsmTask* d_tasks, int32_t ntasks, int32_t max_r, int32_t nc, cudaStream_t st);
+// status = vanishing-pivot test from red = {max|D_RR|, min|diag U|}
+void launch_lu_status(const double* red, int32_t r, int32_t* status, cudaStream_t st);
 void launch_sumsq_reduce(const double* d_parts, const int64_t* d_seg, int32_t nseg,
                          double* d_out, cudaStream_t st);
 

@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -187,9 +188,9 @@ cudaEvent_t Profiler::get_event() {
     return e;
 }
 
-int Profiler::begin(int kid, double flops, double bytes) {
+int Profiler::begin(int kid, double flops, double bytes, double units) {
     if (!on || kid < 0) return -1;
-    Rec r{kid, get_event(), get_event(), flops, bytes};
+    Rec r{kid, get_event(), get_event(), flops, bytes, units};
     H2F_CUDA(cudaEventRecord(r.a, ctx().stream));
     pending_.push_back(r);
     return int(pending_.size()) - 1;
@@ -203,9 +204,15 @@ void Profiler::end(int slot) {
 void Profiler::collect() {
     if (pending_.empty()) return;
     H2F_CUDA(cudaStreamSynchronize(ctx().stream));
+    // H2F_PROF_LOG=path: one line per launch "kernel flops bytes units ms" (development aid)
+    static FILE* log = [] {
+        const char* p = std::getenv("H2F_PROF_LOG");
+        return p ? std::fopen(p, "a") : nullptr;
+    }();
     for (auto& r : pending_) {
         float ms = 0.f;
         H2F_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        if (log) std::fprintf(log, "%s %.6g %.6g %.6g %.6g\n", kernel_name(r.kid), r.flops, r.bytes, r.units, ms);
         Total& t = totals[r.kid];
         t.launches += 1;
         t.seconds += ms * 1e-3;
@@ -226,8 +233,8 @@ Profiler::~Profiler() {
     for (auto e : pool_) cudaEventDestroy(e);
 }
 
-ProfScope::ProfScope(int kid, double flops, double bytes) {
-    if (ctx_ready() && ctx().prof.on) slot = ctx().prof.begin(kid, flops, bytes);
+ProfScope::ProfScope(int kid, double flops, double bytes, double units) {
+    if (ctx_ready() && ctx().prof.on) slot = ctx().prof.begin(kid, flops, bytes, units);
 }
 
 ProfScope::~ProfScope() {

@@ -108,7 +108,7 @@ const char* kernel_name(int kid);
 class Profiler {
   public:
     bool on = false;
-    int begin(int kid, double flops, double bytes);
+    int begin(int kid, double flops, double bytes, double units = 0);
     void end(int slot);
     void collect();  // syncs the stream, folds finished pairs into the totals
     void reset();
@@ -117,7 +117,7 @@ class Profiler {
     ~Profiler();
 
   private:
-    struct Rec { int kid; cudaEvent_t a, b; double flops, bytes; };
+    struct Rec { int kid; cudaEvent_t a, b; double flops, bytes, units; };
     std::vector<Rec> pending_;
     std::vector<cudaEvent_t> pool_;
     cudaEvent_t get_event();
@@ -125,7 +125,7 @@ class Profiler {
 
 struct ProfScope {
     int slot = -1;
-    ProfScope(int kid, double flops = 0, double bytes = 0);
+    ProfScope(int kid, double flops = 0, double bytes = 0, double units = 0);
     ~ProfScope();
 };
 

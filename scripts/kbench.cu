@@ -51,7 +51,10 @@ struct Case {
 };
 
 int main(int argc, char** argv) {
+    const char* only = argc > 1 ? argv[1] : nullptr;
     std::vector<Case> cases = {
+        {"schur_leaf_r13_47x47_x1", 8000, 47, 47, 1, 13, 1, 0},
+        {"schur_r40_110x110_x2", 3000, 110, 110, 2, 40, 1, 0},
         {"schur_r150_300x300_x3", 60, 300, 300, 3, 150, 1, 0},
         {"schur_r60_120x120_x4", 400, 120, 120, 4, 60, 1, 0},
         {"schur_r300_500x500_x2", 12, 500, 500, 2, 300, 1, 0},
@@ -62,6 +65,7 @@ int main(int argc, char** argv) {
     std::mt19937_64 rng(1);
     std::normal_distribution<double> nd;
     for (auto& cs : cases) {
+        if (only && cs.name.find(only) == std::string::npos) continue;
         // operands: one A and B pool per contribution
         const int64_t asz = int64_t(cs.M) * cs.K, bsz = int64_t(cs.K) * cs.N;
         const int64_t npairs = int64_t(cs.ntargets) * cs.ncontrib;

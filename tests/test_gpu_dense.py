@@ -45,8 +45,13 @@ def test_qr_r_matches_lapack(n, wf, path):
         Y = np.random.Generator(np.random.Philox(n)).standard_normal((n, wf))
     R, ms = _lib.dense_qr_r(Y, path)
     R_ref = np.linalg.qr(Y.T, mode="r")
-    # same Householder conventions (dlarfg): R itself agrees, not just R^T R
-    assert np.linalg.norm(R - R_ref) <= 1e-12 * np.linalg.norm(R_ref)
+    if path == 1:
+        # same Householder conventions (dlarfg): R itself agrees
+        assert np.linalg.norm(R - R_ref) <= 1e-12 * np.linalg.norm(R_ref)
+    else:
+        # the shared-memory TSQR folds chunks: R agrees up to row signs
+        d = np.sign(np.diag(R)) * np.sign(np.diag(R_ref))
+        assert np.linalg.norm(d[:, None] * R - R_ref) <= 1e-12 * np.linalg.norm(R_ref)
 
 
 @pytest.mark.parametrize("s,kt,path", [(64, 20, 0), (200, 120, 0), (64, 20, 1), (200, 120, 1), (900, 600, 1),

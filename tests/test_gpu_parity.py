@@ -209,3 +209,27 @@ def test_large_n_path_matches_shared_memory_path(case, monkeypatch):
     assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x2)
     if case != "laplace3d_4096":
         assert structure_of(fac_big) == golden_structure(g)
+
+
+@pytest.mark.parametrize("case", ["cov2d_4096", "cov3d_2048"])
+def test_blocked_lu_and_dmma_trsm_paths(case, monkeypatch):
+    """Force the large-r elimination kernels (cooperative-panel LU, blocked
+    DMMA TRSM; used for r > 192 / r >= 48) onto every cluster: pivots and the
+    whole integer structure stay bit-exact with the reference golden
+    fixture, the solution within 1e-8 of the default path."""
+    g = load(case)
+    _, _, _, h2, prm = problem(case)
+    monkeypatch.setenv("H2F_LU_BLOCKED_MIN", "0")
+    monkeypatch.setenv("H2F_TRSM_DMMA_MIN", "1")
+    fac_b = H.factorize(h2, prm["eps_lu"])
+    monkeypatch.delenv("H2F_LU_BLOCKED_MIN")
+    monkeypatch.delenv("H2F_TRSM_DMMA_MIN")
+    _, _, fac = gpu_factor(case)
+    assert structure_of(fac_b) == golden_structure(g)
+    for lv, rec in zip(g["levels"], fac_b.records):
+        for c, f in rec.factors.items():
+            assert (None if f.piv is None else f.piv.tolist()) == lv["piv"][str(c)]
+    b = rhs(h2, H.matvec)
+    x1 = H.refined_solve(h2, fac_b, b)
+    x2 = H.refined_solve(h2, fac, b)
+    assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x2)
