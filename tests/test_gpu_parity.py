@@ -233,3 +233,36 @@ def test_blocked_lu_and_dmma_trsm_paths(case, monkeypatch):
     x1 = H.refined_solve(h2, fac_b, b)
     x2 = H.refined_solve(h2, fac, b)
     assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x2)
+
+
+def test_solve_multi_sharded_single_rank():
+    """The column-sharded multi-RHS path (config 5) on one GPU: without a
+    process group it is solve_multi; inside a world-size-1 NCCL group the
+    all-gather runs on the device and returns the same bits."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_11152_b200.multigpu import solve_multi_sharded
+
+    h2, prm, fac = gpu_factor("cov2d_1024")
+    B = np.random.default_rng(21).standard_normal((fac.n, 7))
+    X = H.solve_multi(fac, B)
+    assert np.array_equal(solve_multi_sharded(fac, B), X)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        assert np.array_equal(solve_multi_sharded(fac, B), X)
+        with pytest.raises(ValueError):
+            solve_multi_sharded(fac, B[:-1])
+    finally:
+        dist.destroy_process_group()
+    for j in [0, 6]:
+        one = H.solve(fac, B[:, j])
+        assert np.linalg.norm(X[:, j] - one) <= 1e-12 * np.linalg.norm(one)

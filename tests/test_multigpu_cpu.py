@@ -1,0 +1,92 @@
+"""World-size-2 gloo tests of the column-sharded multi-RHS solve
+(paper_2509_11152_b200/multigpu.py, BASELINE config 5).
+
+The per-rank substitution is injected (the CPU oracle's substitute) so the
+host logic -- column ranges, padding of ragged shards, the all-gather and
+the reassembly -- runs here without a GPU.  The GPU path of the same
+function is covered by tests/test_gpu_parity.py::test_solve_multi_sharded_single_rank.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_2509_11152_b200.multigpu import column_ranges
+
+
+def test_column_ranges_cover_and_balance():
+    for q in [0, 1, 7, 8, 255, 256, 257]:
+        for world in [1, 2, 3, 8]:
+            rg = column_ranges(q, world)
+            assert len(rg) == world
+            assert rg[0][0] == 0 and rg[-1][1] == q
+            assert all(a[1] == b[0] for a, b in zip(rg, rg[1:]))
+            widths = [h - l for l, h in rg]
+            assert max(widths) - min(widths) <= 1
+    assert column_ranges(256, 8)[3] == (96, 128)
+    with pytest.raises(ValueError):
+        column_ranges(4, 0)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from threadpoolctl import threadpool_limits
+
+    from golden_util import problem
+    from oracle import h2_oracle as O
+    from paper_2509_11152_b200.multigpu import solve_multi_sharded
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _, _, _, h2, prm = problem("cov2d_1024")
+        with threadpool_limits(1):
+            fac = O.factorize(h2, prm["eps_lu"])
+        B = np.random.default_rng(11).standard_normal((h2.n, q))
+        seen = []
+
+        def solver(block):
+            seen.append(block.shape[1])
+            with threadpool_limits(1):
+                return torch.from_numpy(O.substitute(fac, block.numpy()))
+
+        X = solve_multi_sharded(fac, B, solver=solver)
+        np.save(os.path.join(out_dir, f"x{rank}.npy"), X)
+        np.save(os.path.join(out_dir, f"w{rank}.npy"), np.array(seen))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("q", [5, 8])
+def test_solve_multi_sharded_gloo_world2(tmp_path, q):
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), q, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    from threadpoolctl import threadpool_limits
+
+    from golden_util import problem
+    from oracle import h2_oracle as O
+
+    _, _, _, h2, prm = problem("cov2d_1024")
+    with threadpool_limits(1):
+        fac = O.factorize(h2, prm["eps_lu"])
+        B = np.random.default_rng(11).standard_normal((h2.n, q))
+        # per-shard substitution (BLAS blocking depends on the block width)
+        X_ref = np.hstack([O.substitute(fac, B[:, l:h]) for l, h in column_ranges(q, world)])
+        X_full = O.substitute(fac, B)
+    widths = [int(np.load(tmp_path / f"w{r}.npy")[0]) for r in range(world)]
+    assert widths == [h - l for l, h in column_ranges(q, world)]
+    for r in range(world):
+        X = np.load(tmp_path / f"x{r}.npy")
+        # every rank holds the assembled solution, bit-identical to the shards
+        assert np.array_equal(X, X_ref)
+        assert np.allclose(X, X_full, rtol=0, atol=1e-12 * np.abs(X_full).max())
