@@ -36,6 +36,11 @@ CONFIGS = {
             desc="3D Laplace 1/r N=131072 single GPU (configs[1])"),
     4: dict(problem="helmholtz3d", n=524288, over={"dim": 2, "p0": 8, "eta": 0.9},
             desc="2D oscillatory cos(3r)/r N=524288 (configs[3])"),
+    # configs[4] at single-GPU operator size: the 2^20 factor (>180 GB) does
+    # not fit one B200, so config 2's operator carries the 256-RHS solve
+    5: dict(problem="helmholtz3d", n=131072, over={"kappa": 0.0}, nrhs=256,
+            desc="3D Laplace N=131072 factor reused for a 256-RHS solve_multi, columns sharded over GPUs "
+                 "(configs[4] at the largest single-GPU factor)"),
 }
 DEFAULT_CONFIG = int(os.environ.get("H2F_BENCH_CONFIG", "2"))
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -314,6 +319,97 @@ def run_b200(args, cfg):
         dist.destroy_process_group()
 
 
+def run_multi_rhs(args, cfg):
+    """Config 5: one factorization, then `steps` timed 256-RHS block solves
+    with the columns sharded over the ranks (multigpu.solve_multi_sharded;
+    per-rank substitution on the device, one NCCL all-gather).  Strong
+    scaling: the 256 columns are fixed, each rank solves 256/N."""
+    world, rank, local, dist = dist_setup(want_nccl=True)
+    os.environ["H2F_DEVICE"] = str(local)
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2509_11152_b200 as H
+    from paper_2509_11152_b200 import _lib as L
+    from paper_2509_11152_b200.multigpu import column_ranges, solve_multi_sharded
+
+    n, q = cfg["n"], cfg["nrhs"]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    h2, prm, t_build = build_input(cfg)
+    L.ensure_init()
+    fac = H.factorize(h2, prm["eps_lu"])
+    X_true = np.random.Generator(np.random.Philox(7)).standard_normal((n, q))
+    B = np.empty((n, q))
+    lo, hi = column_ranges(q, world)[rank]
+    for j in range(q):  # columns by single-vector matvecs (harness convention, SURVEY §8d)
+        B[:, j] = H.matvec(h2, X_true[:, j]) if lo <= j < hi or world == 1 else 0.0
+    w = hi - lo
+    b_dev = torch.from_numpy(np.ascontiguousarray(B[:, lo:hi])).to(dev)
+    x_dev = torch.empty_like(b_dev)
+    stream = torch.cuda.ExternalStream(L.stream_handle(), device=dev)
+    import ctypes as C
+
+    lib = L.lib()
+    parts = [torch.empty((n, max(h - l for l, h in column_ranges(q, world))), dtype=torch.float64, device=dev)
+             for _ in range(world)]
+
+    def step():
+        L.check(lib.h2f_solve_dev(fac.handle.ptr, C.c_void_p(b_dev.data_ptr()), C.c_void_p(x_dev.data_ptr()), w),
+                "h2f_solve_dev")
+        if dist:
+            send = parts[rank]
+            send[:, :w].copy_(x_dev)
+            dist.all_gather(parts, send.clone())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = L.kernel_launches()
+    clocks = ClockSampler(local)
+    times = []
+    if dist:
+        dist.barrier()
+    clocks.start()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(torch.cuda.current_stream() if dist else stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    clk = clocks.stop()
+    launches = (L.kernel_launches() - launches0) / args.steps
+    t_step = max_over_ranks(float(np.mean(times)), dist, dev)
+    # e2e through the public API: host B in, host X out (every rank)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    X = solve_multi_sharded(fac, B)
+    t_e2e = max_over_ranks(time.perf_counter() - t0, dist, dev)
+    cols = [j for j in range(q) if lo <= j < hi][:4]
+    e_b = max(float(np.linalg.norm(H.matvec(h2, X[:, j]) - B[:, j]) / np.linalg.norm(B[:, j])) for j in cols)
+    e_b = max_over_ranks(e_b, dist, dev)
+    line = {
+        "metric": f"H2 {q}-RHS solve time, factor reused (s)", "value": t_step, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "n": n, "nrhs": q, "problem": cfg["problem"], **cfg["over"],
+                   "parallelism": f"column shards x{world}", "l2": "flushed between timed steps (256 MB write)"},
+        "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": int(w * n * 8),
+                "d2h_bytes_per_step": int(n * q * 8)},
+        "gpu_launches": int(round(launches)), "clocks": clk, "backward_error_max_sampled": e_b,
+        "factor_bytes": fac.nbytes(), "input_build_s": t_build,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def h2_bytes(h2):
     return sum(b.nbytes for s in (h2.leaf_basis, h2.transfer, h2.coupling, h2.dense) for b in s.values())
 
@@ -352,6 +448,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif "nrhs" in cfg:
+        run_multi_rhs(args, cfg)
     else:
         run_b200(args, cfg)
 

@@ -1,6 +1,8 @@
 // Host-side builders of the batched task lists (GEMM, copy) shared by the
 // factorization driver and the dense per-cluster orchestration.
 #pragma once
+#include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "kernels.h"
@@ -12,6 +14,7 @@ struct GemmBuild {
     std::vector<GemmTask> tasks;
     std::vector<GemmContrib> contribs;
     std::vector<int64_t> tile_start{0};
+    std::vector<int64_t> tile_cost;  // per task: K chunks per tile + epilogue weight
     int64_t norm_tiles = 0;
     double flops = 0, bytes = 0;  // algorithmic work of the launch (profiler)
 
@@ -31,7 +34,9 @@ struct GemmBuild {
             if (cs[i].alpha != cs[0].alpha) throw Error(H2F_E_INTERNAL, "assertion: mixed alpha in one GEMM task");
         contribs.insert(contribs.end(), cs, cs + nc);
         t.contrib_end = int64_t(contribs.size());
+        int64_t chunks = mode == GEMM_ADD ? 2 : 1;
         for (size_t i = 0; i < nc; ++i) {
+            if (cs[i].K > 0) chunks += cdiv(cs[i].K, GEMM_BK);
             flops += 2.0 * M * N * cs[i].K;
             bytes += 8.0 * (double(M) * cs[i].K + double(cs[i].K) * N);
         }
@@ -44,20 +49,46 @@ struct GemmBuild {
         }
         tasks.push_back(t);
         tile_start.push_back(tile_start.back() + nt);
+        tile_cost.push_back(chunks);
         return t.norm_base;
     }
     int64_t add1(double* C, int64_t ldc, int M, int N, int mode, const GemmContrib& c) {
         return add(C, ldc, M, N, mode, &c, 1);
     }
+    // per-CTA tile ranges with equal shares of the total chunk cost
+    std::vector<int64_t> cta_ranges() const {
+        const int64_t ntiles = tile_start.back();
+        const int G = gemm_grid(ntiles);
+        std::vector<int64_t> cta(size_t(G) + 1, ntiles);
+        cta[0] = 0;
+        double total = 0;
+        for (size_t t = 0; t < tasks.size(); ++t) total += double(tile_start[t + 1] - tile_start[t]) * tile_cost[t];
+        double acc = 0;
+        int b = 1;
+        for (size_t t = 0; t < tasks.size() && b < G; ++t) {
+            const int64_t nt = tile_start[t + 1] - tile_start[t];
+            const double c = double(tile_cost[t]), end = acc + double(nt) * c;
+            while (b < G && total * b / G <= end) {
+                int64_t off = int64_t(std::ceil((total * b / G - acc) / c));
+                off = std::min<int64_t>(std::max<int64_t>(off, 0), nt);
+                cta[b] = std::max(cta[b - 1], tile_start[t] + off);
+                ++b;
+            }
+            acc = end;
+        }
+        return cta;
+    }
     void launch(int kid, double* norms = nullptr, double bytes_override = -1.0) {
         if (tasks.empty()) return;
         Context& X = ctx();
+        const int64_t ntiles = tile_start.back();
         auto* dt = X.up.put(tasks);
         auto* dc = X.up.put(contribs);
         auto* ds = X.up.put(tile_start);
+        const int64_t* dcta = ntiles > gemm_grid(ntiles) ? X.up.put(cta_ranges()) : nullptr;
         X.up.flush(X.stream);
-        ProfScope ps(kid, flops, bytes_override >= 0 ? bytes_override : bytes, double(tile_start.back()));
-        launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), tile_start.back(), norms, X.stream);
+        ProfScope ps(kid, flops, bytes_override >= 0 ? bytes_override : bytes, double(ntiles));
+        launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), ntiles, dcta, norms, X.stream);
     }
 };
 

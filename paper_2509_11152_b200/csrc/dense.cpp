@@ -185,6 +185,25 @@ void hh_apply_q(const std::vector<HhJob>& jobs, const std::vector<HhApply>& xs, 
     }
 }
 
+void reorth_batched(const std::vector<ReorthTask>& tasks, Region& scr) {
+    GemmBuild g1, g2;
+    std::vector<RowNormTask> rows;
+    for (auto& t : tasks) {
+        const int s = t.s, k = t.k, kp = t.kept;
+        double* U = t.BT + int64_t(k) * s;  // kept x s, the rows to orthogonalise
+        if (k > 0) {
+            double* Cm = scr.alloc_n<double>(int64_t(k) * kp);
+            // C (k x kp) = V^T U^T ;  U -= C^T V^T
+            g1.add1(Cm, kp, k, kp, GEMM_STORE, contrib(t.V, t.ldv, 1, U, s, 1, s));
+            g2.add1(U, s, kp, s, GEMM_ADD, contrib(Cm, kp, 1, t.V, t.ldv, 1, k, -1.0));
+        }
+        for (int j = 0; j < kp; ++j) rows.push_back(RowNormTask{U + int64_t(j) * s, s, 0});
+    }
+    g1.launch(-1);
+    g2.launch(-1);
+    launch_normalize_rows(upload(rows), int32_t(rows.size()), ctx().stream);
+}
+
 void qr_r_blocked(const std::vector<QrTask>& tasks, Region& scr) {
     std::vector<HhJob> jobs;
     std::vector<RExtractTask> ex;

@@ -43,6 +43,10 @@ void complement_blocked(const std::vector<ComplementTask>& tasks, Region& scr);
 void jacobi_multi_cta(const std::vector<SvdTask>& tasks, double thresh, Region& scr, bool pairwise = false,
                       std::vector<int32_t*>* flags_out = nullptr);
 
+// factorization.py:82-84 for a batch: the kept rows u of BT (rows k..k+kept)
+// get u -= V (V^T u) (two batched DMMA GEMMs) and u /= |u|
+void reorth_batched(const std::vector<ReorthTask>& tasks, Region& scr);
+
 // partial-pivot LU of the n x n row-major A in place (LAPACK getrf pivots,
 // 0-based): cooperative panels + DMMA trailing updates.  red[0] = max|A|
 // before, red[1] = min|diag(U)| after (device; the vanishing-pivot test).

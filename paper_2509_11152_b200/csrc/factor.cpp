@@ -480,7 +480,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         }
         {
             ProfScope ps(K_COMPLEMENT, rf + cf, cb);
-            if (!ro.empty()) launch_reorth(upload(ro), int32_t(ro.size()), st);
+            if (!ro.empty()) reorth_batched(ro, scr);
             if (!cmp.empty()) complement(cmp, scr);
         }
     }

@@ -244,6 +244,18 @@ __global__ void __launch_bounds__(DT) reorth_kernel(const ReorthTask* __restrict
     }
 }
 
+// u /= |u| per row, warp per row, fixed lane-strided summation order
+__global__ void __launch_bounds__(256) normalize_rows_kernel(const RowNormTask* __restrict__ tasks, int nrows) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= nrows) return;
+    const RowNormTask T = tasks[w];
+    double a = 0.0;
+    for (int i = lane; i < T.len; i += 32) a += T.p[i] * T.p[i];
+    a = warp_sum(a);
+    const double inv = 1.0 / sqrt(a);
+    for (int i = lane; i < T.len; i += 32) T.p[i] *= inv;
+}
+
 __global__ void __launch_bounds__(DT) complement_kernel(const ComplementTask* __restrict__ tasks) {
     const ComplementTask T = tasks[blockIdx.x];
     extern __shared__ double taus[];  // [s]
@@ -962,6 +974,12 @@ void launch_jacobi_smem(const SvdTask* d_tasks, int32_t ntasks, int32_t max_n, d
 void launch_reorth(const ReorthTask* d_tasks, int32_t ntasks, cudaStream_t st) {
     if (ntasks <= 0) return;
     reorth_kernel<<<ntasks, DT, 0, st>>>(d_tasks);
+    count_launch();
+}
+
+void launch_normalize_rows(const RowNormTask* d_tasks, int32_t nrows, cudaStream_t st) {
+    if (nrows <= 0) return;
+    normalize_rows_kernel<<<(nrows + 7) / 8, 256, 0, st>>>(d_tasks, nrows);
     count_launch();
 }
 

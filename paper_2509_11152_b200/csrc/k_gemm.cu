@@ -28,74 +28,122 @@ constexpr int GEMM_THREADS = 128;
 // contributions of a tile (no pipeline restart between contributions); the
 // operands are staged in their stored orientation with conflict-free padded
 // strides, alpha (uniform per task) is applied in the epilogue.
-constexpr int BK2 = 32, STAGES = 3;
+constexpr int BK2 = GEMM_BK, STAGES = 3;
 constexpr int LDK2 = BK2 + 4;   // [m][k] / [n][k] layouts (k contiguous)
 constexpr int LDM2 = BM + 4;    // [k][m] / [k][n] layouts
 constexpr int STAGE_ELEMS = (BM * LDK2 > BK2 * LDM2 ? BM * LDK2 : BK2 * LDM2);
 constexpr size_t GEMM2_SMEM = sizeof(double) * 2 * STAGES * STAGE_ELEMS;
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+// cp.async with zero fill: copies `bytes` (0, 8 or 16) of src and zero-fills
+// the rest of the CP-byte destination
+template <int CP>
+__device__ __forceinline__ void cp_async(double* dst, const double* src, int bytes) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    const int sz = valid ? 8 : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(valid ? src : nullptr), "r"(sz));
+    if (CP == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N> __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// stage one BK2 chunk of contribution P (k offset k0) into As/Bs
-__device__ __forceinline__ void stage_chunk(const GemmContrib& P, int M, int N, int m0, int n0, int k0,
-                                            double* As, double* Bs) {
+// Stage one 64 x BK2 operand tile (rows = the M or N index, k = the
+// contraction index) into shared memory, in its stored orientation:
+//   KMAJOR = false: stored R x K (k contiguous) -> smem [r][k], stride LDK2
+//   KMAJOR = true:  stored K x R (r contiguous) -> smem [k][r], stride LDM2
+// Each thread owns a fixed column of the tile and walks rows with a constant
+// pointer stride, so the per-copy cost is one cp.async plus one add; VEC
+// moves 16-byte pairs when the operand is 16-byte aligned.  Out-of-range
+// elements are zero-filled (src-size 0/8), so tails contribute exact zeros.
+template <bool KMAJOR, bool VEC>
+__device__ __forceinline__ void stage_operand(const double* __restrict__ X, int64_t ld, int K, int R, int r0, int k0,
+                                              double* __restrict__ S) {
     const int tid = threadIdx.x;
+    if (!KMAJOR) {
+        constexpr int W = VEC ? 2 : 1;             // doubles per copy
+        constexpr int PER_ROW = BK2 / W;           // copies per tile row
+        constexpr int ROWS_STEP = GEMM_THREADS / PER_ROW;
+        const int kc = (tid % PER_ROW) * W, rb = tid / PER_ROW;
+        const int kv = K - k0 - kc;                // valid k in this copy (<= 0: none)
+        const int bytes = kv >= W ? 8 * W : (kv > 0 ? 8 * kv : 0);
+        const int rmax = R - r0 - rb;
+        const double* src = X + (int64_t)(r0 + rb) * ld + k0 + kc;
+        double* dst = S + rb * LDK2 + kc;
+        const int64_t step = (int64_t)ROWS_STEP * ld;
 #pragma unroll
-    for (int i = 0; i < (BM * BK2) / GEMM_THREADS; ++i) {
-        const int e = tid + GEMM_THREADS * i;
-        if (P.transA) {  // stored K x M: [k][m]
-            const int k = e / BM, m = e % BM;
-            const bool v = (k0 + k < P.K) && (m0 + m < M);
-            cp_async8(As + k * LDM2 + m, P.A + (int64_t)(k0 + k) * P.lda + m0 + m, v);
-        } else {         // stored M x K: [m][k]
-            const int m = e / BK2, k = e % BK2;
-            const bool v = (k0 + k < P.K) && (m0 + m < M);
-            cp_async8(As + m * LDK2 + k, P.A + (int64_t)(m0 + m) * P.lda + k0 + k, v);
+        for (int i = 0; i < 64 / ROWS_STEP; ++i) {
+            cp_async<8 * W>(dst + i * ROWS_STEP * LDK2, src, i * ROWS_STEP < rmax ? bytes : 0);
+            src += step;
         }
-    }
+    } else {
+        constexpr int W = VEC ? 2 : 1;
+        constexpr int PER_K = 64 / W;               // copies per k row
+        constexpr int K_STEP = GEMM_THREADS / PER_K;
+        const int rc = (tid % PER_K) * W, kb = tid / PER_K;
+        const int rv = R - r0 - rc;
+        const int bytes = rv >= W ? 8 * W : (rv > 0 ? 8 * rv : 0);
+        const int kmax = K - k0 - kb;
+        const double* src = X + (int64_t)(k0 + kb) * ld + r0 + rc;
+        double* dst = S + kb * LDM2 + rc;
+        const int64_t step = (int64_t)K_STEP * ld;
 #pragma unroll
-    for (int i = 0; i < (BN * BK2) / GEMM_THREADS; ++i) {
-        const int e = tid + GEMM_THREADS * i;
-        if (P.transB) {  // stored N x K: [n][k]
-            const int n = e / BK2, k = e % BK2;
-            const bool v = (k0 + k < P.K) && (n0 + n < N);
-            cp_async8(Bs + n * LDK2 + k, P.B + (int64_t)(n0 + n) * P.ldb + k0 + k, v);
-        } else {         // stored K x N: [k][n]
-            const int k = e / BN, n = e % BN;
-            const bool v = (k0 + k < P.K) && (n0 + n < N);
-            cp_async8(Bs + k * LDM2 + n, P.B + (int64_t)(k0 + k) * P.ldb + n0 + n, v);
+        for (int i = 0; i < BK2 / K_STEP; ++i) {
+            cp_async<8 * W>(dst + i * K_STEP * LDM2, src, i * K_STEP < kmax ? bytes : 0);
+            src += step;
         }
     }
 }
 
+template <bool KMAJOR>
+__device__ __forceinline__ void stage_any(const double* X, int64_t ld, int K, int R, int r0, int k0, double* S) {
+    const bool vec = ((reinterpret_cast<uintptr_t>(X) | (uintptr_t)(ld * 8)) & 15) == 0;
+    if (vec) stage_operand<KMAJOR, true>(X, ld, K, R, r0, k0, S);
+    else stage_operand<KMAJOR, false>(X, ld, K, R, r0, k0, S);
+}
+
+// stage one BK2 chunk of contribution P (k offset k0) into As/Bs
+__device__ __forceinline__ void stage_chunk(const GemmContrib& P, int M, int N, int m0, int n0, int k0,
+                                            double* As, double* Bs) {
+    if (P.transA) stage_any<true>(P.A, P.lda, P.K, M, m0, k0, As);   // stored K x M: [k][m]
+    else stage_any<false>(P.A, P.lda, P.K, M, m0, k0, As);           // stored M x K: [m][k]
+    if (P.transB) stage_any<false>(P.B, P.ldb, P.K, N, n0, k0, Bs);  // stored N x K: [n][k]
+    else stage_any<true>(P.B, P.ldb, P.K, N, n0, k0, Bs);            // stored K x N: [k][n]
+}
+
+template <bool TA, bool TB>
+__device__ __forceinline__ void mma_kstep(const double* __restrict__ As, const double* __restrict__ Bs,
+                                          double (&acc)[4][4][2], int wm, int wn, int g, int t, int kk) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int m = wm * 32 + i * 8 + g;
+        a[i] = TA ? As[(kk + t) * LDM2 + m] : As[m * LDK2 + kk + t];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int n = wn * 32 + j * 8 + g;
+        b[j] = TB ? Bs[n * LDK2 + kk + t] : Bs[(kk + t) * LDM2 + n];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+}
+
+// kvalid: k steps of the chunk that carry data (the last chunk of a
+// contribution is zero-filled past K; its zero steps are skipped).  Full
+// chunks take the straight-line path so the fragment loads of step k+1
+// overlap the DMMAs of step k.
 template <bool TA, bool TB>
 __device__ __forceinline__ void mma_chunk(const double* __restrict__ As, const double* __restrict__ Bs,
-                                          double (&acc)[4][4][2], int wm, int wn, int g, int t) {
+                                          double (&acc)[4][4][2], int wm, int wn, int g, int t, int kvalid) {
+    if (kvalid >= BK2) {
 #pragma unroll
-    for (int kk = 0; kk < BK2; kk += 4) {
-        double a[4], b[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int m = wm * 32 + i * 8 + g;
-            a[i] = TA ? As[(kk + t) * LDM2 + m] : As[m * LDK2 + kk + t];
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int n = wn * 32 + j * 8 + g;
-            b[j] = TB ? Bs[n * LDK2 + kk + t] : Bs[(kk + t) * LDM2 + n];
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int kk = 0; kk < BK2; kk += 4) mma_kstep<TA, TB>(As, Bs, acc, wm, wn, g, t, kk);
+    } else {
+        for (int kk = 0; kk < kvalid; kk += 4) mma_kstep<TA, TB>(As, Bs, acc, wm, wn, g, t, kk);
     }
 }
 
@@ -110,14 +158,14 @@ struct ChunkMeta {
     int ti;       // task
     int m0, n0;
     int last;     // last chunk of its tile: run the epilogue after it
-    int pad_;
+    int k0;       // k offset of the chunk within its contribution
     int64_t local;  // tile index within the task
 };
 
 __global__ void __launch_bounds__(GEMM_THREADS, 2)
 gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restrict__ contribs,
                   const int64_t* __restrict__ tile_start, int ntasks, int64_t ntiles,
-                  double* __restrict__ norms) {
+                  const int64_t* __restrict__ cta_tiles, double* __restrict__ norms) {
     extern __shared__ __align__(16) double gsm[];
     __shared__ double red[GEMM_THREADS / 32];
     __shared__ ChunkMeta meta[STAGES];
@@ -126,8 +174,17 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
     const int g = lane >> 2, t = lane & 3;
     const int wm = warp >> 1, wn = warp & 1;
 
-    const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
-    const int64_t t_begin = (int64_t)blockIdx.x * per, t_end = min(ntiles, t_begin + per);
+    // tile range of this CTA: host cost-balanced boundaries (tiles differ in
+    // their number of K chunks by orders of magnitude), else an even split
+    int64_t t_begin, t_end;
+    if (cta_tiles) {
+        t_begin = cta_tiles[blockIdx.x];
+        t_end = cta_tiles[blockIdx.x + 1];
+    } else {
+        const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+        t_begin = (int64_t)blockIdx.x * per;
+        t_end = min(ntiles, t_begin + per);
+    }
     if (t_begin >= t_end) return;
 
     // ---- producer cursor (uniform across the CTA) ----
@@ -168,6 +225,7 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
             double* As = gsm + (2 * stage) * STAGE_ELEMS;
             stage_chunk(P, p_M, p_N, p_m0, p_n0, p_pk, As, As + STAGE_ELEMS);
             m.contrib = (int)p_pc;
+            m.k0 = p_pk;
             m.ti = p_ti;
             m.m0 = p_m0;
             m.n0 = p_n0;
@@ -207,12 +265,13 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
             const GemmContrib P = contribs[m.contrib];
             const double* As = gsm + (2 * cur) * STAGE_ELEMS;
             const double* Bs = As + STAGE_ELEMS;
-            // zero-filled tails add exact zeros: no k bound inside the chunk
+            // k steps past the contribution's K hold zeros: skip them
+            const int kv = P.K - m.k0;
             switch (P.transA * 2 + P.transB) {
-            case 0: mma_chunk<false, false>(As, Bs, acc, wm, wn, g, t); break;
-            case 1: mma_chunk<false, true>(As, Bs, acc, wm, wn, g, t); break;
-            case 2: mma_chunk<true, false>(As, Bs, acc, wm, wn, g, t); break;
-            default: mma_chunk<true, true>(As, Bs, acc, wm, wn, g, t); break;
+            case 0: mma_chunk<false, false>(As, Bs, acc, wm, wn, g, t, kv); break;
+            case 1: mma_chunk<false, true>(As, Bs, acc, wm, wn, g, t, kv); break;
+            case 2: mma_chunk<true, false>(As, Bs, acc, wm, wn, g, t, kv); break;
+            default: mma_chunk<true, true>(As, Bs, acc, wm, wn, g, t, kv); break;
             }
         }
         if (!m.last) continue;
@@ -361,17 +420,19 @@ int grid_for(int64_t ntiles, int per_sm) {
 
 }  // namespace
 
+int gemm_grid(int64_t ntiles) { return grid_for(ntiles, 2); }
+
 void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
                        const int64_t* d_tile_start, int32_t ntasks, int64_t ntiles,
-                       double* d_norms, cudaStream_t st) {
+                       const int64_t* d_cta_tiles, double* d_norms, cudaStream_t st) {
     if (ntiles <= 0) return;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(gemm_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM2_SMEM);
         configured = true;
     }
-    gemm_tasks_kernel<<<grid_for(ntiles, 2), GEMM_THREADS, GEMM2_SMEM, st>>>(d_tasks, d_contribs, d_tile_start,
-                                                                             ntasks, ntiles, d_norms);
+    gemm_tasks_kernel<<<gemm_grid(ntiles), GEMM_THREADS, GEMM2_SMEM, st>>>(d_tasks, d_contribs, d_tile_start,
+                                                                          ntasks, ntiles, d_cta_tiles, d_norms);
     count_launch();
 }
 

@@ -39,6 +39,7 @@ struct GemmContrib {
 };
 
 constexpr int GEMM_TILE = 64;
+constexpr int GEMM_BK = 32;   // K chunk of the GEMM pipeline
 
 // ---- batched copy / add / zero with optional transpose --------------------
 enum CopyMode : int32_t { COPY_SET = 0, COPY_ADD = 1, COPY_ZERO = 2 };
@@ -229,14 +230,23 @@ struct GemvContrib {
 };
 
 // ---- launchers (defined in the .cu files) ----------------------------------------
+// grid of launch_gemm_tasks for ntiles tiles (d_cta_tiles, when given, holds
+// gemm_grid(ntiles)+1 tile boundaries, one range per CTA)
+int gemm_grid(int64_t ntiles);
 void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
                        const int64_t* d_tile_start, int32_t ntasks, int64_t ntiles,
-                       double* d_norms, cudaStream_t st);
+                       const int64_t* d_cta_tiles, double* d_norms, cudaStream_t st);
 void launch_copy_tasks(const CopyTask* d_tasks, const int64_t* d_tile_start, int32_t ntasks,
                        int64_t ntiles, cudaStream_t st);
 void launch_qr_r_smem(const QrTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st);
 void launch_jacobi_smem(const SvdTask* d_tasks, int32_t ntasks, int32_t max_n, double thresh, cudaStream_t st);
 void launch_reorth(const ReorthTask* d_tasks, int32_t ntasks, cudaStream_t st);
+struct RowNormTask {      // row /= |row| (one warp per row)
+    double* p;
+    int32_t len;
+    int32_t pad_;
+};
+void launch_normalize_rows(const RowNormTask* d_tasks, int32_t nrows, cudaStream_t st);
 void launch_r_extract(const RExtractTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st);
 // block-cyclic multi-CTA Jacobi: JB-row blocks (jacobi_block_rows), 2 blocks per CTA
 int jacobi_block_rows(int n);

@@ -132,7 +132,7 @@ int main(int argc, char** argv) {
         for (int r = 0; r < reps; ++r) {
             CK(cudaMemcpy(dC, dC0, csz * cs.ntargets * 8, cudaMemcpyDeviceToDevice));
             cudaEventRecord(e0);
-            launch_gemm_tasks(dT, dCs, dS, int(tasks.size()), start.back(), nullptr, 0);
+            launch_gemm_tasks(dT, dCs, dS, int(tasks.size()), start.back(), nullptr, nullptr, 0);
             cudaEventRecord(e1);
             CK(cudaEventSynchronize(e1));
             float ms;

@@ -25,19 +25,7 @@ for vi, var in enumerate(variants):
     try:
         fac = H.factorize(h2, prm["eps_lu"])
     except Exception as e:
-        piv = []
-    for rec in fac.records:
-        worst = (np.inf, -1)
-        for c, f in rec.factors.items():
-            if f.r:
-                lu = f.lu
-                ratio = float(np.abs(np.diag(lu)).min() / max(np.abs(lu).max(), 1e-300))
-                worst = min(worst, (ratio, c))
-        piv.append([rec.level, worst[0], worst[1]])
-    if fac.top_size:
-        tl = fac.top_lu
-        piv.append(["top", float(np.abs(np.diag(tl)).min() / np.abs(tl).max()), -1])
-    print(json.dumps({"variant": var, "pivot_ratio_min": piv, "error": repr(e)}), flush=True); continue
+        print(json.dumps({"variant": var, "error": repr(e)}), flush=True); continue
     tf = time.perf_counter() - t0
     x0 = H.solve(fac, b)
     x = H.refined_solve(h2, fac, b, steps=1)
