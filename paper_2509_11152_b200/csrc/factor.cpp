@@ -629,6 +629,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 tt.r = r;
                 tt.W = int(e.W);
                 tt.col0 = int(c0);
+                tt.mode = TRSM_ELIMINATOR;
                 (nc == 32 ? trs32 : nc == 16 ? trs16 : trs).push_back(tt);
                 if (nc) max_r_dmma[nc == 32 ? 0 : 1] = std::max(max_r_dmma[nc == 32 ? 0 : 1], r);
             }

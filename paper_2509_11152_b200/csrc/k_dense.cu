@@ -779,14 +779,17 @@ __global__ void __launch_bounds__(256, 1) trsm_dmma_kernel(const TrsmTask* __res
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const double* LU = T.LU;
+    const int64_t ldl = T.ldlu ? T.ldlu : r;
+    const int mode = T.mode;
     if (threadIdx.x == 0) {
         for (int i = 0; i < r; ++i) perm[i] = i;
-        for (int k = 0; k < r; ++k) {
-            const int p = T.piv[k];
-            const int t0 = perm[k];
-            perm[k] = perm[p];
-            perm[p] = t0;
-        }
+        if ((mode & TRSM_LOWER) && T.piv)
+            for (int k = 0; k < r; ++k) {
+                const int p = T.piv[k];
+                const int t0 = perm[k];
+                perm[k] = perm[p];
+                perm[p] = t0;
+            }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < r4 * NC; e += 256) {
@@ -796,6 +799,7 @@ __global__ void __launch_bounds__(256, 1) trsm_dmma_kernel(const TrsmTask* __res
     __syncthreads();
     const int nblk = (r + 31) / 32;
     for (int dir = 0; dir < 2; ++dir) {  // 0: unit lower, forward; 1: upper, backward
+        if (!(mode & (dir == 0 ? TRSM_LOWER : TRSM_UPPER))) continue;
         for (int bb = 0; bb < nblk; ++bb) {
             const int blk = dir == 0 ? bb : nblk - 1 - bb;
             const int b0 = blk * 32, nb = min(32, r - b0);
@@ -809,7 +813,7 @@ __global__ void __launch_bounds__(256, 1) trsm_dmma_kernel(const TrsmTask* __res
                     for (int u = 0; u < TPW; ++u) {
                         const int tid_ = warp * TPW + u, ti = tid_ / TN, tj = tid_ % TN;
                         const int row = ti * 8 + g;
-                        const double a = (row < nb && k + t < k_hi) ? __ldg(LU + (int64_t)(b0 + row) * r + k + t) : 0.0;
+                        const double a = (row < nb && k + t < k_hi) ? __ldg(LU + (int64_t)(b0 + row) * ldl + k + t) : 0.0;
                         const double bv = X[(k + t) * NCP + tj * 8 + g];
                         dmma_8x8x4(c[u][0], c[u][1], a, bv);
                     }
@@ -827,7 +831,7 @@ __global__ void __launch_bounds__(256, 1) trsm_dmma_kernel(const TrsmTask* __res
             }
             for (int e = threadIdx.x; e < 32 * 32; e += 256) {
                 const int i = e >> 5, k = e & 31;
-                Lb[i][k] = (i < nb && k < nb) ? LU[(int64_t)(b0 + i) * r + b0 + k] : 0.0;
+                Lb[i][k] = (i < nb && k < nb) ? LU[(int64_t)(b0 + i) * ldl + b0 + k] : 0.0;
             }
             __syncthreads();
             if (threadIdx.x < NC) {
@@ -849,9 +853,10 @@ __global__ void __launch_bounds__(256, 1) trsm_dmma_kernel(const TrsmTask* __res
             __syncthreads();
         }
     }
+    const double sgn = (mode & TRSM_NEGATE) ? -1.0 : 1.0;
     for (int e = threadIdx.x; e < r * NC; e += 256) {
         const int i = e / NC, c = e % NC;
-        if (c < ncols) T.MW[(int64_t)i * T.ldw + T.col0 + c] = -X[i * NCP + c];
+        if (c < ncols) T.MW[(int64_t)i * T.ldw + T.col0 + c] = sgn * X[i * NCP + c];
     }
 }
 

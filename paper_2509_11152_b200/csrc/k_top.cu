@@ -308,6 +308,14 @@ void launch_top_perm(const int32_t* piv, int32_t n, int32_t* perm, cudaStream_t 
     count_launch();
 }
 
+void launch_permute_rows(const double* src, const int32_t* perm, int32_t n, int32_t nrhs, double* dst,
+                         cudaStream_t st) {
+    const int64_t tot = int64_t(n) * nrhs;
+    if (tot <= 0) return;
+    permute_rows_kernel<<<unsigned((tot + 255) / 256), 256, 0, st>>>(src, perm, n, nrhs, dst);
+    count_launch();
+}
+
 void launch_top_solve(const double* lu, const int32_t* perm, int32_t n, double* x, int32_t nrhs, double* tmp,
                       int32_t* sync, cudaStream_t st) {
     if (n <= 0) return;

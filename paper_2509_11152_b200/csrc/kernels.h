@@ -118,15 +118,23 @@ struct LuTask {          // partial-pivot LU of the r x r view of D_cc
     int32_t* status;     // device: cluster index that failed (first), else -1
 };
 
-struct TrsmTask {        // MW = -(U^-1 L^-1 P G) column block
+// TrsmTask.mode bits (trsm_dmma_kernel): which factors of LU = P^T L U to
+// apply to the column block, and the sign of the result
+constexpr int32_t TRSM_LOWER = 1;   // X = L^-1 P G (pivots, unit lower)
+constexpr int32_t TRSM_UPPER = 2;   // X = U^-1 X
+constexpr int32_t TRSM_NEGATE = 4;  // MW = -X
+constexpr int32_t TRSM_ELIMINATOR = TRSM_LOWER | TRSM_UPPER | TRSM_NEGATE;  // -W = -(LU)^-1 P G
+
+struct TrsmTask {        // MW = op((LU)^-1 P G) column block
     const double* LU;
     const int32_t* piv;
     const double* G;     // r x W row-major, ld
-    double* MW;          // r x W row-major, ld
+    double* MW;          // r x W row-major, ld (may alias G: the block is staged first)
     int64_t ldg, ldw;
     int32_t r, W;
     int32_t col0;        // first column of this CTA chunk
-    int32_t pad_;
+    int32_t mode;        // TRSM_* bits (trsm_dmma_kernel; trsm_kernel is TRSM_ELIMINATOR only)
+    int64_t ldlu;        // row stride of LU (0: r); piv == nullptr: no row interchanges
 };
 
 // ---- blocked Householder QR with a cooperative panel (k_hh.cu) ---------------------
@@ -315,6 +323,9 @@ void launch_scatter_rows(const double* src, const int64_t* idx, int64_t n, int32
 // dense top solve: x <- (LU)^-1 P x through tmp (n x nrhs); sync holds
 // 1 + ceil(n/64) ints; perm from launch_top_perm (k_top.cu)
 void launch_top_perm(const int32_t* piv, int32_t n, int32_t* perm, cudaStream_t st);
+// dst[i, :] = src[perm[i], :] for an n x nrhs row-major block
+void launch_permute_rows(const double* src, const int32_t* perm, int32_t n, int32_t nrhs, double* dst,
+                         cudaStream_t st);
 void launch_top_solve(const double* lu, const int32_t* perm, int32_t n, double* x, int32_t nrhs,
                       double* tmp, int32_t* sync, cudaStream_t st);
 

@@ -9,9 +9,92 @@
 #include <algorithm>
 #include <map>
 
+#include "builders.h"
 #include "factor.h"
 
 namespace h2f {
+
+// multi-RHS substitution on the DMMA tile GEMM from this many columns on
+// (below: the per-vector solve_tasks kernels)
+constexpr int SOLVE_GEMM_MIN_RHS = 4;
+
+namespace {
+
+template <class T> T* to_dev(Region& r, const std::vector<T>& v) {
+    T* d = r.alloc_n<T>(std::max<size_t>(v.size(), 1));
+    if (!v.empty())
+        H2F_CUDA(cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, ctx().stream));
+    return d;
+}
+
+// a GEMM / copy / TRSM task list uploaded once with the plan
+struct DevGemm {
+    GemmTask* t = nullptr;
+    GemmContrib* c = nullptr;
+    int64_t *ts = nullptr, *cta = nullptr;
+    int32_t nt = 0;
+    int64_t ntiles = 0;
+    double flops = 0, bytes = 0;
+    void build(Region& mem, const GemmBuild& g) {
+        if (g.tasks.empty()) return;
+        t = to_dev(mem, g.tasks);
+        c = to_dev(mem, g.contribs);
+        ts = to_dev(mem, g.tile_start);
+        ntiles = g.tile_start.back();
+        if (ntiles > gemm_grid(ntiles)) cta = to_dev(mem, g.cta_ranges());
+        nt = int32_t(g.tasks.size());
+        flops = g.flops;
+        bytes = g.bytes;
+    }
+    void launch(int kid, cudaStream_t st) const {
+        if (!nt) return;
+        ProfScope ps(kid, flops, bytes, double(ntiles));
+        launch_gemm_tasks(t, c, ts, nt, ntiles, cta, nullptr, st);
+    }
+};
+
+struct DevCopy {
+    CopyTask* t = nullptr;
+    int64_t* ts = nullptr;
+    int32_t nt = 0;
+    int64_t ntiles = 0;
+    double bytes = 0;
+    void build(Region& mem, const CopyBuild& c) {
+        if (c.tasks.empty()) return;
+        t = to_dev(mem, c.tasks);
+        ts = to_dev(mem, c.tile_start);
+        nt = int32_t(c.tasks.size());
+        ntiles = c.tile_start.back();
+        bytes = c.bytes;
+    }
+    void launch(int kid, cudaStream_t st) const {
+        if (!nt) return;
+        ProfScope ps(kid, 0.0, bytes);
+        launch_copy_tasks(t, ts, nt, ntiles, st);
+    }
+};
+
+struct DevTrsm {
+    TrsmTask* t[2] = {};  // 32- and 16-column variants
+    int32_t n[2] = {}, max_r[2] = {1, 1};
+    double flops = 0;
+    void build(Region& mem, const std::vector<TrsmTask> (&v)[2], const int (&mr)[2], double f) {
+        for (int i = 0; i < 2; ++i) {
+            n[i] = int32_t(v[i].size());
+            if (n[i]) t[i] = to_dev(mem, v[i]);
+            max_r[i] = mr[i];
+        }
+        flops = f;
+    }
+    void launch(int kid, cudaStream_t st) const {
+        if (!n[0] && !n[1]) return;
+        ProfScope ps(kid, flops, 0.0);
+        if (n[0]) launch_trsm_dmma(t[0], n[0], max_r[0], 32, st);
+        if (n[1]) launch_trsm_dmma(t[1], n[1], max_r[1], 16, st);
+    }
+};
+
+}  // namespace
 
 struct SolvePlan {
     struct Batch {
@@ -26,6 +109,13 @@ struct SolvePlan {
         SolveTask* tk[4] = {};
         int32_t ntk[4] = {};
         double fwd_flops = 0, fwd_bytes = 0, sc_bytes = 0;
+        // multi-RHS path (nrhs >= SOLVE_GEMM_MIN_RHS): forward = rotation
+        // GEMM, products GEMM, pivoted unit-lower TRSM, skeleton copy,
+        // scatter; backward = upper TRSM, gather GEMM, add, rotation GEMM, copy
+        bool gemm = false;
+        DevGemm f_rot, f_prod, b_gather, b_rot;
+        DevCopy f_copy, b_add, b_copy;
+        DevTrsm f_trsm, b_trsm;
     };
     struct Level {
         int64_t total = 0;
@@ -49,13 +139,6 @@ Factorization::~Factorization() = default;
 
 namespace {
 
-template <class T> T* to_dev(Region& r, const std::vector<T>& v) {
-    T* d = r.alloc_n<T>(std::max<size_t>(v.size(), 1));
-    if (!v.empty())
-        H2F_CUDA(cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, ctx().stream));
-    return d;
-}
-
 SolvePlan& get_plan(Factorization& f, int nrhs) {
     auto it = f.plans.find(nrhs);
     if (it != f.plans.end()) return *it->second;
@@ -63,6 +146,17 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
     SolvePlan& P = *plan;
     P.nrhs = nrhs;
     int64_t scratch_rows = 0, work_max = 0;
+    bool use_gemm = nrhs >= SOLVE_GEMM_MIN_RHS;
+    for (auto& rec : f.recs)
+        for (auto& cf : rec.factors)
+            if (cf.r > 0 && trsm_dmma_cols(cf.r) == 0) use_gemm = false;
+    const int q = nrhs;
+    struct HostBatch {
+        size_t level, batch;
+        std::vector<SolveCluster> cls;
+        std::vector<SolveEdge> edges;
+    };
+    std::vector<HostBatch> host_batches;
     for (auto& rec : f.recs) {
         SolvePlan::Level L;
         L.total = rec.total();
@@ -151,6 +245,8 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
                 bytes_b += 8.0 * (double(cf.s) * cf.s + double(cf.r) * cf.r + cf.r * ew) +
                            16.0 * (cf.s + ew) * nrhs;
             }
+            SolvePlan::Batch B;
+            if (use_gemm) host_batches.push_back({P.levels.size(), L.batches.size(), cls, edges});
             std::vector<ScatterGroup> gs;
             std::vector<int64_t> list;
             for (int64_t lo : group_order) {
@@ -163,7 +259,6 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
                 sg.end = int64_t(list.size());
                 gs.push_back(sg);
             }
-            SolvePlan::Batch B;
             B.ncl = int32_t(cls.size());
             B.cl = to_dev(P.mem, cls);
             B.edges = to_dev(P.mem, edges);
@@ -191,10 +286,130 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
     launch_top_perm(f.top_piv, int32_t(f.top_size), P.top_perm, ctx().stream);
     P.scratch = P.mem.alloc_n<double>(std::max<int64_t>(scratch_rows, 1) * nrhs);
     P.work = P.mem.alloc_n<double>(std::max<int64_t>(work_max, 1));
+    for (auto& hb : host_batches) {
+        SolvePlan::Batch& B = P.levels[hb.level].batches[hb.batch];
+        double* yv = P.yv[hb.level];
+        GemmBuild frot, fprod, bgat, brot;
+        CopyBuild fcopy, badd, bcopy;
+        std::vector<TrsmTask> ft[2], bt[2];
+        int mr[2] = {1, 1};
+        double tf = 0;
+        int64_t wo = 0;
+        for (auto& sc : hb.cls) {
+            const int s_ = sc.s, r_ = sc.r;
+            double* yc = yv + sc.off * q;
+            double* wk = P.work + wo;
+            double* acc = wk + int64_t(s_) * q;
+            wo += (int64_t(s_) + r_) * q;
+            // forward (solve.py:90-128): wk = Q~^T y_c
+            frot.add1(wk, q, s_, q, GEMM_STORE, contrib(sc.q, s_, 1, yc, q, 0, s_));
+            // skeleton rows pass through; redundant rows are solved below
+            fcopy.add(yc + int64_t(r_) * q, q, s_ - r_, q, wk + int64_t(r_) * q, q, 0, COPY_SET);
+            // backward (solve.py:131-164): y_c = Q~ y_c (after the TRSM and the gather-add)
+            brot.add1(wk, q, s_, q, GEMM_STORE, contrib(sc.q, s_, 0, yc, q, 0, s_));
+            bcopy.add(yc, q, s_, q, wk, q, 0, COPY_SET);
+            if (r_ == 0) continue;
+            // products (W x q) = (-W)^T y_R into the scatter scratch
+            fprod.add1(P.scratch + sc.soff * q, q, int(sc.W), q, GEMM_STORE, contrib(sc.mw, sc.W, 1, wk, q, 0, r_));
+            const int nc = trsm_dmma_cols(r_), vi = nc == 32 ? 0 : 1;
+            mr[vi] = std::max(mr[vi], r_);
+            tf += double(r_) * r_ * q;
+            for (int c0 = 0; c0 < q; c0 += nc) {
+                TrsmTask t{};
+                t.LU = sc.lu;
+                t.piv = sc.piv;
+                t.r = r_;
+                t.W = q;
+                t.col0 = c0;
+                t.ldg = t.ldw = q;
+                t.G = wk;
+                t.MW = yc;
+                t.mode = TRSM_LOWER;
+                ft[vi].push_back(t);
+                t.G = yc;
+                t.mode = TRSM_UPPER;
+                bt[vi].push_back(t);
+            }
+            // gather: acc = sum_e (-W_e) y[span_e], in edge order
+            std::vector<GemmContrib> cs;
+            for (int64_t e = sc.edge_begin; e < sc.edge_end; ++e) {
+                const SolveEdge& E = hb.edges[e];
+                cs.push_back(contrib(E.mat, E.ld, 0, yv + E.lo * q, q, 0, E.w));
+            }
+            bgat.add(acc, q, r_, q, GEMM_STORE, cs.data(), cs.size());
+            badd.add(yc, q, r_, q, acc, q, 0, COPY_ADD);
+        }
+        B.f_rot.build(P.mem, frot);
+        B.f_prod.build(P.mem, fprod);
+        B.f_copy.build(P.mem, fcopy);
+        B.f_trsm.build(P.mem, ft, mr, tf);
+        B.b_trsm.build(P.mem, bt, mr, tf);
+        B.b_gather.build(P.mem, bgat);
+        B.b_add.build(P.mem, badd);
+        B.b_rot.build(P.mem, brot);
+        B.b_copy.build(P.mem, bcopy);
+        B.gemm = true;
+    }
     ctx().sync();
     auto& ref = *plan;
     f.plans[nrhs] = std::move(plan);
     return ref;
+}
+
+}  // namespace
+
+namespace {
+
+// Dense top solve (solve.py:46-55) for a block of right-hand sides: row
+// permutation, then blocked forward/backward substitution in 64-row steps --
+// the diagonal block by the DMMA TRSM kernel, the rest of the column by one
+// DMMA tile GEMM per step -- so the top LU is streamed twice per solve
+// instead of once per right-hand side.
+void top_solve_blocked(Factorization& f, SolvePlan& P, cudaStream_t st) {
+    const int64_t n = f.top_size;
+    const int q = P.nrhs;
+    if (n == 0) return;
+    constexpr int NB = 64;
+    launch_permute_rows(P.ytop, P.top_perm, int32_t(n), q, P.ttop, st);
+    const int nc = trsm_dmma_cols(NB);
+    auto diag = [&](int64_t k0, int nb, int mode) {
+        std::vector<TrsmTask> ts;
+        for (int c0 = 0; c0 < q; c0 += nc) {
+            TrsmTask t{};
+            t.LU = f.top_lu + k0 * n + k0;
+            t.ldlu = n;
+            t.piv = nullptr;
+            t.G = P.ttop + k0 * q;
+            t.MW = P.ttop + k0 * q;
+            t.ldg = t.ldw = q;
+            t.r = nb;
+            t.W = q;
+            t.col0 = c0;
+            t.mode = mode;
+            ts.push_back(t);
+        }
+        launch_trsm_dmma(upload(ts), int32_t(ts.size()), nb, nc, st);
+    };
+    for (int64_t k0 = 0; k0 < n; k0 += NB) {  // L y = P b
+        const int nb = int(std::min<int64_t>(NB, n - k0));
+        diag(k0, nb, TRSM_LOWER);
+        const int64_t rest = n - k0 - nb;
+        if (rest <= 0) continue;
+        GemmBuild g;
+        g.add1(P.ttop + (k0 + nb) * q, q, int(rest), q, GEMM_ADD,
+               contrib(f.top_lu + (k0 + nb) * n + k0, n, 0, P.ttop + k0 * q, q, 0, nb, -1.0));
+        g.launch(-1);
+    }
+    for (int64_t k0 = ((n - 1) / NB) * NB; k0 >= 0; k0 -= NB) {  // U x = y
+        const int nb = int(std::min<int64_t>(NB, n - k0));
+        diag(k0, nb, TRSM_UPPER);
+        if (k0 == 0) continue;
+        GemmBuild g;
+        g.add1(P.ttop, q, int(k0), q, GEMM_ADD,
+               contrib(f.top_lu + k0, n, 0, P.ttop + k0 * q, q, 0, nb, -1.0));
+        g.launch(-1);
+    }
+    H2F_CUDA(cudaMemcpyAsync(P.ytop, P.ttop, sizeof(double) * n * q, cudaMemcpyDeviceToDevice, st));
 }
 
 }  // namespace
@@ -215,6 +430,15 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
     for (size_t li = 0; li < R; ++li) {
         auto& L = P.levels[li];
         for (auto& B : L.batches) {
+            if (B.gemm) {
+                B.f_rot.launch(K_SOLVE_FWD, st);
+                B.f_prod.launch(K_SOLVE_FWD, st);
+                B.f_trsm.launch(K_SOLVE_FWD, st);
+                B.f_copy.launch(K_SOLVE_FWD, st);
+                ProfScope ps(K_SOLVE_SCATTER, 0.0, B.sc_bytes);
+                launch_fwd_scatter(B.groups, B.ngroups, B.list, P.scratch, P.yv[li], nrhs, st);
+                continue;
+            }
             {
                 ProfScope ps(K_SOLVE_FWD, B.fwd_flops, B.fwd_bytes);
                 launch_solve_tasks(B.tk[0], B.ntk[0], B.cl, B.edges, P.yv[li], P.scratch, P.work, nrhs, st);
@@ -229,7 +453,8 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
     {
         const double nt = double(f.top_size);
         ProfScope ps(K_SOLVE_TOP, 2.0 * nt * nt * nrhs, 8.0 * nt * nt);
-        launch_top_solve(f.top_lu, P.top_perm, int(f.top_size), P.ytop, nrhs, P.ttop, P.top_sync, st);
+        if (nrhs >= SOLVE_GEMM_MIN_RHS) top_solve_blocked(f, P, st);
+        else launch_top_solve(f.top_lu, P.top_perm, int(f.top_size), P.ytop, nrhs, P.ttop, P.top_sync, st);
     }
     for (size_t li = R; li-- > 0;) {
         auto& L = P.levels[li];
@@ -237,6 +462,14 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
         launch_scatter_rows(src, L.up, L.up_n, nrhs, P.yv[li], st);
         for (size_t bi = L.batches.size(); bi-- > 0;) {
             auto& B = L.batches[bi];
+            if (B.gemm) {
+                B.b_trsm.launch(K_SOLVE_BWD, st);
+                B.b_gather.launch(K_SOLVE_BWD, st);
+                B.b_add.launch(K_SOLVE_BWD, st);
+                B.b_rot.launch(K_SOLVE_BWD, st);
+                B.b_copy.launch(K_SOLVE_BWD, st);
+                continue;
+            }
             ProfScope ps(K_SOLVE_BWD, B.fwd_flops, B.fwd_bytes);
             launch_solve_tasks(B.tk[2], B.ntk[2], B.cl, B.edges, P.yv[li], P.scratch, P.work, nrhs, st);
             launch_solve_tasks(B.tk[3], B.ntk[3], B.cl, B.edges, P.yv[li], P.scratch, P.work, nrhs, st);

@@ -266,3 +266,21 @@ def test_solve_multi_sharded_single_rank():
     for j in [0, 6]:
         one = H.solve(fac, B[:, j])
         assert np.linalg.norm(X[:, j] - one) <= 1e-12 * np.linalg.norm(one)
+
+
+@pytest.mark.parametrize("case,q", [("cov2d_4096", 16), ("laplace3d_4096", 40)])
+def test_solve_multi_block_path_matches_single_vector_path(case, q):
+    """nrhs >= 4 runs the block substitution (DMMA GEMM rotations/products/
+    gathers, DMMA TRSM, blocked top solve); every column must agree with the
+    single-vector kernels and with the oracle's substitution."""
+    h2, prm, fac = gpu_factor(case)
+    B = np.random.default_rng(5).standard_normal((fac.n, q))
+    X = H.solve_multi(fac, B)
+    for j in [0, q // 2, q - 1]:
+        one = H.solve(fac, B[:, j])
+        assert np.linalg.norm(X[:, j] - one) <= 1e-11 * np.linalg.norm(one)
+    with one_thread():
+        of = O.factorize(h2, prm["eps_lu"])
+        Xo = O.substitute(of, B[:, :3])
+    if case.startswith("cov2d"):
+        assert np.linalg.norm(X[:, :3] - Xo) <= 1e-8 * np.linalg.norm(Xo)
