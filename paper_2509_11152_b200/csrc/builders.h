@@ -52,6 +52,36 @@ struct GemmBuild {
         tile_cost.push_back(chunks);
         return t.norm_base;
     }
+    // task whose `nc` contributions already sit at [begin, begin+nc) of an
+    // external (pinned-uploaded) contribution array `ext`; kflops = sum of K,
+    // chunks = sum of ceil(K / GEMM_BK), alpha uniform (the caller's duty)
+    const GemmContrib* ext = nullptr;
+    int64_t add_ext(double* C, int64_t ldc, int M, int N, int mode, int64_t begin, int64_t nc, double ksum,
+                    int64_t chunks) {
+        if (M <= 0 || N <= 0) return -1;
+        GemmTask t{};
+        t.C = C;
+        t.ldc = ldc;
+        t.M = M;
+        t.N = N;
+        t.mode = mode;
+        t.tiles_n = int(cdiv(N, GEMM_TILE));
+        t.contrib_begin = begin;
+        t.contrib_end = begin + nc;
+        flops += 2.0 * M * N * ksum;
+        bytes += 8.0 * ksum * (double(M) + N);
+        bytes += mode == GEMM_ADD ? 16.0 * M * N : (mode == GEMM_STORE ? 8.0 * M * N : 0.0);
+        t.norm_base = -1;
+        const int64_t nt = tiles(M, N);
+        if (mode == GEMM_NORM) {
+            t.norm_base = norm_tiles;
+            norm_tiles += nt;
+        }
+        tasks.push_back(t);
+        tile_start.push_back(tile_start.back() + nt);
+        tile_cost.push_back(chunks + (mode == GEMM_ADD ? 2 : 1));
+        return t.norm_base;
+    }
     int64_t add1(double* C, int64_t ldc, int M, int N, int mode, const GemmContrib& c) {
         return add(C, ldc, M, N, mode, &c, 1);
     }
@@ -83,7 +113,7 @@ struct GemmBuild {
         Context& X = ctx();
         const int64_t ntiles = tile_start.back();
         auto* dt = X.up.put(tasks);
-        auto* dc = X.up.put(contribs);
+        const GemmContrib* dc = ext ? ext : X.up.put(contribs);
         auto* ds = X.up.put(tile_start);
         const int64_t* dcta = ntiles > gemm_grid(ntiles) ? X.up.put(cta_ranges()) : nullptr;
         X.up.flush(X.stream);

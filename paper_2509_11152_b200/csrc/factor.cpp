@@ -198,12 +198,24 @@ class Factorizer {
     int batch_counter = 0;
     std::vector<size_t> level_marks;
     std::vector<int> mark_node;  // node-indexed batch membership stamp
+    std::vector<int> node_bi;    // node -> position in the current batch (valid where stamped)
     int stamp = 0;
     int target_stamp = 0;
     bool level_prof = false;
     FILE* aug_log = nullptr;  // H2F_AUG_LOG=path: per-cluster augmentation shapes (development aid)
     double level_prev[K_COUNT] = {};
     std::chrono::steady_clock::time_point level_t0;
+    // host wall time per section of process_batch (H2F_LEVEL_PROF); the two
+    // sync entries are the host blocked on the device
+    enum { HT_PICK, HT_AUG, HT_SYNC1, HT_AUG2, HT_PROJ, HT_ELIM, HT_SCHUR, HT_SYNC2, HT_CREATE, HT_TRANS, HT_N };
+    double ht[HT_N] = {};
+    std::chrono::steady_clock::time_point ht_last = std::chrono::steady_clock::now();
+    void tick(int i) {
+        if (!level_prof) return;
+        const auto now = std::chrono::steady_clock::now();
+        ht[i] += std::chrono::duration<double>(now - ht_last).count();
+        ht_last = now;
+    }
     void dump_level_profile(int level);
 
     std::unique_ptr<Lvl> leaf_level(int level);
@@ -288,11 +300,15 @@ void Factorizer::attach_couplings(Lvl& L) {
 void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     Context& X = ctx();
     cudaStream_t st = X.stream;
+    tick(HT_PICK);
     Region& scr = scratch[batch_counter++ & 1];
     scr.reset();
     const int nb = int(batch.size());
     ++stamp;
-    for (int c : batch) mark_node[c] = stamp;
+    for (int bi = 0; bi < nb; ++bi) {
+        mark_node[batch[bi]] = stamp;
+        node_bi[batch[bi]] = bi;
+    }
     auto in_batch = [&](int c) { return mark_node[c] == stamp; };
 
     // ------------------------------------------------------------- augment
@@ -324,6 +340,9 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         // the shared-memory TSQR serves n <= hh_min_n; above, the blocked
         // Householder with cooperative panels (dense.cpp)
         const int hh_min_n = std::min(small_n_max, env_int("H2F_HH_MIN_N", 32));
+        // one-CTA shared-memory Jacobi up to this n; above, the block-cyclic
+        // multi-CTA Jacobi (n/16 CTAs per cluster) finishes a batch sooner
+        const int svd_smem_max = std::min(small_n_max, env_int("H2F_SVD_SMEM_MAX", 64));
         H2F_CUDA(cudaMemsetAsync(kept_d, 0, sizeof(int) * nb, st));
         for (int bi = 0; bi < nb; ++bi) {
             const int c = batch[bi], ci = L.at(c);
@@ -384,7 +403,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                     qr_small.push_back(QrTask{Z, R, wf, n, wf, 0, wf, 0});
                 }
             }
-            if (n <= small_n_max) {
+            if (n <= svd_smem_max) {
                 svd_small.push_back(sv);
                 max_n_small = std::max(max_n_small, n);
             } else {
@@ -443,7 +462,9 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     }
     int* kept_h = static_cast<int*>(X.pinned_buf(sizeof(int) * nb));
     H2F_CUDA(cudaMemcpyAsync(kept_h, kept_d, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
+    tick(HT_AUG);
     X.sync();
+    tick(HT_SYNC1);
     std::vector<int> kept(kept_h, kept_h + nb);
     if (aug_log) {
         for (int bi = 0; bi < nb; ++bi)
@@ -494,14 +515,17 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         // stored extent and every consumer treats the added rows as zeros
     }
 
+    tick(HT_AUG2);
     // ------------------------------------------------------------- project
     clock.mark(PH_PROJECT);
     {
-        std::set<std::pair<bool, Key>> items;  // (is_fill, key), dense first like the reference
+        std::vector<std::pair<bool, Key>> items;  // (is_fill, key), dense first like the reference
         for (int c : batch) {
-            items.insert({false, mkkey(c, c)});
-            for (auto& kv : L.touch[L.at(c)]) items.insert({!kv.second.dense, kv.second.key});
+            items.push_back({false, mkkey(c, c)});
+            for (auto& kv : L.touch[L.at(c)]) items.push_back({!kv.second.dense, kv.second.key});
         }
+        std::sort(items.begin(), items.end());
+        items.erase(std::unique(items.begin(), items.end()), items.end());
         GemmBuild p1, p2;
         for (auto& it : items) {
             View& B = L.block(it.second, !it.first);
@@ -511,17 +535,17 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             if (ra && rb) {
                 double* tmp = scr.alloc_n<double>(int64_t(B.rows) * B.cols);
                 const int sa = B.rows, sb = B.cols;
-                double* qa = Q[std::find(batch.begin(), batch.end(), a) - batch.begin()];
-                double* qb = Q[std::find(batch.begin(), batch.end(), b) - batch.begin()];
+                double* qa = Q[node_bi[a]];
+                double* qb = Q[node_bi[b]];
                 p1.add1(tmp, B.cols, B.rows, B.cols, GEMM_STORE, contrib(qa, sa, 1, B.p, B.ld, 0, sa));
                 p2.add1(out, B.cols, B.rows, B.cols, GEMM_STORE, contrib(tmp, B.cols, 0, qb, sb, 0, sb));
             } else if (ra) {
                 const int sa = B.rows;
-                double* qa = Q[std::find(batch.begin(), batch.end(), a) - batch.begin()];
+                double* qa = Q[node_bi[a]];
                 p1.add1(out, B.cols, B.rows, B.cols, GEMM_STORE, contrib(qa, sa, 1, B.p, B.ld, 0, sa));
             } else if (rb) {
                 const int sb = B.cols;
-                double* qb = Q[std::find(batch.begin(), batch.end(), b) - batch.begin()];
+                double* qb = Q[node_bi[b]];
                 p1.add1(out, B.cols, B.rows, B.cols, GEMM_STORE, contrib(B.p, B.ld, 0, qb, sb, 0, sb));
             } else {
                 throw Error(H2F_E_INTERNAL, "assertion: projected block touches no batch member");
@@ -532,6 +556,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         p2.launch(K_GEMM_PROJECT);
     }
 
+    tick(HT_PROJ);
     // ------------------------------------------------------------- eliminate
     clock.mark(PH_PARTIAL_LU);
     struct Elim {
@@ -669,6 +694,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         }
     }
 
+    tick(HT_ELIM);
     // Schur updates (factorization.py:122-126) fused with the scatter into the
     // target blocks (factorization.py:476-505).  (target, contribution) pairs
     // are collected in reference order and grouped per target by a stable
@@ -679,6 +705,11 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         int M, N;
         int64_t count;
     };
+    // one (target, contribution) pair in compact form: elimination e, panel
+    // pair (i, j); swap = the transposed (0, j) form -W_j^T g_0
+    struct TCon {
+        int32_t t, e, i, j;  // j < 0: swap, panel -j-1
+    };
     struct Cand {
         Key key;
         int M, N;
@@ -686,7 +717,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         int64_t base, ntiles;
     };
     std::vector<THdr> thdr;
-    std::vector<std::pair<int, GemmContrib>> tcon;
+    std::vector<TCon> tcon;
     std::vector<Cand> cands;
     {
         size_t guess = 0;
@@ -695,7 +726,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     }
     const int tstamp = ++target_stamp;
     // every target is a (sub)block of one View; the view carries its slot
-    auto add_target = [&](View& Vw, double* C, int64_t ldc, int Mr, int Nc, const GemmContrib& g) {
+    auto add_target = [&](View& Vw, double* C, int64_t ldc, int Mr, int Nc, int32_t ei, int32_t i, int32_t j) {
         if (Mr <= 0 || Nc <= 0) return;
         if (Vw.stamp != tstamp) {
             Vw.stamp = tstamp;
@@ -706,29 +737,24 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         if (t.C != C || t.M != Mr || t.N != Nc || t.ldc != ldc)
             throw Error(H2F_E_INTERNAL, "assertion: Schur target shape mismatch");
         ++t.count;
-        tcon.push_back({Vw.tidx, g});
+        tcon.push_back({Vw.tidx, ei, i, j});
     };
-    for (auto& e : el) {
+    for (size_t ei = 0; ei < el.size(); ++ei) {
+        auto& e = el[ei];
         const int c = e.c, r = e.r, kt = e.kt;
         std::vector<int> opos(e.np);
         for (int i = 1; i < e.np; ++i) opos[i] = L.at(e.ids[i]);
         std::vector<Nbrs::Item>::const_iterator walk{}, walk_end{};
         for (int i = 0; i < e.np; ++i)
             for (int j = i; j < e.np; ++j) {
-                const GemmContrib g = contrib(e.G + e.offs[i], e.W, 1, e.MW + e.offs[j], e.W, 0, r);
-                const int wi = e.widths[i], wj = e.widths[j];
                 if (i == 0 && j == 0) {
                     View& Dcc = L.dcc(e.ci);
-                    add_target(Dcc, Dcc.p + int64_t(r) * Dcc.ld + r, Dcc.ld, kt, kt, g);
+                    add_target(Dcc, Dcc.p + int64_t(r) * Dcc.ld + r, Dcc.ld, kt, kt, int32_t(ei), 0, 0);
                 } else if (i == 0) {
                     const Entry& en = e.ents[j - 1];
                     View* B = en.v;
-                    if (key_a(en.key) == c) {
-                        add_target(*B, B->p + int64_t(r) * B->ld, B->ld, kt, B->cols, g);
-                    } else {
-                        const GemmContrib gt = contrib(e.MW + e.offs[j], e.W, 1, e.G + e.offs[0], e.W, 0, r);
-                        add_target(*B, B->p + r, B->ld, B->rows, kt, gt);
-                    }
+                    if (key_a(en.key) == c) add_target(*B, B->p + int64_t(r) * B->ld, B->ld, kt, B->cols, int32_t(ei), 0, j);
+                    else add_target(*B, B->p + r, B->ld, B->rows, kt, int32_t(ei), 0, -j - 1);
                 } else {
                     View* B = nullptr;
                     if (i == j) {
@@ -741,15 +767,15 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                         if (walk != walk_end && walk->first == e.ids[j]) B = walk->second.v;
                     }
                     if (B) {
-                        add_target(*B, B->p, B->ld, B->rows, B->cols, g);
+                        add_target(*B, B->p, B->ld, B->rows, B->cols, int32_t(ei), i, j);
                     } else {
                         Cand cd;
                         cd.key = mkkey(e.ids[i], e.ids[j]);
-                        cd.M = wi;
-                        cd.N = wj;
-                        cd.g = g;
+                        cd.M = e.widths[i];
+                        cd.N = e.widths[j];
+                        cd.g = contrib(e.G + e.offs[i], e.W, 1, e.MW + e.offs[j], e.W, 0, r);
                         cd.base = 0;
-                        cd.ntiles = GemmBuild::tiles(wi, wj);
+                        cd.ntiles = GemmBuild::tiles(cd.M, cd.N);
                         cands.push_back(cd);
                     }
                 }
@@ -761,20 +787,37 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     double schur_bytes = 0;
     for (auto& e : el) schur_bytes += 16.0 * e.r * double(e.W);
     {
+        // contributions grouped per target (stable counting sort, reference
+        // order within a target) written straight into pinned upload memory
+        const size_t ncon = tcon.size() + cands.size();
+        GemmContrib* hc = nullptr;
+        sch.ext = X.up.reserve<GemmContrib>(std::max<size_t>(ncon, 1), &hc);
         std::vector<int64_t> start(thdr.size() + 1, 0);
         for (size_t t = 0; t < thdr.size(); ++t) start[t + 1] = start[t] + thdr[t].count;
         std::vector<int64_t> fill(start.begin(), start.end() - 1);
-        std::vector<GemmContrib> grouped(tcon.size());
-        for (auto& pc : tcon) grouped[fill[pc.first]++] = pc.second;
+        std::vector<double> ksum(thdr.size(), 0.0);
+        std::vector<int64_t> chunks(thdr.size(), 0);
+        for (const TCon& tc : tcon) {
+            const Elim& E = el[tc.e];
+            GemmContrib& g = hc[fill[tc.t]++];
+            if (tc.j >= 0) g = contrib(E.G + E.offs[tc.i], E.W, 1, E.MW + E.offs[tc.j], E.W, 0, E.r);
+            else g = contrib(E.MW + E.offs[-tc.j - 1], E.W, 1, E.G + E.offs[0], E.W, 0, E.r);
+            ksum[tc.t] += E.r;
+            chunks[tc.t] += cdiv(E.r, GEMM_BK);
+        }
         sch.tasks.reserve(thdr.size() + cands.size());
-        sch.contribs.reserve(tcon.size() + cands.size());
         for (size_t t = 0; t < thdr.size(); ++t) {
             const THdr& h = thdr[t];
             schur_bytes += 16.0 * h.M * double(h.N);
-            sch.add(h.C, h.ldc, h.M, h.N, GEMM_ADD, grouped.data() + start[t], size_t(h.count));
+            sch.add_ext(h.C, h.ldc, h.M, h.N, GEMM_ADD, start[t], h.count, ksum[t], chunks[t]);
+        }
+        int64_t pos = int64_t(tcon.size());
+        for (auto& cd : cands) {
+            hc[pos] = cd.g;
+            cd.base = sch.add_ext(nullptr, 0, cd.M, cd.N, GEMM_NORM, pos, 1, cd.g.K, cdiv(cd.g.K, GEMM_BK));
+            ++pos;
         }
     }
-    for (auto& cd : cands) cd.base = sch.add1(nullptr, 0, cd.M, cd.N, GEMM_NORM, cd.g);
     double* norms_d = sch.norm_tiles ? scr.alloc_n<double>(sch.norm_tiles) : nullptr;
     double* cand_ss_d = cands.empty() ? nullptr : scr.alloc_n<double>(cands.size());
     sch.launch(K_GEMM_SCHUR, norms_d, schur_bytes);
@@ -786,6 +829,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         ProfScope ps(K_REDUCE, 0.0, 8.0 * double(sch.norm_tiles));
         launch_sumsq_reduce(norms_d, upload(seg), int32_t(cands.size()), cand_ss_d, st);
     }
+    tick(HT_SCHUR);
     // one sync: LU status + candidate norms
     const size_t nbytes_read = sizeof(int) * nb + sizeof(double) * cands.size() + 8;
     char* hbuf = static_cast<char*>(X.pinned_buf(nbytes_read + 64));
@@ -795,6 +839,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     if (!cands.empty())
         H2F_CUDA(cudaMemcpyAsync(ss_h, cand_ss_d, sizeof(double) * cands.size(), cudaMemcpyDeviceToHost, st));
     X.sync();
+    tick(HT_SYNC2);
     for (int bi = 0; bi < nb; ++bi)
         if (status_h[bi]) {
             Error err(H2F_E_SINGULAR, "cluster " + std::to_string(batch[bi]) + " at level " +
@@ -857,6 +902,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         }
         L.done[ci] = 1;
     }
+    tick(HT_CREATE);
 }
 
 std::unique_ptr<Lvl> Factorizer::transition(Lvl& L) {
@@ -1040,6 +1086,13 @@ void Factorizer::dump_level_profile(int level) {
         if (d > 1e-4) std::fprintf(stderr, " %s=%.4f", kernel_name(k), d);
     }
     std::fprintf(stderr, " | kernels %.4f\n", dev);
+    static const char* names[HT_N] = {"pick", "aug", "sync1", "aug2", "proj", "elim", "schur", "sync2", "create", "trans"};
+    std::fprintf(stderr, "[level %d host]", level);
+    for (int i = 0; i < HT_N; ++i) {
+        std::fprintf(stderr, " %s=%.4f", names[i], ht[i]);
+        ht[i] = 0;
+    }
+    std::fprintf(stderr, "\n");
 }
 
 void Factorizer::run(double norm_estimate, const double* v0) {
@@ -1050,6 +1103,7 @@ void Factorizer::run(double norm_estimate, const double* v0) {
         level_t0 = std::chrono::steady_clock::now();
     }
     mark_node.assign(M.nnodes, 0);
+    node_bi.assign(M.nnodes, -1);
     if (const char* p = std::getenv("H2F_AUG_LOG")) aug_log = std::fopen(p, "a");
     clock.mark(PH_NORM);
     if (norm_estimate < 0) {
@@ -1069,6 +1123,7 @@ void Factorizer::run(double norm_estimate, const double* v0) {
         for (int level = M.depth; level >= M.top; --level) {
             level_marks.push_back(clock.size());
             clock.mark(PH_EXTRACT);
+            tick(HT_TRANS);
             if (!L) L = leaf_level(level);
             for (size_t i = 0; i < L->clusters.size(); ++i) L->live[i] = int(L->size[i]);
             attach_couplings(*L);
@@ -1147,6 +1202,7 @@ void Factorizer::run(double norm_estimate, const double* v0) {
                 L.reset();
             }
             F.recs.push_back(std::move(rec));
+            tick(HT_TRANS);
             if (level_prof) dump_level_profile(level);
         }
     }

@@ -112,6 +112,40 @@ __device__ __forceinline__ bool jac_rotation(double a, double b, double g, doubl
     return true;
 }
 
+// Row pair rotation with cached squared norms (a = |x|^2, b = |y|^2 on entry,
+// updated on exit): one dot product per pair instead of three.  After the
+// rotation the exact identities a' = a - t g, b' = b + t g hold; a norm that
+// shrinks below 1/64 of its old value is recomputed from the rotated row (the
+// update would lose relative accuracy to cancellation, cf. LAPACK dgesvj).
+// One warp per pair; a and b are warp-uniform.
+__device__ __forceinline__ bool jac_rotate_cached(double* __restrict__ x, double* __restrict__ y, int n, double tol,
+                                                  double& a, double& b) {
+    const int lane = threadIdx.x & 31;
+    double g = 0.0;
+    for (int i = lane; i < n; i += 32) g += x[i] * y[i];
+    g = warp_sum(g);
+    if (!(g != 0.0 && a > 0.0 && b > 0.0 && g * g > (tol * tol) * (a * b))) return false;
+    const double d = b - a;
+    const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(d * d + 4.0 * g * g));
+    const double c = rsqrt(1.0 + t * t), sn = c * t;
+    double ax = 0.0, by = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        const double u = x[i], v = y[i];
+        const double xu = c * u - sn * v, yv = sn * u + c * v;
+        x[i] = xu;
+        y[i] = yv;
+        ax += xu * xu;
+        by += yv * yv;
+    }
+    double a2 = a - t * g, b2 = b + t * g;
+    const bool ra = !(a2 >= a * (1.0 / 64.0)), rb = !(b2 >= b * (1.0 / 64.0));
+    if (ra) a2 = warp_sum(ax);
+    if (rb) b2 = warp_sum(by);
+    a = a2;
+    b = b2;
+    return true;
+}
+
 // circle-method round robin: player list [0, rot...]; pair i of round st
 __device__ __forceinline__ void rr_pair(int i, int st, int mm, int& p, int& q) {
     auto pos = [&](int j) { return j == 0 ? 0 : 1 + ((j - 1 + st) % (mm - 1)); };
@@ -120,39 +154,35 @@ __device__ __forceinline__ void rr_pair(int i, int st, int mm, int& p, int& q) {
 }
 
 // one-sided (Hestenes) Jacobi on the m rows (length n) of A, in place
-__device__ void jacobi_sweeps(double* A, int m, int n, int* flag) {
+__device__ void jacobi_sweeps(double* A, int m, int n, int* flag, double* nrm) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const double tol = 2.220446049250313e-16 * sqrt((double)n);
     const int mm = m + (m & 1);
     for (int sweep = 0; sweep < 60; ++sweep) {
         if (threadIdx.x == 0) *flag = 0;
+        // exact squared row norms at the start of every sweep (no drift)
+        for (int i = warp; i < m; i += nw) {
+            const double* ri = A + (int64_t)i * n;
+            double v = 0.0;
+            for (int c = lane; c < n; c += 32) v += ri[c] * ri[c];
+            v = warp_sum(v);
+            if (lane == 0) nrm[i] = v;
+        }
         __syncthreads();
         for (int st = 0; st < mm - 1; ++st) {
             for (int pi = warp; pi < mm / 2; pi += nw) {
                 int p, q;
                 rr_pair(pi, st, mm, p, q);
                 if (p >= m || q >= m) continue;
-                double* rp = A + (int64_t)p * n;
-                double* rq = A + (int64_t)q * n;
-                double a = 0.0, b = 0.0, g = 0.0;
-                for (int i = lane; i < n; i += 32) {
-                    const double x = rp[i], y = rq[i];
-                    a += x * x;
-                    b += y * y;
-                    g += x * y;
-                }
-                a = warp_sum(a);
-                b = warp_sum(b);
-                g = warp_sum(g);
-                double c, sn;
-                if (jac_rotation(a, b, g, tol, c, sn)) {
-                    for (int i = lane; i < n; i += 32) {
-                        const double x = rp[i], y = rq[i];
-                        rp[i] = c * x - sn * y;
-                        rq[i] = sn * x + c * y;
+                double a = nrm[p], b = nrm[q];
+                if (jac_rotate_cached(A + (int64_t)p * n, A + (int64_t)q * n, n, tol, a, b)) {
+                    if (lane == 0) {
+                        nrm[p] = a;
+                        nrm[q] = b;
+                        *flag = 1;
                     }
-                    if (lane == 0) *flag = 1;
                 }
+                __syncwarp();
             }
             __syncthreads();
         }
@@ -207,7 +237,7 @@ __global__ void __launch_bounds__(DT) jacobi_smem_kernel(const SvdTask* __restri
     double* A = dsh;
     for (int e = threadIdx.x; e < m * n; e += DT) A[e] = T.R[e];
     __syncthreads();
-    jacobi_sweeps(A, m, n, &flag);
+    jacobi_sweeps(A, m, n, &flag, A + m * n + 2 * m);  // after sig[m], rank[m]
     jacobi_finish(A, m, n, thresh, A + m * n, reinterpret_cast<int*>(A + m * n + m), &kept_s, T.U,
                   T.kept_out);
 }
@@ -538,6 +568,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* 
     extern __shared__ double bsm[];  // 2*JB rows of n; after the sweeps: sig[m]
     __shared__ int kept_s;
     __shared__ int rot_s;
+    __shared__ double bn[2 * JB];  // squared norms of the staged rows
     if (m == 0) {
         if (rank == 0 && threadIdx.x == 0) *CT.t.kept_out = 0;
         return;
@@ -578,6 +609,14 @@ __global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* 
                 }
             }
             __syncthreads();
+            for (int r = warp; r < 2 * JB; r += nw) {
+                const double* rr = bsm + (int64_t)r * n;
+                double v = 0.0;
+                for (int i = lane; i < n; i += 32) v += rr[i] * rr[i];
+                v = warp_sum(v);
+                if (lane == 0) bn[r] = v;
+            }
+            __syncthreads();
             if (st == 0) {
                 // rotations inside each block: round robin on JB rows, warps
                 // [0, nw/2) on block p, [nw/2, nw) on block q
@@ -588,16 +627,34 @@ __global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* 
                         int a, b;
                         rr_pair(pi, is, jbe, a, b);
                         if (a >= JB || b >= JB) continue;
-                        rotated |= jac_rotate_smem(bsm + (int64_t)(blk * JB + a) * n, bsm + (int64_t)(blk * JB + b) * n,
-                                                   n, tol);
+                        const int ra = blk * JB + a, rb = blk * JB + b;
+                        double na = bn[ra], nb = bn[rb];
+                        if (jac_rotate_cached(bsm + (int64_t)ra * n, bsm + (int64_t)rb * n, n, tol, na, nb)) {
+                            rotated = true;
+                            if (lane == 0) {
+                                bn[ra] = na;
+                                bn[rb] = nb;
+                            }
+                        }
+                        __syncwarp();
                     }
                     __syncthreads();
                 }
             }
             // cross rotations: inner step s pairs p-row i with q-row (i + s) % JB
             for (int s = 0; s < JB; ++s) {
-                for (int i = warp; i < JB; i += nw)
-                    rotated |= jac_rotate_smem(bsm + (int64_t)i * n, bsm + (int64_t)(JB + (i + s) % JB) * n, n, tol);
+                for (int i = warp; i < JB; i += nw) {
+                    const int rq = JB + (i + s) % JB;
+                    double na = bn[i], nb = bn[rq];
+                    if (jac_rotate_cached(bsm + (int64_t)i * n, bsm + (int64_t)rq * n, n, tol, na, nb)) {
+                        rotated = true;
+                        if (lane == 0) {
+                            bn[i] = na;
+                            bn[rq] = nb;
+                        }
+                    }
+                    __syncwarp();
+                }
                 __syncthreads();
             }
             for (int r = 0; r < 2 * JB; ++r) {
@@ -970,7 +1027,7 @@ void launch_qr_r_smem(const QrTask* d_tasks, int32_t ntasks, int32_t max_n, cuda
 void launch_jacobi_smem(const SvdTask* d_tasks, int32_t ntasks, int32_t max_n, double thresh,
                         cudaStream_t st) {
     if (ntasks <= 0) return;
-    const size_t smem = sizeof(double) * (size_t(max_n) * max_n + max_n) + sizeof(int) * max_n + 64;
+    const size_t smem = sizeof(double) * (size_t(max_n) * max_n + 3 * size_t(max_n)) + 64;  // A, sig, rank, norms
     cudaFuncSetAttribute(jacobi_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     jacobi_smem_kernel<<<ntasks, DT, smem, st>>>(d_tasks, thresh);
     count_launch();

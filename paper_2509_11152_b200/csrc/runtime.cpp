@@ -126,6 +126,13 @@ void Region::reset() {
 
 // ---------------------------------------------------------------- Uploader
 void* Uploader::put_bytes(const void* src, size_t bytes) {
+    void* host = nullptr;
+    void* d = reserve_bytes(bytes, &host);
+    if (bytes) std::memcpy(host, src, bytes);
+    return d;
+}
+
+void* Uploader::reserve_bytes(size_t bytes, void** host) {
     const size_t need = align_up(bytes ? bytes : 1);
     if (chunks_.empty() || used_ + need > chunks_[cur_].cap) {
         if (!chunks_.empty()) {
@@ -144,7 +151,7 @@ void* Uploader::put_bytes(const void* src, size_t bytes) {
         used_ = flushed_ = 0;
     }
     Chunk& c = chunks_[cur_];
-    if (bytes) std::memcpy(c.host + used_, src, bytes);
+    *host = c.host + used_;
     void* d = c.dev + used_;
     used_ += need;
     return d;

@@ -86,6 +86,15 @@ class Uploader {
         return static_cast<T*>(put_bytes(v.data(), v.size() * sizeof(T)));
     }
     void* put_bytes(const void* src, size_t bytes);
+    // space for `bytes` that the caller fills through *host before the next
+    // flush (avoids a staging copy for large task arrays)
+    void* reserve_bytes(size_t bytes, void** host);
+    template <class T> T* reserve(size_t n, T** host) {
+        void* h = nullptr;
+        T* d = static_cast<T*>(reserve_bytes(n * sizeof(T), &h));
+        *host = static_cast<T*>(h);
+        return d;
+    }
     void flush(cudaStream_t st);
     void reset();  // only after the stream has drained
     ~Uploader();
