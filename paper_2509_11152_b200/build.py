@@ -47,7 +47,7 @@ def _compile(src, verbose):
     if src.endswith(".cu") and verbose:
         cmd += ["-Xptxas", "-v"]
     if src.endswith(".cpp"):
-        cmd = [NVCC, *COMMON, "-x", "c++", "-c", path, "-o", _obj(src)]
+        cmd = [NVCC, *COMMON, "-Xcompiler", "-fopenmp", "-x", "c++", "-c", path, "-o", _obj(src)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed on {src}:\n{res.stderr}")
@@ -65,7 +65,7 @@ def build(verbose=False, force=False):
                     print(f"[{src}]\n{err}", file=sys.stderr)
     objs = [_obj(s) for s in SOURCES]
     if force or todo or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lgomp"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}")

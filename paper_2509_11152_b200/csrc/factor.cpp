@@ -39,7 +39,6 @@ struct View {
     double* p = nullptr;
     int64_t ld = 0;
     int rows = 0, cols = 0;
-    int stamp = 0, tidx = -1;  // Schur-target slot of the current batch
 };
 
 struct CouplingW {    // coupling block with logical zero padding (factorization.py:396-403)
@@ -200,14 +199,13 @@ class Factorizer {
     std::vector<int> mark_node;  // node-indexed batch membership stamp
     std::vector<int> node_bi;    // node -> position in the current batch (valid where stamped)
     int stamp = 0;
-    int target_stamp = 0;
     bool level_prof = false;
     FILE* aug_log = nullptr;  // H2F_AUG_LOG=path: per-cluster augmentation shapes (development aid)
     double level_prev[K_COUNT] = {};
     std::chrono::steady_clock::time_point level_t0;
     // host wall time per section of process_batch (H2F_LEVEL_PROF); the two
     // sync entries are the host blocked on the device
-    enum { HT_PICK, HT_AUG, HT_SYNC1, HT_AUG2, HT_PROJ, HT_ELIM, HT_SCHUR, HT_SYNC2, HT_CREATE, HT_TRANS, HT_N };
+    enum { HT_PICK, HT_AUG, HT_SYNC1, HT_AUG2, HT_PROJ, HT_ELIM, HT_S1, HT_S2, HT_S3, HT_SCHUR, HT_SYNC2, HT_CREATE, HT_TRANS, HT_N };
     double ht[HT_N] = {};
     std::chrono::steady_clock::time_point ht_last = std::chrono::steady_clock::now();
     void tick(int i) {
@@ -716,47 +714,41 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         GemmContrib g;
         int64_t base, ntiles;
     };
-    std::vector<THdr> thdr;
-    std::vector<TCon> tcon;
     std::vector<Cand> cands;
-    {
-        size_t guess = 0;
-        for (auto& e : el) guess += size_t(e.np) * (e.np + 1) / 2;
-        tcon.reserve(guess);
-    }
-    const int tstamp = ++target_stamp;
-    // every target is a (sub)block of one View; the view carries its slot
-    auto add_target = [&](View& Vw, double* C, int64_t ldc, int Mr, int Nc, int32_t ei, int32_t i, int32_t j) {
-        if (Mr <= 0 || Nc <= 0) return;
-        if (Vw.stamp != tstamp) {
-            Vw.stamp = tstamp;
-            Vw.tidx = int(thdr.size());
-            thdr.push_back({C, ldc, Mr, Nc, 0});
-        }
-        THdr& t = thdr[Vw.tidx];
-        if (t.C != C || t.M != Mr || t.N != Nc || t.ldc != ldc)
-            throw Error(H2F_E_INTERNAL, "assertion: Schur target shape mismatch");
-        ++t.count;
-        tcon.push_back({Vw.tidx, ei, i, j});
+    int64_t npairs = 0;  // updates of the batch
+    for (auto& e : el) npairs += int64_t(e.np) * (e.np + 1) / 2;
+    // Target resolution in two passes: (1) per eliminated cluster, in
+    // parallel, every update (i, j) is mapped to its target (sub)block -- the
+    // neighbour-list walks and block lookups, i.e. the cache misses; (2)
+    // slots per target and grouped contributions (bucket-parallel, below).
+    struct Upd {
+        const View* v;  // nullptr: fill candidate
+        double* C;
+        int64_t ldc;
+        int32_t M, N, i, j;  // j < 0: swap form, panel -j-1
     };
+    std::vector<std::vector<Upd>> upd(el.size());
+#pragma omp parallel for schedule(dynamic, 1) if (npairs > 20000)
     for (size_t ei = 0; ei < el.size(); ++ei) {
-        auto& e = el[ei];
+        const Elim& e = el[ei];
         const int c = e.c, r = e.r, kt = e.kt;
+        std::vector<Upd>& out = upd[ei];
+        out.reserve(size_t(e.np) * (e.np + 1) / 2);
         std::vector<int> opos(e.np);
-        for (int i = 1; i < e.np; ++i) opos[i] = L.at(e.ids[i]);
+        for (int i = 1; i < e.np; ++i) opos[i] = L.pos.at(e.ids[i]);
         std::vector<Nbrs::Item>::const_iterator walk{}, walk_end{};
         for (int i = 0; i < e.np; ++i)
             for (int j = i; j < e.np; ++j) {
                 if (i == 0 && j == 0) {
-                    View& Dcc = L.dcc(e.ci);
-                    add_target(Dcc, Dcc.p + int64_t(r) * Dcc.ld + r, Dcc.ld, kt, kt, int32_t(ei), 0, 0);
+                    const View& Dcc = *L.diag[e.ci];
+                    out.push_back({&Dcc, Dcc.p + int64_t(r) * Dcc.ld + r, Dcc.ld, kt, kt, 0, 0});
                 } else if (i == 0) {
                     const Entry& en = e.ents[j - 1];
-                    View* B = en.v;
-                    if (key_a(en.key) == c) add_target(*B, B->p + int64_t(r) * B->ld, B->ld, kt, B->cols, int32_t(ei), 0, j);
-                    else add_target(*B, B->p + r, B->ld, B->rows, kt, int32_t(ei), 0, -j - 1);
+                    const View* B = en.v;
+                    if (key_a(en.key) == c) out.push_back({B, B->p + int64_t(r) * B->ld, B->ld, kt, B->cols, 0, j});
+                    else out.push_back({B, B->p + r, B->ld, B->rows, kt, 0, -j - 1});
                 } else {
-                    View* B = nullptr;
+                    const View* B = nullptr;
                     if (i == j) {
                         B = L.diag[opos[i]];
                         walk = L.touch[opos[i]].begin();
@@ -766,58 +758,127 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                         while (walk != walk_end && walk->first < e.ids[j]) ++walk;
                         if (walk != walk_end && walk->first == e.ids[j]) B = walk->second.v;
                     }
-                    if (B) {
-                        add_target(*B, B->p, B->ld, B->rows, B->cols, int32_t(ei), i, j);
-                    } else {
-                        Cand cd;
-                        cd.key = mkkey(e.ids[i], e.ids[j]);
-                        cd.M = e.widths[i];
-                        cd.N = e.widths[j];
-                        cd.g = contrib(e.G + e.offs[i], e.W, 1, e.MW + e.offs[j], e.W, 0, r);
-                        cd.base = 0;
-                        cd.ntiles = GemmBuild::tiles(cd.M, cd.N);
-                        cands.push_back(cd);
-                    }
+                    if (B) out.push_back({B, B->p, B->ld, B->rows, B->cols, i, j});
+                    else out.push_back({nullptr, nullptr, 0, e.widths[i], e.widths[j], i, j});
                 }
             }
     }
+    tick(HT_S1);
+    // (2) slots and grouped contributions, parallel over hash buckets of the
+    // target view: a bucket scans all updates in reference order and keeps
+    // its own targets, so the contributions of every target stay in
+    // reference order (the only order the numerics depend on); the task order
+    // is bucket-major, deterministic for a given arena layout.
+    size_t total = 0;
+    for (auto& u : upd) total += u.size();
+    for (size_t ei = 0; ei < el.size(); ++ei) {  // fill candidates, serial, reference order
+        const Elim& e = el[ei];
+        for (const Upd& u : upd[ei]) {
+            if (u.v || u.M <= 0 || u.N <= 0) continue;
+            Cand cd;
+            cd.key = mkkey(e.ids[u.i], e.ids[u.j]);
+            cd.M = u.M;
+            cd.N = u.N;
+            cd.g = contrib(e.G + e.offs[u.i], e.W, 1, e.MW + e.offs[u.j], e.W, 0, e.r);
+            cd.base = 0;
+            cd.ntiles = GemmBuild::tiles(cd.M, cd.N);
+            cands.push_back(cd);
+        }
+    }
+    const int NBK = total > 20000 ? 16 : 1;
+    struct Bucket {
+        std::vector<THdr> th;
+        std::vector<TCon> tc;  // t = bucket-local slot
+        std::vector<double> ksum;
+        std::vector<int64_t> chunks;
+        int64_t slot0 = 0, con0 = 0;
+        bool bad = false;
+    };
+    std::vector<Bucket> bk(NBK);
+    auto bucket_of = [&](const View* v) {
+        const uint64_t h = (reinterpret_cast<uintptr_t>(v) >> 4) * 0x9E3779B97F4A7C15ull;
+        return int((h >> 40) % uint64_t(NBK));
+    };
+#pragma omp parallel for schedule(static, 1) if (NBK > 1)
+    for (int b = 0; b < NBK; ++b) {
+        Bucket& B = bk[b];
+        size_t cap = 1024;
+        while (cap < 4 * total / NBK + 16) cap <<= 1;
+        std::vector<std::pair<const View*, int>> table(cap, {nullptr, -1});
+        const size_t mask = cap - 1;
+        for (size_t ei = 0; ei < el.size(); ++ei)
+            for (const Upd& u : upd[ei]) {
+                if (!u.v || u.M <= 0 || u.N <= 0 || bucket_of(u.v) != b) continue;
+                size_t h = ((reinterpret_cast<uintptr_t>(u.v) >> 4) * 0x9E3779B97F4A7C15ull >> 20) & mask;
+                while (table[h].first && table[h].first != u.v) h = (h + 1) & mask;
+                int t;
+                if (!table[h].first) {
+                    t = int(B.th.size());
+                    table[h] = {u.v, t};
+                    B.th.push_back({u.C, u.ldc, u.M, u.N, 0});
+                    B.ksum.push_back(0.0);
+                    B.chunks.push_back(0);
+                } else {
+                    t = table[h].second;
+                    const THdr& th = B.th[t];
+                    if (th.C != u.C || th.M != u.M || th.N != u.N || th.ldc != u.ldc) B.bad = true;
+                }
+                ++B.th[t].count;
+                B.ksum[t] += el[ei].r;
+                B.chunks[t] += cdiv(el[ei].r, GEMM_BK);
+                B.tc.push_back({t, int32_t(ei), u.i, u.j});
+            }
+    }
+    int64_t nslots = 0, ntc = 0;
+    for (auto& B : bk) {
+        if (B.bad) throw Error(H2F_E_INTERNAL, "assertion: Schur target shape mismatch");
+        B.slot0 = nslots;
+        B.con0 = ntc;
+        nslots += int64_t(B.th.size());
+        ntc += int64_t(B.tc.size());
+    }
+    tick(HT_S2);
     GemmBuild sch;
     // algorithmic bytes: panels G and -W read once per
     // cluster, every existing target element read+written once
     double schur_bytes = 0;
     for (auto& e : el) schur_bytes += 16.0 * e.r * double(e.W);
     {
-        // contributions grouped per target (stable counting sort, reference
-        // order within a target) written straight into pinned upload memory
-        const size_t ncon = tcon.size() + cands.size();
+        // contributions grouped per target (stable counting sort per bucket)
+        // written straight into pinned upload memory
+        const size_t ncon = size_t(ntc) + cands.size();
         GemmContrib* hc = nullptr;
         sch.ext = X.up.reserve<GemmContrib>(std::max<size_t>(ncon, 1), &hc);
-        std::vector<int64_t> start(thdr.size() + 1, 0);
-        for (size_t t = 0; t < thdr.size(); ++t) start[t + 1] = start[t] + thdr[t].count;
-        std::vector<int64_t> fill(start.begin(), start.end() - 1);
-        std::vector<double> ksum(thdr.size(), 0.0);
-        std::vector<int64_t> chunks(thdr.size(), 0);
-        for (const TCon& tc : tcon) {
-            const Elim& E = el[tc.e];
-            GemmContrib& g = hc[fill[tc.t]++];
-            if (tc.j >= 0) g = contrib(E.G + E.offs[tc.i], E.W, 1, E.MW + E.offs[tc.j], E.W, 0, E.r);
-            else g = contrib(E.MW + E.offs[-tc.j - 1], E.W, 1, E.G + E.offs[0], E.W, 0, E.r);
-            ksum[tc.t] += E.r;
-            chunks[tc.t] += cdiv(E.r, GEMM_BK);
+        std::vector<int64_t> tstart(size_t(nslots) + 1, 0);
+        for (auto& B : bk)
+            for (size_t t = 0; t < B.th.size(); ++t) tstart[B.slot0 + t + 1] = B.th[t].count;
+        for (int64_t t = 0; t < nslots; ++t) tstart[t + 1] += tstart[t];
+#pragma omp parallel for schedule(static, 1) if (NBK > 1)
+        for (int b = 0; b < NBK; ++b) {
+            Bucket& B = bk[b];
+            std::vector<int64_t> fill(tstart.begin() + B.slot0, tstart.begin() + B.slot0 + int64_t(B.th.size()));
+            for (const TCon& tc : B.tc) {
+                const Elim& E = el[tc.e];
+                GemmContrib& g = hc[fill[tc.t]++];
+                if (tc.j >= 0) g = contrib(E.G + E.offs[tc.i], E.W, 1, E.MW + E.offs[tc.j], E.W, 0, E.r);
+                else g = contrib(E.MW + E.offs[-tc.j - 1], E.W, 1, E.G + E.offs[0], E.W, 0, E.r);
+            }
         }
-        sch.tasks.reserve(thdr.size() + cands.size());
-        for (size_t t = 0; t < thdr.size(); ++t) {
-            const THdr& h = thdr[t];
-            schur_bytes += 16.0 * h.M * double(h.N);
-            sch.add_ext(h.C, h.ldc, h.M, h.N, GEMM_ADD, start[t], h.count, ksum[t], chunks[t]);
-        }
-        int64_t pos = int64_t(tcon.size());
+        sch.tasks.reserve(size_t(nslots) + cands.size());
+        for (auto& B : bk)
+            for (size_t t = 0; t < B.th.size(); ++t) {
+                const THdr& h = B.th[t];
+                schur_bytes += 16.0 * h.M * double(h.N);
+                sch.add_ext(h.C, h.ldc, h.M, h.N, GEMM_ADD, tstart[B.slot0 + t], h.count, B.ksum[t], B.chunks[t]);
+            }
+        int64_t pos = ntc;
         for (auto& cd : cands) {
             hc[pos] = cd.g;
             cd.base = sch.add_ext(nullptr, 0, cd.M, cd.N, GEMM_NORM, pos, 1, cd.g.K, cdiv(cd.g.K, GEMM_BK));
             ++pos;
         }
     }
+    tick(HT_S3);
     double* norms_d = sch.norm_tiles ? scr.alloc_n<double>(sch.norm_tiles) : nullptr;
     double* cand_ss_d = cands.empty() ? nullptr : scr.alloc_n<double>(cands.size());
     sch.launch(K_GEMM_SCHUR, norms_d, schur_bytes);
@@ -1086,7 +1147,7 @@ void Factorizer::dump_level_profile(int level) {
         if (d > 1e-4) std::fprintf(stderr, " %s=%.4f", kernel_name(k), d);
     }
     std::fprintf(stderr, " | kernels %.4f\n", dev);
-    static const char* names[HT_N] = {"pick", "aug", "sync1", "aug2", "proj", "elim", "schur", "sync2", "create", "trans"};
+    static const char* names[HT_N] = {"pick", "aug", "sync1", "aug2", "proj", "elim", "s.resolve", "s.slots", "s.fill", "s.launch", "sync2", "create", "trans"};
     std::fprintf(stderr, "[level %d host]", level);
     for (int i = 0; i < HT_N; ++i) {
         std::fprintf(stderr, " %s=%.4f", names[i], ht[i]);

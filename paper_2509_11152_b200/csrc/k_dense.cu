@@ -525,6 +525,54 @@ __global__ void __launch_bounds__(JT, 1) jacobi_coop_kernel(const CoopSvdTask* _
     }
 }
 
+constexpr int JBT = 512;  // threads per CTA of the block-cyclic Jacobi
+
+// jac_rotate_cached with the row pair split over W warps (a named barrier of
+// 32*W threads per pair group, id 1 + grp): each warp owns a contiguous
+// slice of the rows, the dot products are summed over the slices in a fixed
+// order through `red` (double-buffered by the group's call parity `par`).
+template <int W>
+__device__ __forceinline__ bool jac_rotate_split(double* __restrict__ x, double* __restrict__ y, int n, double tol,
+                                                 double& a, double& b, int grp, int sub, double* red, int& par) {
+    if (W == 1) return jac_rotate_cached(x, y, n, tol, a, b);
+    const int lane = threadIdx.x & 31;
+    const int len = (n + W - 1) / W, i0 = sub * len, i1 = min(n, i0 + len);
+    auto group_sum = [&](double v) {
+        v = warp_sum(v);
+        double* slot = red + (grp * 2 + par) * W;
+        if (lane == 0) slot[sub] = v;
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * W) : "memory");
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) t += slot[w];
+        par ^= 1;
+        return t;
+    };
+    double g = 0.0;
+    for (int i = i0 + lane; i < i1; i += 32) g += x[i] * y[i];
+    g = group_sum(g);
+    if (!(g != 0.0 && a > 0.0 && b > 0.0 && g * g > (tol * tol) * (a * b))) return false;
+    const double d = b - a;
+    const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(d * d + 4.0 * g * g));
+    const double c = rsqrt(1.0 + t * t), sn = c * t;
+    double ax = 0.0, by = 0.0;
+    for (int i = i0 + lane; i < i1; i += 32) {
+        const double u = x[i], v = y[i];
+        const double xu = c * u - sn * v, yv = sn * u + c * v;
+        x[i] = xu;
+        y[i] = yv;
+        ax += xu * xu;
+        by += yv * yv;
+    }
+    double a2 = a - t * g, b2 = b + t * g;
+    const bool ra = !(a2 >= a * (1.0 / 64.0)), rb = !(b2 >= b * (1.0 / 64.0));
+    if (ra) a2 = group_sum(ax);
+    if (rb) b2 = group_sum(by);
+    a = a2;
+    b = b2;
+    return true;
+}
+
 // ---- block-cyclic multi-CTA Jacobi ----------------------------------------------
 // The m rows are cut into 2P blocks of JB rows; P co-resident CTAs play a
 // round-robin tournament over the blocks.  In one block step a CTA stages its
@@ -558,17 +606,21 @@ __device__ __forceinline__ bool jac_rotate_smem(double* __restrict__ x, double* 
 }
 
 template <int JB>
-__global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* __restrict__ tasks,
+__global__ void __launch_bounds__(JBT, 1) jacobi_block_kernel(const CoopSvdTask* __restrict__ tasks,
                                                             const int* __restrict__ cta_task, double thresh) {
     const CoopSvdTask CT = tasks[cta_task[blockIdx.x]];
     const int rank = blockIdx.x - CT.cta0, P = CT.ncta, NB2 = 2 * CT.ncta;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = JT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = JBT / 32;
     const int m = CT.t.m, n = CT.t.n;
     double* A = CT.t.R;
     extern __shared__ double bsm[];  // 2*JB rows of n; after the sweeps: sig[m]
     __shared__ int kept_s;
     __shared__ int rot_s;
     __shared__ double bn[2 * JB];  // squared norms of the staged rows
+    constexpr int WPP = (JBT / 32) / JB;  // warps per row pair (JB pairs per round)
+    __shared__ double red[JB * 2 * WPP];
+    const int grp = warp / WPP, sub = warp % WPP;
+    int par = 0;
     if (m == 0) {
         if (rank == 0 && threadIdx.x == 0) *CT.t.kept_out = 0;
         return;
@@ -597,7 +649,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* 
                         const int row = r < JB ? p0 + r : q0 + r - JB;
                         const bool ok = r < 2 * JB && (r < JB ? r < np : r - JB < nq);
                         v[u] = ok ? __ldcg(A + (int64_t)row * n + i) : 0.0;
-                        i += JT;
+                        i += JBT;
                         while (i >= n) {
                             i -= n;
                             ++r;
@@ -618,9 +670,9 @@ __global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* 
             }
             __syncthreads();
             if (st == 0) {
-                // rotations inside each block: round robin on JB rows, warps
-                // [0, nw/2) on block p, [nw/2, nw) on block q
-                const int half = nw / 2, blk = warp / half, wi = warp % half;
+                // rotations inside each block: round robin on JB rows, pair
+                // groups [0, JB/2) on block p, [JB/2, JB) on block q
+                const int half = JB / 2, blk = grp / half, wi = grp % half;
                 const int jbe = JB + (JB & 1);
                 for (int is = 0; is < jbe - 1; ++is) {
                     for (int pi = wi; pi < jbe / 2; pi += half) {
@@ -629,31 +681,30 @@ __global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* 
                         if (a >= JB || b >= JB) continue;
                         const int ra = blk * JB + a, rb = blk * JB + b;
                         double na = bn[ra], nb = bn[rb];
-                        if (jac_rotate_cached(bsm + (int64_t)ra * n, bsm + (int64_t)rb * n, n, tol, na, nb)) {
+                        if (jac_rotate_split<WPP>(bsm + (int64_t)ra * n, bsm + (int64_t)rb * n, n, tol, na, nb, grp, sub,
+                                                  red, par)) {
                             rotated = true;
-                            if (lane == 0) {
+                            if (lane == 0 && sub == 0) {
                                 bn[ra] = na;
                                 bn[rb] = nb;
                             }
                         }
-                        __syncwarp();
                     }
                     __syncthreads();
                 }
             }
             // cross rotations: inner step s pairs p-row i with q-row (i + s) % JB
             for (int s = 0; s < JB; ++s) {
-                for (int i = warp; i < JB; i += nw) {
-                    const int rq = JB + (i + s) % JB;
-                    double na = bn[i], nb = bn[rq];
-                    if (jac_rotate_cached(bsm + (int64_t)i * n, bsm + (int64_t)rq * n, n, tol, na, nb)) {
-                        rotated = true;
-                        if (lane == 0) {
-                            bn[i] = na;
-                            bn[rq] = nb;
-                        }
+                const int i = grp;
+                const int rq = JB + (i + s) % JB;
+                double na = bn[i], nb = bn[rq];
+                if (jac_rotate_split<WPP>(bsm + (int64_t)i * n, bsm + (int64_t)rq * n, n, tol, na, nb, grp, sub, red,
+                                          par)) {
+                    rotated = true;
+                    if (lane == 0 && sub == 0) {
+                        bn[i] = na;
+                        bn[rq] = nb;
                     }
-                    __syncwarp();
                 }
                 __syncthreads();
             }
@@ -663,7 +714,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* 
                 if (!v) continue;
                 double* dst = A + (int64_t)row * n;
                 const double* src = bsm + (int64_t)r * n;
-                for (int i = threadIdx.x; i < n; i += JT) __stcg(dst + i, src[i]);
+                for (int i = threadIdx.x; i < n; i += JBT) __stcg(dst + i, src[i]);
             }
             cta_group_barrier(CT.bar, P);
         }
@@ -683,11 +734,11 @@ __global__ void __launch_bounds__(JT, 1) jacobi_block_kernel(const CoopSvdTask* 
     }
     cta_group_barrier(CT.bar, P);
     double* dsh = bsm;
-    for (int i = threadIdx.x; i < m; i += JT) dsh[i] = __ldcg(CT.sig + i);
+    for (int i = threadIdx.x; i < m; i += JBT) dsh[i] = __ldcg(CT.sig + i);
     if (threadIdx.x == 0) kept_s = 0;
     __syncthreads();
     int cnt = 0;
-    for (int i = threadIdx.x; i < m; i += JT) cnt += dsh[i] >= thresh;
+    for (int i = threadIdx.x; i < m; i += JBT) cnt += dsh[i] >= thresh;
     atomicAdd(&kept_s, cnt);
     __syncthreads();
     const int kept = kept_s;
@@ -1127,7 +1178,7 @@ int jacobi_block_capacity(int max_n, int max_m) {
     const void* fn = jacobi_block_rows(max_n) == 8 ? (const void*)jacobi_block_kernel<8> : (const void*)jacobi_block_kernel<4>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, JT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, JBT, smem);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return per_sm * sms;
@@ -1140,7 +1191,7 @@ cudaError_t launch_jacobi_block(const CoopSvdTask* d_tasks, int32_t total_ctas, 
     const void* fn = jacobi_block_rows(max_n) == 8 ? (const void*)jacobi_block_kernel<8> : (const void*)jacobi_block_kernel<4>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {(void*)&d_tasks, (void*)&d_cta_task, (void*)&thresh};
-    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(total_ctas), dim3(JT), args, smem, st);
+    cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(total_ctas), dim3(JBT), args, smem, st);
     count_launch();
     return e;
 }

@@ -9,11 +9,27 @@ from oracle import h2_oracle as O
 
 fam, n, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 over = {}
+perturb = 0.0
 for a in sys.argv[4:]:
-    k, v = a.split('='); over[k] = float(v) if '.' in v else int(v)
+    k, v = a.split('=')
+    if k == "perturb":
+        perturb = float(v)
+        continue
+    over[k] = float(v) if '.' in v or 'e' in v else int(v)
 t0 = time.perf_counter()
 tree, part, spec, h2, prm = P.build_problem(fam, n, **over)
 print("build", time.perf_counter() - t0, flush=True)
+if perturb:
+    # rounding-level perturbation of the dense near field (a different draw of
+    # the same algorithm on an operator equal to working precision)
+    rng = np.random.default_rng(1)
+    for key in sorted(h2.dense):
+        blk = h2.dense[key]
+        z = rng.standard_normal(blk.shape)
+        if key[0] == key[1]:
+            z = 0.5 * (z + z.T)  # diagonal blocks stay symmetric
+        h2.dense[key] = blk * (1.0 + perturb * z)
+    print("perturbed dense blocks by", perturb, flush=True)
 x_ref = np.random.Generator(np.random.Philox(7)).standard_normal(n)
 with threadpool_limits(1):
     b = O.matvec(h2, x_ref)
