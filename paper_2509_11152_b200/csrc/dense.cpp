@@ -117,7 +117,7 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
                 k.ldm = J.ldm;
                 k.Vt = keep ? scr.alloc_n<double>(int64_t(HH_NB) * pp.Lp) : vbuf[pp.job];
                 k.T = scr.alloc_n<double>(HH_NB * HH_NB);
-                k.part = scr.alloc_n<double>(int64_t(pp.ncta + 1) * (HH_NB + 2));
+                k.part = scr.alloc_n<double>(int64_t(2) * (pp.ncta + 1) * (HH_NB + 2));
                 k.gram = scr.alloc_n<double>(int64_t(pp.ncta) * HH_NB * HH_NB);
                 k.bar = bars + 2 * t;
                 k.L = J.L;

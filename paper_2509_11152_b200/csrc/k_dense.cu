@@ -13,6 +13,7 @@
 // results are run-to-run deterministic.
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -1166,7 +1167,15 @@ int jacobi_coop_capacity(int max_n, int max_m) {
 }
 
 
-int jacobi_block_rows(int n) { return (size_t(16) * n * 8 <= size_t(200) * 1024) ? 8 : 4; }
+int jacobi_block_rows(int n) {
+    // H2F_JACOBI_JB4_MIN_N: use 4-row blocks (twice the CTAs per task) from this n on
+    static const int jb4_min = [] {
+        const char* e = std::getenv("H2F_JACOBI_JB4_MIN_N");
+        return e ? std::atoi(e) : 1 << 30;
+    }();
+    if (n >= jb4_min) return 4;
+    return (size_t(16) * n * 8 <= size_t(200) * 1024) ? 8 : 4;
+}
 
 size_t jacobi_block_smem(int max_n, int max_m) {
     const int jb = jacobi_block_rows(max_n);

@@ -5,7 +5,8 @@
 // complete QR of b_aug, :98) once the clusters outgrow one CTA.  One panel of
 // HH_NB columns is spread over `ncta` co-resident CTAs, each holding a
 // contiguous slice of the panel's rows in shared memory; every column costs
-// two group barriers (norm, then the dots with the rest of the panel) and the
+// one group barrier (norm and the dots with the rest of the panel travel
+// together, the reflector's dots are recovered from the unscaled ones) and the
 // partial sums are reduced in a fixed order, so the factor is bitwise
 // reproducible.  The trailing update A -= V T^T (V^T A) runs on the DMMA tile
 // GEMM (k_gemm.cu) between panels.
@@ -64,6 +65,7 @@ hh_panel_kernel(const HhPanelTask* __restrict__ tasks, const int32_t* __restrict
     __shared__ double taus[HH_NB];
     __shared__ double red[HW];
     __shared__ double dsh[HH_NB + 2];
+    __shared__ double wsh[HH_NB];
     __shared__ double Tm[HH_NB][HH_NB + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* M0 = T.M + (int64_t)T.j0 * T.ldm + T.j0 + r0;
@@ -73,68 +75,63 @@ hh_panel_kernel(const HhPanelTask* __restrict__ tasks, const int32_t* __restrict
             S[jj * lds + i] = (jj < nbp && i < rows) ? M0[(int64_t)jj * T.ldm + i] : 0.0;
     __syncthreads();
 
-    // pa: [G + 1] partial norms + alpha, double-buffered by column parity (a
-    // column with tau == 0 skips the second barrier); pb: [(G + 1) * HH_NB]
-    // partial dots + heads
-    double* pb = T.part + 2 * (G + 1);
+    // One group barrier per column: every CTA publishes, for the rows it owns
+    // strictly below the diagonal, ss = |x|^2 and dx_c = x . a_c for the
+    // panel columns c > jj (x = column jj before scaling); CTA 0, which owns
+    // the panel's diagonal rows, adds alpha = a_jj[jj] and the head row a_c[jj].
+    // With beta, tau, scal = 1/(alpha - beta) (dlarfg) the reflector is
+    // v = [1; scal x], so v . a_c = a_c[jj] + scal dx_c and w_c = tau v . a_c.
+    // Partials: (G + 1) x (HH_NB + 2) per buffer, double-buffered by column
+    // parity (a CTA cannot reach column jj + 2 before every CTA has read jj).
+    const int PW = HH_NB + 2;
     for (int jj = 0; jj < nbp; ++jj) {
-        double* pa = T.part + (jj & 1) * (G + 1);
+        double* pp = T.part + (int64_t)(jj & 1) * (G + 1) * PW;
         const int lo = (int)max((int64_t)0, (int64_t)(jj + 1) - r0);  // local rows strictly below the diagonal
-        double ss = 0.0;
-        for (int i = lo + threadIdx.x; i < rows; i += HT) {
-            const double x = S[jj * lds + i];
-            ss += x * x;
+        // slot 0: ss; slots c (jj < c < nbp): dx_c
+        for (int c = jj + warp; c < nbp; c += HW) {
+            double d = 0.0;
+            if (c == jj)
+                for (int i = lo + lane; i < rows; i += 32) d += S[jj * lds + i] * S[jj * lds + i];
+            else
+                for (int i = lo + lane; i < rows; i += 32) d += S[jj * lds + i] * S[c * lds + i];
+            d = warp_sum(d);
+            if (lane == 0) pp[(int64_t)g * PW + (c == jj ? 0 : c)] = d;
         }
-        ss = block_sum(ss, red);
-        if (threadIdx.x == 0) {
-            pa[g] = ss;
-            if (g == 0) pa[G] = S[jj * lds + jj];
-        }
+        if (g == 0)
+            for (int c = jj + threadIdx.x; c < nbp; c += HT) pp[(int64_t)G * PW + (c == jj ? 0 : c)] = S[c * lds + jj];
         group_barrier(T.bar, G);
-        if (warp == 0) {
+        // fixed-order sums over the CTAs (identical in every CTA)
+        for (int c = jj + warp; c < nbp; c += HW) {
             double v = 0.0;
-            for (int q = lane; q < G; q += 32) v += __ldcg(pa + q);
+            for (int q = lane; q < G; q += 32) v += __ldcg(pp + (int64_t)q * PW + (c == jj ? 0 : c));
             v = warp_sum(v);
-            if (lane == 0) {
-                dsh[HH_NB] = v;
-                dsh[HH_NB + 1] = __ldcg(pa + G);
-            }
+            if (lane == 0) dsh[c] = v;
         }
+        if (threadIdx.x == 0) dsh[HH_NB] = __ldcg(pp + (int64_t)G * PW);  // alpha
         __syncthreads();
         double beta, tau, scal;
-        hh_reflector(dsh[HH_NB + 1], dsh[HH_NB], beta, tau, scal);
-        if (tau != 0.0)
+        hh_reflector(dsh[HH_NB], dsh[jj], beta, tau, scal);
+        // w_c = tau (a_c[jj] + scal dx_c) for c > jj (tau is identical in every CTA)
+        if (tau != 0.0) {
+            for (int c = jj + 1 + threadIdx.x; c < nbp; c += HT)
+                wsh[c] = tau * (__ldcg(pp + (int64_t)G * PW + c) + scal * dsh[c]);
+            __syncthreads();
+            // a_c -= w_c v on the owned rows below the diagonal (v = scal x),
+            // then x -> v; CTA 0 also updates the head row
+            const int w = nbp - jj - 1;
+            for (int e = threadIdx.x; e < w * rows; e += HT) {
+                const int c = jj + 1 + e / rows, i = e % rows;
+                if (i >= lo) S[c * lds + i] -= wsh[c] * (scal * S[jj * lds + i]);
+            }
+            if (g == 0)
+                for (int c = jj + 1 + threadIdx.x; c < nbp; c += HT) S[c * lds + jj] -= wsh[c];
+            __syncthreads();
             for (int i = lo + threadIdx.x; i < rows; i += HT) S[jj * lds + i] *= scal;
+        }
         if (threadIdx.x == 0) {
             taus[jj] = tau;
             if (g == 0) S[jj * lds + jj] = beta;
         }
-        __syncthreads();
-        if (tau == 0.0 || jj + 1 >= nbp) continue;  // tau is identical in every CTA
-        for (int c = jj + 1 + warp; c < nbp; c += HW) {
-            double d = 0.0;
-            for (int i = lo + lane; i < rows; i += 32) d += S[jj * lds + i] * S[c * lds + i];
-            d = warp_sum(d);
-            if (lane == 0) {
-                pb[(int64_t)g * HH_NB + c] = d;
-                if (g == 0) pb[(int64_t)G * HH_NB + c] = S[c * lds + jj];
-            }
-        }
-        group_barrier(T.bar, G);
-        for (int c = jj + 1 + warp; c < nbp; c += HW) {
-            double v = 0.0;
-            for (int q = lane; q < G; q += 32) v += __ldcg(pb + (int64_t)q * HH_NB + c);
-            v = warp_sum(v);
-            if (lane == 0) dsh[c] = (v + __ldcg(pb + (int64_t)G * HH_NB + c)) * tau;
-        }
-        __syncthreads();
-        const int w = nbp - jj - 1;
-        for (int e = threadIdx.x; e < w * rows; e += HT) {
-            const int c = jj + 1 + e / rows, i = e % rows;
-            if (i >= lo) S[c * lds + i] -= dsh[c] * S[jj * lds + i];
-        }
-        if (g == 0)
-            for (int c = jj + 1 + threadIdx.x; c < nbp; c += HT) S[c * lds + jj] -= dsh[c];
         __syncthreads();
     }
 

@@ -150,7 +150,7 @@ struct HhPanelTask {
     int64_t ldm;
     double* Vt;
     double* T;
-    double* part;        // (ncta + 1) * (HH_NB + 2) doubles
+    double* part;        // 2 * (ncta + 1) * (HH_NB + 2) doubles (column-parity double buffer)
     double* gram;        // ncta * HH_NB * HH_NB doubles
     uint32_t* bar;       // 2 words, zeroed
     int32_t L, j0, nbp, chunk;
