@@ -3,6 +3,7 @@
 #pragma once
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.h"
@@ -118,7 +119,14 @@ struct GemmBuild {
         const int64_t* dcta = ntiles > gemm_grid(ntiles) ? X.up.put(cta_ranges()) : nullptr;
         X.up.flush(X.stream);
         ProfScope ps(kid, flops, bytes_override >= 0 ? bytes_override : bytes, double(ntiles));
-        launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), ntiles, dcta, norms, X.stream);
+        // short average K per tile: the C read-modify-write dominates, use
+        // the variant that prefetches C during the tile's math
+        static const double kmax = [] {
+            const char* e = std::getenv("H2F_GEMM_PREC_KMAX");
+            return e ? std::atof(e) : 96.0;
+        }();
+        const double keff = flops / (double(ntiles) * 2.0 * GEMM_TILE * GEMM_TILE);
+        launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), ntiles, dcta, norms, X.stream, keff < kmax);
     }
 };
 

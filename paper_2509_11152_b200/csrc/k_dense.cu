@@ -1171,7 +1171,7 @@ int jacobi_block_rows(int n) {
     // H2F_JACOBI_JB4_MIN_N: use 4-row blocks (twice the CTAs per task) from this n on
     static const int jb4_min = [] {
         const char* e = std::getenv("H2F_JACOBI_JB4_MIN_N");
-        return e ? std::atoi(e) : 1 << 30;
+        return e ? std::atoi(e) : 512;
     }();
     if (n >= jb4_min) return 4;
     return (size_t(16) * n * 8 <= size_t(200) * 1024) ? 8 : 4;

@@ -28,11 +28,15 @@ constexpr int GEMM_THREADS = 128;
 // contributions of a tile (no pipeline restart between contributions); the
 // operands are staged in their stored orientation with conflict-free padded
 // strides, alpha (uniform per task) is applied in the epilogue.
-constexpr int BK2 = GEMM_BK, STAGES = 3;
+constexpr int BK2 = GEMM_BK;
 constexpr int LDK2 = BK2 + 4;   // [m][k] / [n][k] layouts (k contiguous)
 constexpr int LDM2 = BM + 4;    // [k][m] / [k][n] layouts
 constexpr int STAGE_ELEMS = (BM * LDK2 > BK2 * LDM2 ? BM * LDK2 : BK2 * LDM2);
-constexpr size_t GEMM2_SMEM = sizeof(double) * 2 * STAGES * STAGE_ELEMS;
+constexpr int LDC = BN + 4;     // prefetched C tile [m][n]
+// stages x (A, B) + (PREC) the prefetched C tile
+template <int NS, bool PREC> constexpr size_t gemm_smem() {
+    return sizeof(double) * (2 * NS * STAGE_ELEMS + (PREC ? BM * LDC : 0));
+}
 
 // cp.async with zero fill: copies `bytes` (0, 8 or 16) of src and zero-fills
 // the rest of the CP-byte destination
@@ -160,15 +164,24 @@ struct ChunkMeta {
     int last;     // last chunk of its tile: run the epilogue after it
     int k0;       // k offset of the chunk within its contribution
     int64_t local;  // tile index within the task
+    int first;    // first chunk of its tile
+    int pad_;
 };
 
+// NS pipeline stages; PREC: the C tile of a GEMM_ADD task is prefetched into
+// shared memory (cp.async) when the tile's first chunk is consumed, so its
+// read latency overlaps the tile's math instead of the epilogue (pays off for
+// short-K tiles, where the read-modify-write of C dominates)
+template <int NS, bool PREC>
 __global__ void __launch_bounds__(GEMM_THREADS, 2)
 gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restrict__ contribs,
                   const int64_t* __restrict__ tile_start, int ntasks, int64_t ntiles,
                   const int64_t* __restrict__ cta_tiles, double* __restrict__ norms) {
+    constexpr int STAGES = NS;
     extern __shared__ __align__(16) double gsm[];
     __shared__ double red[GEMM_THREADS / 32];
     __shared__ ChunkMeta meta[STAGES];
+    double* Cs = gsm + 2 * STAGES * STAGE_ELEMS;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -193,7 +206,9 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
     int64_t p_pc = 0, p_end = 0;
     int p_pk = 0, p_m0 = 0, p_n0 = 0, p_M = 0, p_N = 0;
     int64_t p_local = 0;
+    int p_first = 1;
     auto open_tile = [&]() {
+        p_first = 1;
         while (p_ti + 1 < ntasks && p_tile >= tile_start[p_ti + 1]) ++p_ti;
         const GemmTask& T = tasks[p_ti];
         p_local = p_tile - tile_start[p_ti];
@@ -213,6 +228,7 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
             m.contrib = -1;
         } else if (p_pc >= p_end) {  // tile without contributions: epilogue only
             m.contrib = -2;
+            m.first = 1;
             m.ti = p_ti;
             m.m0 = p_m0;
             m.n0 = p_n0;
@@ -226,6 +242,8 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
             stage_chunk(P, p_M, p_N, p_m0, p_n0, p_pk, As, As + STAGE_ELEMS);
             m.contrib = (int)p_pc;
             m.k0 = p_pk;
+            m.first = p_first;
+            p_first = 0;
             m.ti = p_ti;
             m.m0 = p_m0;
             m.n0 = p_n0;
@@ -261,6 +279,36 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
         const ChunkMeta m = meta[cur];
         if (m.contrib == -1) break;
         issue((it + STAGES - 1) % STAGES);  // refills the stage consumed last iteration
+        if (PREC && m.contrib >= 0 && m.first) {
+            const GemmTask& T = tasks[m.ti];
+            if (T.mode == GEMM_ADD) {
+                // 64 x 64 C tile -> Cs (zero-filled outside M x N); the top-of-
+                // loop barrier guarantees the previous epilogue is done with Cs
+                const bool vec = ((reinterpret_cast<uintptr_t>(T.C) | (uintptr_t)(T.ldc * 8)) & 15) == 0;
+                const int rmax = T.M - m.m0;
+                if (vec) {
+                    const int c2 = (threadIdx.x & 31) * 2, rb = threadIdx.x >> 5;
+                    const int cv = T.N - m.n0 - c2;
+                    const int bytes = cv >= 2 ? 16 : (cv > 0 ? 8 : 0);
+                    const double* src = T.C + (int64_t)(m.m0 + rb) * T.ldc + m.n0 + c2;
+#pragma unroll
+                    for (int r = 0; r < BM; r += 4) {
+                        cp_async<16>(Cs + (r + rb) * LDC + c2, src, r + rb < rmax ? bytes : 0);
+                        src += 4 * T.ldc;
+                    }
+                } else {
+                    const int c1 = threadIdx.x & 63, rb = threadIdx.x >> 6;
+                    const int bytes = c1 < T.N - m.n0 ? 8 : 0;
+                    const double* src = T.C + (int64_t)(m.m0 + rb) * T.ldc + m.n0 + c1;
+#pragma unroll 8
+                    for (int r = 0; r < BM; r += 2) {
+                        cp_async<8>(Cs + (r + rb) * LDC + c1, src, r + rb < rmax ? bytes : 0);
+                        src += 2 * T.ldc;
+                    }
+                }
+                cp_async_commit();
+            }
+        }
         if (m.contrib >= 0) {
             const GemmContrib P = contribs[m.contrib];
             const double* As = gsm + (2 * cur) * STAGE_ELEMS;
@@ -277,6 +325,7 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
         if (!m.last) continue;
         // ---- epilogue of tile m ----
         const GemmTask T = tasks[m.ti];
+        if (m.contrib == -2 && T.mode == GEMM_ADD) continue;  // C += 0
         const double alpha = (T.contrib_end > T.contrib_begin) ? contribs[T.contrib_begin].alpha : 1.0;
         if (T.mode == GEMM_NORM) {
             double ss = 0.0;
@@ -299,7 +348,17 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
             // the stores: the compiler cannot hoist loads over possibly
             // aliasing stores on its own
             double cv[4][4][2];
-            if (T.mode == GEMM_ADD) {
+            if (PREC && T.mode == GEMM_ADD) {
+                cp_async_wait<0>();
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+#pragma unroll
+                        for (int q = 0; q < 2; ++q)
+                            cv[i][j][q] = Cs[(wm * 32 + i * 8 + g) * LDC + wn * 32 + j * 8 + 2 * t + q];
+            } else if (T.mode == GEMM_ADD) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int row = m.m0 + wm * 32 + i * 8 + g;
@@ -424,15 +483,24 @@ int gemm_grid(int64_t ntiles) { return grid_for(ntiles, 2); }
 
 void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
                        const int64_t* d_tile_start, int32_t ntasks, int64_t ntiles,
-                       const int64_t* d_cta_tiles, double* d_norms, cudaStream_t st) {
+                       const int64_t* d_cta_tiles, double* d_norms, cudaStream_t st, bool short_k) {
     if (ntiles <= 0) return;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(gemm_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM2_SMEM);
+        cudaFuncSetAttribute(gemm_tasks_kernel<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)gemm_smem<3, false>());
+        cudaFuncSetAttribute(gemm_tasks_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)gemm_smem<2, true>());
         configured = true;
     }
-    gemm_tasks_kernel<<<gemm_grid(ntiles), GEMM_THREADS, GEMM2_SMEM, st>>>(d_tasks, d_contribs, d_tile_start,
-                                                                          ntasks, ntiles, d_cta_tiles, d_norms);
+    static const bool force_prec = std::getenv("H2F_GEMM_PREC") != nullptr;
+    static const bool no_prec = std::getenv("H2F_GEMM_NOPREC") != nullptr;
+    if ((short_k || force_prec) && !no_prec)
+        gemm_tasks_kernel<2, true><<<gemm_grid(ntiles), GEMM_THREADS, gemm_smem<2, true>(), st>>>(
+            d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_cta_tiles, d_norms);
+    else
+        gemm_tasks_kernel<3, false><<<gemm_grid(ntiles), GEMM_THREADS, gemm_smem<3, false>(), st>>>(
+            d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_cta_tiles, d_norms);
     count_launch();
 }
 

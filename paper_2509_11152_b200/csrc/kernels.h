@@ -243,7 +243,7 @@ struct GemvContrib {
 int gemm_grid(int64_t ntiles);
 void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
                        const int64_t* d_tile_start, int32_t ntasks, int64_t ntiles,
-                       const int64_t* d_cta_tiles, double* d_norms, cudaStream_t st);
+                       const int64_t* d_cta_tiles, double* d_norms, cudaStream_t st, bool short_k = false);
 void launch_copy_tasks(const CopyTask* d_tasks, const int64_t* d_tile_start, int32_t ntasks,
                        int64_t ntiles, cudaStream_t st);
 void launch_qr_r_smem(const QrTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st);
