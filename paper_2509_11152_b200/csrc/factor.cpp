@@ -728,6 +728,12 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         int32_t M, N, i, j;  // j < 0: swap form, panel -j-1
     };
     std::vector<std::vector<Upd>> upd(el.size());
+    std::vector<std::vector<int64_t>> boff(el.size());  // per cluster: bucket segment offsets
+    const int NBK = npairs > 20000 ? 16 : 1;
+    auto bucket_of = [NBK](const View* v) {
+        const uint64_t h = (reinterpret_cast<uintptr_t>(v) >> 4) * 0x9E3779B97F4A7C15ull;
+        return int((h >> 40) % uint64_t(NBK));
+    };
 #pragma omp parallel for schedule(dynamic, 1) if (npairs > 20000)
     for (size_t ei = 0; ei < el.size(); ++ei) {
         const Elim& e = el[ei];
@@ -762,6 +768,16 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                     else out.push_back({nullptr, nullptr, 0, e.widths[i], e.widths[j], i, j});
                 }
             }
+        // stable counting sort of the targeted updates by bucket; candidates
+        // (v == nullptr) go to the extra last segment
+        std::vector<int64_t>& off = boff[ei];
+        off.assign(NBK + 2, 0);
+        for (const Upd& u : out) ++off[1 + (u.v ? bucket_of(u.v) : NBK)];
+        for (int b = 0; b < NBK + 1; ++b) off[b + 1] += off[b];
+        std::vector<Upd> sorted(out.size());
+        std::vector<int64_t> pos(off.begin(), off.end() - 1);
+        for (const Upd& u : out) sorted[pos[u.v ? bucket_of(u.v) : NBK]++] = u;
+        out.swap(sorted);
     }
     tick(HT_S1);
     // (2) slots and grouped contributions, parallel over hash buckets of the
@@ -769,12 +785,11 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     // its own targets, so the contributions of every target stay in
     // reference order (the only order the numerics depend on); the task order
     // is bucket-major, deterministic for a given arena layout.
-    size_t total = 0;
-    for (auto& u : upd) total += u.size();
     for (size_t ei = 0; ei < el.size(); ++ei) {  // fill candidates, serial, reference order
         const Elim& e = el[ei];
-        for (const Upd& u : upd[ei]) {
-            if (u.v || u.M <= 0 || u.N <= 0) continue;
+        for (int64_t k = boff[ei][NBK]; k < boff[ei][NBK + 1]; ++k) {
+            const Upd& u = upd[ei][k];
+            if (u.M <= 0 || u.N <= 0) continue;
             Cand cd;
             cd.key = mkkey(e.ids[u.i], e.ids[u.j]);
             cd.M = u.M;
@@ -785,7 +800,6 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             cands.push_back(cd);
         }
     }
-    const int NBK = total > 20000 ? 16 : 1;
     struct Bucket {
         std::vector<THdr> th;
         std::vector<TCon> tc;  // t = bucket-local slot
@@ -795,20 +809,19 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         bool bad = false;
     };
     std::vector<Bucket> bk(NBK);
-    auto bucket_of = [&](const View* v) {
-        const uint64_t h = (reinterpret_cast<uintptr_t>(v) >> 4) * 0x9E3779B97F4A7C15ull;
-        return int((h >> 40) % uint64_t(NBK));
-    };
 #pragma omp parallel for schedule(static, 1) if (NBK > 1)
     for (int b = 0; b < NBK; ++b) {
         Bucket& B = bk[b];
+        size_t mine = 0;  // updates of this bucket: bounds its distinct targets
+        for (size_t ei = 0; ei < el.size(); ++ei) mine += size_t(boff[ei][b + 1] - boff[ei][b]);
         size_t cap = 1024;
-        while (cap < 4 * total / NBK + 16) cap <<= 1;
+        while (cap < 2 * mine + 16) cap <<= 1;
         std::vector<std::pair<const View*, int>> table(cap, {nullptr, -1});
         const size_t mask = cap - 1;
         for (size_t ei = 0; ei < el.size(); ++ei)
-            for (const Upd& u : upd[ei]) {
-                if (!u.v || u.M <= 0 || u.N <= 0 || bucket_of(u.v) != b) continue;
+            for (int64_t k = boff[ei][b]; k < boff[ei][b + 1]; ++k) {
+                const Upd& u = upd[ei][k];
+                if (u.M <= 0 || u.N <= 0) continue;
                 size_t h = ((reinterpret_cast<uintptr_t>(u.v) >> 4) * 0x9E3779B97F4A7C15ull >> 20) & mask;
                 while (table[h].first && table[h].first != u.v) h = (h + 1) & mask;
                 int t;

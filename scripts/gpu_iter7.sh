@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
+timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+tail -5 gpurun_out/pytest_gpu.log
+H2F_LEVEL_PROF=1 timeout 900 python scripts/scale_probe.py helmholtz3d:131072:kappa=0.0 > gpurun_out/scale.log 2> gpurun_out/scale.err
+echo "probe exit $?"; grep -i "level.*host" gpurun_out/scale.err | cut -c1-400
+python -c "
+import json; d=json.loads(open('gpurun_out/scale.log').readline()); print('fact', d['fact_s'], 'e_b', d['e_b'], d['e_b_raw'])"
