@@ -114,7 +114,8 @@ struct SolvePlan {
         // scatter; backward = upper TRSM, gather GEMM, add, rotation GEMM, copy
         bool gemm = false;
         DevGemm f_rot, f_prod, b_gather, b_rot;
-        DevCopy f_copy, b_add, b_copy;
+        DevCopy f_copy, b_copy;
+        std::vector<DevCopy> b_add;  // one launch per split-K partial of the gather
         DevTrsm f_trsm, b_trsm;
     };
     struct Level {
@@ -290,7 +291,8 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
         SolvePlan::Batch& B = P.levels[hb.level].batches[hb.batch];
         double* yv = P.yv[hb.level];
         GemmBuild frot, fprod, bgat, brot;
-        CopyBuild fcopy, badd, bcopy;
+        CopyBuild fcopy, bcopy;
+        std::vector<CopyBuild> badd;
         std::vector<TrsmTask> ft[2], bt[2];
         int mr[2] = {1, 1};
         double tf = 0;
@@ -300,7 +302,8 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
             double* yc = yv + sc.off * q;
             double* wk = P.work + wo;
             double* acc = wk + int64_t(s_) * q;
-            wo += (int64_t(s_) + r_) * q;
+            const int nsplit = r_ > 0 ? int(std::max<int64_t>(1, cdiv(sc.W, SOLVE_GATHER_COLS))) : 0;
+            wo += (int64_t(s_) + int64_t(nsplit) * r_) * q;
             // forward (solve.py:90-128): wk = Q~^T y_c
             frot.add1(wk, q, s_, q, GEMM_STORE, contrib(sc.q, s_, 1, yc, q, 0, s_));
             // skeleton rows pass through; redundant rows are solved below
@@ -330,14 +333,28 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
                 t.mode = TRSM_UPPER;
                 bt[vi].push_back(t);
             }
-            // gather: acc = sum_e (-W_e) y[span_e], in edge order
-            std::vector<GemmContrib> cs;
+            // gather acc = sum_e (-W_e) y[span_e], split-K: the concatenated
+            // edge columns are cut into SOLVE_GATHER_COLS-wide ranges, each a
+            // GEMM task into its own partial (r x q), the partials are added
+            // to y_R in range order (deterministic)
+            std::vector<std::vector<GemmContrib>> cs(nsplit);
+            int64_t col = 0;
             for (int64_t e = sc.edge_begin; e < sc.edge_end; ++e) {
                 const SolveEdge& E = hb.edges[e];
-                cs.push_back(contrib(E.mat, E.ld, 0, yv + E.lo * q, q, 0, E.w));
+                for (int k0 = 0; k0 < E.w;) {
+                    const int part = int(col / SOLVE_GATHER_COLS);
+                    const int len = int(std::min<int64_t>(E.w - k0, (part + 1) * int64_t(SOLVE_GATHER_COLS) - col));
+                    cs[part].push_back(contrib(E.mat + k0, E.ld, 0, yv + (E.lo + k0) * q, q, 0, len));
+                    k0 += len;
+                    col += len;
+                }
             }
-            bgat.add(acc, q, r_, q, GEMM_STORE, cs.data(), cs.size());
-            badd.add(yc, q, r_, q, acc, q, 0, COPY_ADD);
+            if (int(badd.size()) < nsplit) badd.resize(nsplit);
+            for (int part = 0; part < nsplit; ++part) {
+                double* dst = acc + int64_t(part) * r_ * q;
+                bgat.add(dst, q, r_, q, GEMM_STORE, cs[part].data(), cs[part].size());
+                badd[part].add(yc, q, r_, q, dst, q, 0, COPY_ADD);
+            }
         }
         B.f_rot.build(P.mem, frot);
         B.f_prod.build(P.mem, fprod);
@@ -345,7 +362,8 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
         B.f_trsm.build(P.mem, ft, mr, tf);
         B.b_trsm.build(P.mem, bt, mr, tf);
         B.b_gather.build(P.mem, bgat);
-        B.b_add.build(P.mem, badd);
+        B.b_add.resize(badd.size());
+        for (size_t i = 0; i < badd.size(); ++i) B.b_add[i].build(P.mem, badd[i]);
         B.b_rot.build(P.mem, brot);
         B.b_copy.build(P.mem, bcopy);
         B.gemm = true;
@@ -433,8 +451,8 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
             if (B.gemm) {
                 B.f_rot.launch(K_SOLVE_FWD, st);
                 B.f_prod.launch(K_SOLVE_FWD, st);
-                B.f_trsm.launch(K_SOLVE_FWD, st);
-                B.f_copy.launch(K_SOLVE_FWD, st);
+                B.f_trsm.launch(K_TRSM, st);
+                B.f_copy.launch(K_COPY, st);
                 ProfScope ps(K_SOLVE_SCATTER, 0.0, B.sc_bytes);
                 launch_fwd_scatter(B.groups, B.ngroups, B.list, P.scratch, P.yv[li], nrhs, st);
                 continue;
@@ -463,11 +481,11 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
         for (size_t bi = L.batches.size(); bi-- > 0;) {
             auto& B = L.batches[bi];
             if (B.gemm) {
-                B.b_trsm.launch(K_SOLVE_BWD, st);
+                B.b_trsm.launch(K_TRSM, st);
                 B.b_gather.launch(K_SOLVE_BWD, st);
-                B.b_add.launch(K_SOLVE_BWD, st);
+                for (auto& a : B.b_add) a.launch(K_COPY, st);
                 B.b_rot.launch(K_SOLVE_BWD, st);
-                B.b_copy.launch(K_SOLVE_BWD, st);
+                B.b_copy.launch(K_COPY, st);
                 continue;
             }
             ProfScope ps(K_SOLVE_BWD, B.fwd_flops, B.fwd_bytes);

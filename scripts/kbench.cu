@@ -54,6 +54,8 @@ int main(int argc, char** argv) {
     const char* only = argc > 1 ? argv[1] : nullptr;
     std::vector<Case> cases = {
         {"schur_leaf_r13_47x47_x1", 8000, 47, 47, 1, 13, 1, 0},
+        {"schur_r10_64x64_x6", 8000, 64, 64, 6, 10, 1, 0},
+        {"schur_r8_48x48_x4", 8000, 48, 48, 4, 8, 1, 0},
         {"schur_r40_110x110_x2", 3000, 110, 110, 2, 40, 1, 0},
         {"schur_r150_300x300_x3", 60, 300, 300, 3, 150, 1, 0},
         {"schur_r60_120x120_x4", 400, 120, 120, 4, 60, 1, 0},

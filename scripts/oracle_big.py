@@ -10,10 +10,14 @@ from oracle import h2_oracle as O
 fam, n, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 over = {}
 perturb = 0.0
+pseed = 1
 for a in sys.argv[4:]:
     k, v = a.split('=')
     if k == "perturb":
         perturb = float(v)
+        continue
+    if k == "seed":
+        pseed = int(v)
         continue
     over[k] = float(v) if '.' in v or 'e' in v else int(v)
 t0 = time.perf_counter()
@@ -22,7 +26,7 @@ print("build", time.perf_counter() - t0, flush=True)
 if perturb:
     # rounding-level perturbation of the dense near field (a different draw of
     # the same algorithm on an operator equal to working precision)
-    rng = np.random.default_rng(1)
+    rng = np.random.default_rng(pseed)
     for key in sorted(h2.dense):
         blk = h2.dense[key]
         z = rng.standard_normal(blk.shape)
