@@ -116,55 +116,6 @@ __device__ __forceinline__ void stage_chunk(const GemmContrib& P, int M, int N, 
     else stage_any<true>(P.B, P.ldb, P.K, N, n0, k0, Bs);            // stored K x N: [k][n]
 }
 
-// Short contributions of a tile share one K chunk: up to GEMM_MAXSEG
-// segments (contribution, k offset, slot offset, length) fill the 32 k slots
-// back to back.  Only for the (transA, !transB) layout -- A stored K x M, B
-// stored K x N, both staged k-major -- which every Schur contribution has.
-constexpr int GEMM_MAXSEG = 4;
-struct Seg {
-    const double* A;
-    const double* B;
-    int64_t lda, ldb;
-    int k0, off;
-};
-
-template <bool VEC, bool ISB>
-__device__ __forceinline__ void stage_packed_op(const Seg* sg, int nseg, int total, int R, int r0, double* S) {
-    constexpr int W = VEC ? 2 : 1;
-    constexpr int PER_K = 64 / W;
-    constexpr int K_STEP = GEMM_THREADS / PER_K;
-    const int tid = threadIdx.x;
-    const int rc = (tid % PER_K) * W, kb = tid / PER_K;
-    const int rv = R - r0 - rc;
-    const int bytes = rv >= W ? 8 * W : (rv > 0 ? 8 * rv : 0);
-    double* dst = S + kb * LDM2 + rc;
-#pragma unroll
-    for (int i = 0; i < BK2 / K_STEP; ++i) {
-        const int k = kb + i * K_STEP;
-        int sidx = 0;
-#pragma unroll
-        for (int q = 1; q < GEMM_MAXSEG; ++q) sidx += (q < nseg && k >= sg[q].off);
-        const Seg& g = sg[sidx];
-        const double* X = ISB ? g.B : g.A;
-        const int64_t ld = ISB ? g.ldb : g.lda;
-        const double* src = X + (int64_t)(g.k0 + k - g.off) * ld + r0 + rc;
-        cp_async<8 * W>(dst + i * K_STEP * LDM2, src, k < total ? bytes : 0);
-    }
-}
-
-__device__ __forceinline__ void stage_packed(const Seg* sg, int nseg, int total, int M, int N, int m0, int n0,
-                                             double* As, double* Bs) {
-    bool va = true, vb = true;
-    for (int q = 0; q < nseg; ++q) {
-        va &= ((reinterpret_cast<uintptr_t>(sg[q].A) | (uintptr_t)(sg[q].lda * 8)) & 15) == 0;
-        vb &= ((reinterpret_cast<uintptr_t>(sg[q].B) | (uintptr_t)(sg[q].ldb * 8)) & 15) == 0;
-    }
-    if (va) stage_packed_op<true, false>(sg, nseg, total, M, m0, As);
-    else stage_packed_op<false, false>(sg, nseg, total, M, m0, As);
-    if (vb) stage_packed_op<true, true>(sg, nseg, total, N, n0, Bs);
-    else stage_packed_op<false, true>(sg, nseg, total, N, n0, Bs);
-}
-
 template <bool TA, bool TB>
 __device__ __forceinline__ void mma_kstep(const double* __restrict__ As, const double* __restrict__ Bs,
                                           double (&acc)[4][4][2], int wm, int wn, int g, int t, int kk) {
@@ -297,27 +248,14 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
             m.n0 = p_n0;
             m.local = p_local;
             const int len0 = min(BK2, P.K - p_pk);
-            int total = len0, nseg = 1;
-            Seg sg[GEMM_MAXSEG];
-            const bool packable = P.transA && !P.transB;
-            if (packable) sg[0] = Seg{P.A, P.B, P.lda, P.ldb, p_pk, 0};
+            const int total = len0;
+            stage_chunk(P, p_M, p_N, p_m0, p_n0, m.k0, As, As + STAGE_ELEMS);
             p_pk += len0;
             if (p_pk >= P.K) {
                 p_pk = 0;
                 ++p_pc;
                 while (p_pc < p_end && contribs[p_pc].K <= 0) ++p_pc;
-                // whole short contributions that follow ride in the same chunk
-                while (packable && nseg < GEMM_MAXSEG && p_pc < p_end) {
-                    const GemmContrib Q = contribs[p_pc];
-                    if (!(Q.transA && !Q.transB) || Q.K > BK2 - total) break;
-                    sg[nseg++] = Seg{Q.A, Q.B, Q.lda, Q.ldb, 0, total};
-                    total += Q.K;
-                    ++p_pc;
-                    while (p_pc < p_end && contribs[p_pc].K <= 0) ++p_pc;
-                }
             }
-            if (nseg > 1) stage_packed(sg, nseg, total, p_M, p_N, p_m0, p_n0, As, As + STAGE_ELEMS);
-            else stage_chunk(P, p_M, p_N, p_m0, p_n0, m.k0, As, As + STAGE_ELEMS);
             m.kv = total;
             m.last = p_pc >= p_end;
             if (m.last) {

@@ -193,7 +193,11 @@ __global__ void __launch_bounds__(ST)
 fwd_scatter_kernel(const ScatterGroup* __restrict__ groups, const int64_t* __restrict__ list,
                    const double* __restrict__ scratch, double* __restrict__ y, int nrhs) {
     const ScatterGroup G = groups[blockIdx.x];
-    for (int64_t e = threadIdx.x; e < (int64_t)G.w * nrhs; e += ST) {
+    // gridDim.y CTAs share a group's element range (multi-RHS blocks)
+    const int64_t tot = (int64_t)G.w * nrhs;
+    const int64_t per = (tot + gridDim.y - 1) / gridDim.y;
+    const int64_t e0 = (int64_t)blockIdx.y * per, e1 = min(tot, e0 + per);
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += ST) {
         double acc = y[G.lo * nrhs + e];
         for (int64_t l = G.begin; l < G.end; ++l) acc += scratch[list[l] * nrhs + e];
         y[G.lo * nrhs + e] = acc;
@@ -296,9 +300,9 @@ void launch_solve_tasks(const SolveTask* d_tasks, int32_t ntasks, const SolveClu
 }
 
 void launch_fwd_scatter(const ScatterGroup* d_groups, int32_t ngroups, const int64_t* d_list,
-                        const double* scratch, double* y, int32_t nrhs, cudaStream_t st) {
+                        const double* scratch, double* y, int32_t nrhs, cudaStream_t st, int32_t ysplit) {
     if (ngroups <= 0) return;
-    fwd_scatter_kernel<<<ngroups, ST, 0, st>>>(d_groups, d_list, scratch, y, nrhs);
+    fwd_scatter_kernel<<<dim3(ngroups, max(1, ysplit)), ST, 0, st>>>(d_groups, d_list, scratch, y, nrhs);
     count_launch();
 }
 

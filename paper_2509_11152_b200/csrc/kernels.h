@@ -315,7 +315,7 @@ void launch_solve_tasks(const SolveTask* d_tasks, int32_t ntasks, const SolveClu
                         const SolveEdge* d_edges, double* y, double* scratch, double* work, int32_t nrhs,
                         cudaStream_t st);
 void launch_fwd_scatter(const ScatterGroup* d_groups, int32_t ngroups, const int64_t* d_list,
-                        const double* scratch, double* y, int32_t nrhs, cudaStream_t st);
+                        const double* scratch, double* y, int32_t nrhs, cudaStream_t st, int32_t ysplit = 1);
 void launch_gather_rows(const double* src, const int64_t* idx, int64_t n, int32_t nrhs,
                         double* dst, cudaStream_t st);
 void launch_scatter_rows(const double* src, const int64_t* idx, int64_t n, int32_t nrhs,

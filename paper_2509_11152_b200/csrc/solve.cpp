@@ -117,6 +117,7 @@ struct SolvePlan {
         DevCopy f_copy, b_copy;
         std::vector<DevCopy> b_add;  // one launch per split-K partial of the gather
         DevTrsm f_trsm, b_trsm;
+        int32_t scatter_split = 1;  // CTAs per scatter group (multi-RHS)
     };
     struct Level {
         int64_t total = 0;
@@ -264,6 +265,11 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
             B.cl = to_dev(P.mem, cls);
             B.edges = to_dev(P.mem, edges);
             B.ngroups = int32_t(gs.size());
+            {
+                int64_t wmax = 1;
+                for (auto& g : gs) wmax = std::max<int64_t>(wmax, g.w);
+                B.scatter_split = int32_t(std::min<int64_t>(64, cdiv(wmax * nrhs, 4096)));
+            }
             B.groups = to_dev(P.mem, gs);
             B.list = to_dev(P.mem, list);
             for (int q = 0; q < 4; ++q) {
@@ -454,7 +460,7 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
                 B.f_trsm.launch(K_TRSM, st);
                 B.f_copy.launch(K_COPY, st);
                 ProfScope ps(K_SOLVE_SCATTER, 0.0, B.sc_bytes);
-                launch_fwd_scatter(B.groups, B.ngroups, B.list, P.scratch, P.yv[li], nrhs, st);
+                launch_fwd_scatter(B.groups, B.ngroups, B.list, P.scratch, P.yv[li], nrhs, st, B.scatter_split);
                 continue;
             }
             {
