@@ -188,29 +188,38 @@ hh_panel_kernel(const HhPanelTask* __restrict__ tasks, const int32_t* __restrict
 }
 
 // out[a][c] = sum_b op(T)[a][b] * (sum_ch P[ch][b][c]),  op(T) = T^T (trans) or T
-__global__ void hh_tmul_kernel(const HhTmulTask* __restrict__ tasks) {
+// 32 columns per CTA, 8 row-threads: the split-K partial sums of the 32 x 32
+// block S are formed with independent loads (4 rows per thread), then T (or
+// T^T) is applied from shared memory
+constexpr int TM_COLS = 32, TM_ROWS = 8;
+__global__ void __launch_bounds__(TM_COLS * TM_ROWS) hh_tmul_kernel(const HhTmulTask* __restrict__ tasks) {
     const HhTmulTask R = tasks[blockIdx.y];
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= R.ncols) return;
-    double S[HH_NB];
+    __shared__ double Ssh[HH_NB][TM_COLS + 1];
+    __shared__ double Tsh[HH_NB][HH_NB + 1];
+    const int cx = threadIdx.x % TM_COLS, ty = threadIdx.x / TM_COLS;
+    const int c0 = blockIdx.x * TM_COLS;
+    if (c0 >= R.ncols) return;
+    const int c = c0 + cx;
+    for (int e = threadIdx.x; e < HH_NB * HH_NB; e += TM_COLS * TM_ROWS) Tsh[e / HH_NB][e % HH_NB] = R.T[e];
 #pragma unroll
-    for (int b = 0; b < HH_NB; ++b) S[b] = 0.0;
-    for (int ch = 0; ch < R.nchunks; ++ch) {
-        const double* P = R.P + (int64_t)ch * R.nrows * R.ncols;
-#pragma unroll
-        for (int b = 0; b < HH_NB; ++b)
-            if (b < R.nrows) S[b] += P[(int64_t)b * R.ncols + c];
+    for (int q = 0; q < HH_NB / TM_ROWS; ++q) {
+        const int b = ty + q * TM_ROWS;
+        double v = 0.0;
+        if (c < R.ncols && b < R.nrows)
+            for (int ch = 0; ch < R.nchunks; ++ch) v += R.P[((int64_t)ch * R.nrows + b) * R.ncols + c];
+        Ssh[b][cx] = v;
     }
+    __syncthreads();
+    if (c >= R.ncols) return;
 #pragma unroll
-    for (int a = 0; a < HH_NB; ++a) {
-        if (a >= R.nrows) break;
+    for (int q = 0; q < HH_NB / TM_ROWS; ++q) {
+        const int a = ty + q * TM_ROWS;
+        if (a >= R.nrows) continue;
         double acc = 0.0;
         if (R.trans) {
-#pragma unroll
-            for (int b = 0; b <= a; ++b) acc += R.T[b * HH_NB + a] * S[b];
+            for (int b = 0; b <= a; ++b) acc += Tsh[b][a] * Ssh[b][cx];
         } else {
-#pragma unroll
-            for (int b = a; b < HH_NB; ++b) acc += R.T[a * HH_NB + b] * S[b];
+            for (int b = a; b < HH_NB; ++b) acc += Tsh[a][b] * Ssh[b][cx];
         }
         R.out[(int64_t)a * R.ncols + c] = acc;
     }
@@ -255,8 +264,8 @@ cudaError_t launch_hh_panel(const HhPanelTask* d_tasks, const int32_t* d_cta_tas
 
 void launch_hh_tmul(const HhTmulTask* d_tasks, int32_t ntasks, int32_t max_cols, cudaStream_t st) {
     if (ntasks <= 0 || max_cols <= 0) return;
-    dim3 grid((max_cols + 127) / 128, ntasks);
-    hh_tmul_kernel<<<grid, 128, 0, st>>>(d_tasks);
+    dim3 grid((max_cols + TM_COLS - 1) / TM_COLS, ntasks);
+    hh_tmul_kernel<<<grid, TM_COLS * TM_ROWS, 0, st>>>(d_tasks);
     count_launch();
 }
 
