@@ -367,16 +367,17 @@ __global__ void r_extract_kernel(const RExtractTask* __restrict__ tasks) {
 __device__ __forceinline__ void cta_group_barrier(uint32_t* bar, int nct) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile uint32_t* gen = bar + 1;
-        const uint32_t g = *gen;
+        // monotonic arrival counter (zeroed before the launch): the k-th
+        // barrier completes when the counter reaches k * n -- one release
+        // atomic per CTA, acquire polling, no reset round trip
         __threadfence();
-        if (atomicAdd(bar, 1u) == uint32_t(nct - 1)) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g) __nanosleep(20);
-        }
+        uint32_t old;
+        asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+        const uint32_t target = (old / uint32_t(nct) + 1u) * uint32_t(nct);
+        uint32_t cur;
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+        } while (int32_t(cur - target) < 0);
         __threadfence();
     }
     __syncthreads();

@@ -37,16 +37,17 @@ __device__ __forceinline__ void hh_reflector(double alpha, double ss, double& be
 __device__ __forceinline__ void group_barrier(uint32_t* bar, int n) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile uint32_t* gen = bar + 1;
-        const uint32_t g = *gen;
+        // monotonic arrival counter (zeroed before the launch): the k-th
+        // barrier completes when the counter reaches k * n -- one release
+        // atomic per CTA, acquire polling, no reset round trip
         __threadfence();
-        if (atomicAdd(bar, 1u) == uint32_t(n - 1)) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g) __nanosleep(20);
-        }
+        uint32_t old;
+        asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+        const uint32_t target = (old / uint32_t(n) + 1u) * uint32_t(n);
+        uint32_t cur;
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+        } while (int32_t(cur - target) < 0);
         __threadfence();
     }
     __syncthreads();

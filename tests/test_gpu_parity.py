@@ -284,3 +284,17 @@ def test_solve_multi_block_path_matches_single_vector_path(case, q):
         Xo = O.substitute(of, B[:, :3])
     if case.startswith("cov2d"):
         assert np.linalg.norm(X[:, :3] - Xo) <= 1e-8 * np.linalg.norm(Xo)
+
+
+def test_device_harness_report_matches_reference_schema():
+    """The device harness (reference harness.run, harness.py:197-249) returns
+    the reference report keys; e_b and the digest follow the GPU path."""
+    from paper_2509_11152_b200.harness import run
+
+    rep = run("cov2d", 1024)
+    for key in ["version", "config", "n", "e_b", "solution_digest", "h2_bytes", "factor_bytes",
+                "kmax_construction", "kmax_factorization", "csp_max", "timings", "phases", "levels", "ranks"]:
+        assert key in rep
+    assert rep["n"] == 1024 and rep["e_b"] <= 1e-10
+    assert set(["factorization", "solve"]) <= set(rep["timings"])
+    assert "partial_lu" in rep["phases"] and len(rep["levels"]) == len(rep["ranks"])
