@@ -1038,25 +1038,47 @@ __global__ void row_swaps_kernel(double* A, int64_t lda, int ncols, int k0, int 
 }
 
 // A[k0:k0+nb, c0:c0+ncols] = L11^-1 A[...]  (L11 unit lower of the panel)
-__global__ void trsm_unit_lower_rows_kernel(double* A, int64_t lda, int k0, int nb, int c0, int ncols) {
+// X = L11^-1 X for the nb (<= TOP_PANEL_NB) panel rows of columns [c0, c0+ncols):
+// L11 staged once per CTA in shared memory, the column's nb values in
+// registers (fully unrolled), one thread per column
+__global__ void __launch_bounds__(256) trsm_unit_lower_rows_kernel(double* A, int64_t lda, int k0, int nb, int c0,
+                                                                   int ncols) {
+    __shared__ double Ls[TOP_PANEL_NB][TOP_PANEL_NB + 1];
+    for (int e = threadIdx.x; e < TOP_PANEL_NB * TOP_PANEL_NB; e += blockDim.x) {
+        const int i = e / TOP_PANEL_NB, k = e % TOP_PANEL_NB;
+        Ls[i][k] = (i < nb && k < i) ? A[(int64_t)(k0 + i) * lda + k0 + k] : 0.0;
+    }
+    __syncthreads();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= ncols) return;
-    double* x = A + c0 + j;
-    for (int i = 1; i < nb; ++i) {
-        const double* li = A + (int64_t)(k0 + i) * lda + k0;
-        double acc = x[(int64_t)(k0 + i) * lda];
-        for (int k = 0; k < i; ++k) acc -= li[k] * x[(int64_t)(k0 + k) * lda];
-        x[(int64_t)(k0 + i) * lda] = acc;
+    double* x = A + (int64_t)k0 * lda + c0 + j;
+    double v[TOP_PANEL_NB];
+#pragma unroll
+    for (int i = 0; i < TOP_PANEL_NB; ++i) v[i] = i < nb ? x[(int64_t)i * lda] : 0.0;
+#pragma unroll
+    for (int i = 1; i < TOP_PANEL_NB; ++i) {
+        double acc = v[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) acc -= Ls[i][k] * v[k];
+        v[i] = acc;
     }
+#pragma unroll
+    for (int i = 1; i < TOP_PANEL_NB; ++i)
+        if (i < nb) x[(int64_t)i * lda] = v[i];
 }
 
+// max |A| over all CTAs: per-CTA block max, then an integer atomicMax on the
+// bit pattern (monotone for non-negative doubles, so the result is exact
+// and order independent); *out must be 0 before the launch
 __global__ void absmax_kernel(const double* A, int64_t lda, int rows, int cols, double* out) {
     __shared__ double sh[32];
     double m = 0.0;
-    for (int64_t e = threadIdx.x; e < (int64_t)rows * cols; e += blockDim.x)
+    const int64_t tot = (int64_t)rows * cols;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x)
         m = fmax(m, fabs(A[(e / cols) * lda + (e % cols)]));
     m = block_max(m, sh);
-    if (threadIdx.x == 0) *out = m;
+    if (threadIdx.x == 0)
+        atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__double_as_longlong(m));
 }
 
 __global__ void diag_absmin_kernel(const double* A, int64_t lda, int n, double* out) {
@@ -1269,14 +1291,17 @@ void launch_row_swaps(double* A, int64_t lda, int32_t ncols_total, int32_t k0, i
 void launch_trsm_unit_lower_rows(const double* A, int64_t lda, int32_t k0, int32_t nb, int32_t c0,
                                  int32_t ncols, cudaStream_t st) {
     if (ncols <= 0) return;
-    trsm_unit_lower_rows_kernel<<<(ncols + 127) / 128, 128, 0, st>>>(const_cast<double*>(A), lda, k0,
+    trsm_unit_lower_rows_kernel<<<(ncols + 255) / 256, 256, 0, st>>>(const_cast<double*>(A), lda, k0,
                                                                       nb, c0, ncols);
     count_launch();
 }
 
 void launch_absmax(const double* A, int64_t lda, int32_t rows, int32_t cols, double* out,
                    cudaStream_t st) {
-    absmax_kernel<<<1, 1024, 0, st>>>(A, lda, rows, cols, out);
+    cudaMemsetAsync(out, 0, sizeof(double), st);
+    const int64_t tot = int64_t(rows) * cols;
+    const int grid = int(std::min<int64_t>(148 * 4, std::max<int64_t>(1, (tot + 1023) / 1024)));
+    absmax_kernel<<<grid, 1024, 0, st>>>(A, lda, rows, cols, out);
     count_launch();
 }
 
