@@ -10,8 +10,13 @@ import paper_2509_11152_b200 as H
 
 fam, n, ndraws = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 over = {}
+SAVE = set()
 for a in sys.argv[4:]:
-    k, v = a.split('='); over[k] = float(v) if '.' in v or 'e' in v else int(v)
+    k, v = a.split('=')
+    if k == "save":
+        SAVE = {int(t) for t in v.split(',')}
+        continue
+    over[k] = float(v) if '.' in v or 'e' in v else int(v)
 tree, part, spec, h2, prm = H.build_problem(fam, n, **over)
 x_ref = np.random.Generator(np.random.Philox(7)).standard_normal(n)
 for d in range(ndraws):
@@ -37,5 +42,15 @@ for d in range(ndraws):
     eb = float(np.linalg.norm(H.matvec(h2p, x) - b) / np.linalg.norm(b))
     print(json.dumps({"draw": d, "perturb": 0.0 if d == 0 else 1e-14, "fact_s": round(tf, 2), "e_b_raw": eb0,
                       "e_b": eb, "levels": [[r.level, r.nbatches, r.max_rank] for r in fac.records]}), flush=True)
+    if d in SAVE:
+        save = {"x": x, "x0": x0}
+        for rec in fac.records:
+            cl = list(rec.clusters)
+            save[f"L{rec.level}_clusters"] = np.array(cl)
+            save[f"L{rec.level}_size"] = np.array([rec.size[c] for c in cl])
+            save[f"L{rec.level}_r"] = np.array([rec.factors[c].r for c in cl])
+            save[f"L{rec.level}_batches"] = np.concatenate([np.array(bb) for bb in rec.batches])
+            save[f"L{rec.level}_blen"] = np.array([len(bb) for bb in rec.batches])
+        np.savez(f"gpurun_out/draw{d}_structure.npz", **save)
     del fac, h2p
     gc.collect()
