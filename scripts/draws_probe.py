@@ -11,15 +11,19 @@ import paper_2509_11152_b200 as H
 fam, n, ndraws = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 over = {}
 SAVE = set()
+FIRST = 0
 for a in sys.argv[4:]:
     k, v = a.split('=')
+    if k == "first":
+        FIRST = int(v)
+        continue
     if k == "save":
         SAVE = {int(t) for t in v.split(',')}
         continue
     over[k] = float(v) if '.' in v or 'e' in v else int(v)
 tree, part, spec, h2, prm = H.build_problem(fam, n, **over)
 x_ref = np.random.Generator(np.random.Philox(7)).standard_normal(n)
-for d in range(ndraws):
+for d in range(FIRST, ndraws):
     h2p = copy.copy(h2)
     object.__setattr__(h2p, "_h2f_device", None)
     if d > 0:
