@@ -425,6 +425,10 @@ def h2_bytes(h2):
     return sum(b.nbytes for s in (h2.leaf_basis, h2.transfer, h2.coupling, h2.dense) for b in s.values())
 
 
+TRAFFIC_NOTE = ("null: Schur GEMM launches differ 100x in size, so one ncu capture gives no per-launch average; "
+                "dram bytes of 4 captured launches are in profiles/r01_ncu_gemm_config2.txt")
+
+
 def roofline(prof, peaks, peak_kind, dmma_tf):
     """Dominant kernel (most device time) against its bound."""
     if not prof:
@@ -438,12 +442,12 @@ def roofline(prof, peaks, peak_kind, dmma_tf):
     if ai >= ridge:
         achieved = p["flops"] / p["seconds"] / 1e12
         return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": dmma_tf, "unit": "TFLOP/s",
-                "frac": achieved / dmma_tf, "traffic": None,
+                "frac": achieved / dmma_tf, "traffic": None, "traffic_note": TRAFFIC_NOTE,
                 "peak_source": "FP64 DMMA m8n8k4 peak measured in this run (MEASURED_PEAKS.json has no FP64)",
                 "launches": p["launches"], "seconds": p["seconds"]}
     achieved = p["bytes"] / p["seconds"] / 1e9
     return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "peak_source": f"{peak_kind} hbm_gbs",
+            "frac": achieved / hbm, "traffic": None, "traffic_note": TRAFFIC_NOTE, "peak_source": f"{peak_kind} hbm_gbs",
             "launches": p["launches"], "seconds": p["seconds"]}
 
 
