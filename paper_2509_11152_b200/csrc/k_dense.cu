@@ -177,6 +177,7 @@ __device__ void jacobi_sweeps(double* A, int m, int n, int* flag, double* nrm) {
                 if (p >= m || q >= m) continue;
                 double a = nrm[p], b = nrm[q];
                 if (jac_rotate_cached(A + (int64_t)p * n, A + (int64_t)q * n, n, tol, a, b)) {
+                    __syncwarp();  // every lane has read nrm[p], nrm[q] before lane 0 rewrites them
                     if (lane == 0) {
                         nrm[p] = a;
                         nrm[q] = b;
