@@ -179,6 +179,13 @@ int h2f_factor_level_info(h2f_factor f, int32_t rec, h2f_level_info* info);
 int h2f_factor_level_arrays(h2f_factor f, int32_t rec, int64_t* clusters, int64_t* offsets,
                             int64_t* sizes, int64_t* batch_ptr, int64_t* batch_ids,
                             int64_t* up_index);
+/* fill keys of record rec (factorization.py:502-505, 573-588): the canonical
+ * pairs present when the level started, init_pairs [num_init][2], and every
+ * block created by the level's batches in creation order, created
+ * [num_created][3] = (batch index, a, b).  Call with NULL arrays for the
+ * counts. */
+int h2f_factor_level_fills(h2f_factor f, int32_t rec, int64_t* num_init, int64_t* init_pairs,
+                           int64_t* num_created, int64_t* created);
 int h2f_factor_cluster_info(h2f_factor f, int32_t rec, int32_t cluster, h2f_cluster_info* ci);
 /* q: s*s row-major; lu: r*r row-major; piv: r (0-based LAPACK swaps);
  * edge_other/kind [num_edges] (kind 0 self, 1 full, 2 skel), edge_width [num_edges] */
@@ -195,6 +202,21 @@ int h2f_factor_top(h2f_factor f, double* top_lu, int32_t* top_piv);
 int h2f_greedy_coloring(int64_t num_clusters, const int64_t* clusters, int64_t num_pairs,
                         const int64_t* pairs, int32_t* colors_out, int32_t* num_colors,
                         int32_t* max_degree);
+
+/* ---- structure replay (parity diagnostics) ----------------------------------
+ * Replaces this library's threshold decisions by those of another run (the
+ * CPU oracle) for every later h2f_factorize until cleared:
+ *   kept_rows    [nkept][3]     (level, cluster, kept)   factorization.py:80
+ *   created_rows [ncreated][4]  (level, creating cluster, a, b) for every
+ *                               fill block the run created  factorization.py:502-505
+ * With identical decisions the batches, ranks and fill pattern coincide, so
+ * the solutions differ only by floating-point rounding.  stats: number of
+ * kept counts taken from the table, fill decisions that differ from this
+ * run's own norm test. */
+int h2f_debug_replay_set(const int64_t* kept_rows, int64_t nkept, const int64_t* created_rows,
+                         int64_t ncreated);
+int h2f_debug_replay_clear(void);
+int h2f_debug_replay_stats(int64_t* kept_forced, int64_t* fill_changed);
 
 #ifdef __cplusplus
 }

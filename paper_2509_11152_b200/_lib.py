@@ -96,16 +96,21 @@ _SIGS = {
     "h2f_factor_info_get": (C.c_int, [C.c_void_p, C.POINTER(FactorInfo)]),
     "h2f_factor_level_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(LevelInfo)]),
     "h2f_factor_level_arrays": (C.c_int, [C.c_void_p, C.c_int32, i64p, i64p, i64p, i64p, i64p, i64p]),
+    "h2f_factor_level_fills": (C.c_int, [C.c_void_p, C.c_int32, i64p, i64p, i64p, i64p]),
     "h2f_factor_cluster_info": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(ClusterInfo)]),
     "h2f_factor_cluster_arrays": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, f64p, f64p, i32p, i64p,
                                             i32p, i64p]),
     "h2f_factor_cluster_edge": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, f64p]),
     "h2f_factor_top": (C.c_int, [C.c_void_p, f64p, i32p]),
     "h2f_greedy_coloring": (C.c_int, [C.c_int64, i64p, C.c_int64, i64p, i32p, i32p, i32p]),
+    "h2f_debug_replay_set": (C.c_int, [i64p, C.c_int64, i64p, C.c_int64]),
+    "h2f_debug_replay_clear": (C.c_int, []),
+    "h2f_debug_replay_stats": (C.c_int, [i64p, i64p]),
 }
 
 _lib = None
 _initialised = False
+_device = None
 
 
 class H2FError(RuntimeError):
@@ -152,14 +157,26 @@ def check(code, what=""):
 
 
 def ensure_init(device=None):
-    """Create the library's CUDA context (once per process)."""
-    global _initialised
+    """Create the library's CUDA context (once per process).
+
+    Device: the argument, else H2F_DEVICE, else LOCAL_RANK (one process per
+    GPU under torchrun), else 0."""
+    global _initialised, _device
     if not _initialised:
-        dev = int(os.environ.get("H2F_DEVICE", "0")) if device is None else device
+        if device is None:
+            device = int(os.environ.get("H2F_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+        dev = int(device)
         arena = float(os.environ.get("H2F_ARENA_GB", "0"))
         check(lib().h2f_init(dev, arena), "h2f_init")
         _initialised = True
+        _device = dev
     return lib()
+
+
+def device():
+    """CUDA ordinal the library context lives on (initialises it)."""
+    ensure_init()
+    return _device
 
 
 def ptr(a, typ=f64p):
@@ -251,3 +268,23 @@ def dense_complement(BT, path):
     ms = C.c_double()
     check(ensure_init().h2f_dense_complement(ptr(BT), s, kt, int(path), ptr(Q), C.byref(ms)))
     return Q, ms.value
+
+
+# ---- structure replay (parity diagnostics) ----------------------------------
+
+def replay_set(kept_rows, created_rows):
+    """Force the threshold decisions of another run: kept_rows (k, 3) =
+    (level, cluster, kept), created_rows (f, 4) = (level, creator, a, b)."""
+    k = as_i64(np.asarray(kept_rows).reshape(-1, 3))
+    f = as_i64(np.asarray(created_rows).reshape(-1, 4))
+    check(ensure_init().h2f_debug_replay_set(ptr(k, i64p), k.shape[0], ptr(f, i64p), f.shape[0]))
+
+
+def replay_clear():
+    check(ensure_init().h2f_debug_replay_clear())
+
+
+def replay_stats():
+    a, b = C.c_int64(), C.c_int64()
+    check(ensure_init().h2f_debug_replay_stats(C.byref(a), C.byref(b)))
+    return {"kept_forced": a.value, "fill_changed": b.value}

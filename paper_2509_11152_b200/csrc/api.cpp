@@ -2,6 +2,7 @@
 // converts h2f::Error / std::exception into a status code + h2f_last_error().
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -22,8 +23,37 @@ namespace {
 
 thread_local std::string g_err;
 
+// One context (arena, upload ring, plan cache, profiler) per process: every
+// entry point runs under this lock, so concurrent callers (ctypes releases the
+// GIL) serialise instead of racing on the host allocator state -- concurrent
+// solves are safe as the reference promises.  Recursive because
+// entry points may call each other.  The calling thread is also bound to the
+// context's device, whatever cudaSetDevice it did itself.
+std::recursive_mutex g_lock;
+
+void bind_device() {
+    if (ctx_ready()) H2F_CUDA(cudaSetDevice(ctx().device));
+}
+
+// a *_dev pointer must be device memory of the context's device
+void check_dev_ptr(const void* p, const char* what) {
+    if (!p) throw Error(H2F_E_ARG, std::string(what) + ": null device pointer");
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        throw Error(H2F_E_ARG, std::string(what) + ": not a CUDA pointer");
+    }
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+        throw Error(H2F_E_ARG, std::string(what) + ": host pointer passed to a _dev entry point");
+    if (a.device != ctx().device)
+        throw Error(H2F_E_ARG, std::string(what) + ": pointer on device " + std::to_string(a.device) +
+                                   ", library context on device " + std::to_string(ctx().device));
+}
+
 template <class Fn> int guard(Fn&& fn) {
+    std::lock_guard<std::recursive_mutex> hold(g_lock);
     try {
+        bind_device();
         fn();
         return H2F_OK;
     } catch (const Error& e) {
@@ -247,6 +277,8 @@ int h2f_matrix_nbytes(h2f_matrix m, int64_t* bytes) {
 int h2f_matvec_dev(h2f_matrix m, const double* x_dev, double* y_dev, int64_t nrhs) {
     return guard([&] {
         if (nrhs < 1) throw Error(H2F_E_ARG, "nrhs must be >= 1");
+        check_dev_ptr(x_dev, "x_dev");
+        check_dev_ptr(y_dev, "y_dev");
         matvec_device(*m->m, x_dev, y_dev, int(nrhs));
         ctx().sync();
     });
@@ -270,8 +302,10 @@ int h2f_norm2(h2f_matrix m, const double* v0, int32_t iters, double* est) {
 
 int h2f_factorize(h2f_matrix m, double eps_lu, double norm_estimate, const double* v0, h2f_factor* out,
                   h2f_status* status) {
+    std::lock_guard<std::recursive_mutex> hold(g_lock);
     if (status) *status = {H2F_OK, -1, -1};
     try {
+        bind_device();
         Factorization* f = factorize(*m->m, eps_lu, norm_estimate, v0);
         *out = new h2f_factor_s{f};
         return H2F_OK;
@@ -302,6 +336,8 @@ int h2f_factor_destroy(h2f_factor f) {
 int h2f_solve_dev(h2f_factor f, const double* b_dev, double* x_dev, int64_t nrhs) {
     return guard([&] {
         if (nrhs < 1) throw Error(H2F_E_ARG, "nrhs must be >= 1");
+        check_dev_ptr(b_dev, "b_dev");
+        check_dev_ptr(x_dev, "x_dev");
         solve_device(*f->f, b_dev, x_dev, int(nrhs));
         ctx().sync();
     });
@@ -321,6 +357,8 @@ int h2f_solve(h2f_factor f, const double* b, double* x, int64_t nrhs) {
 
 int h2f_refined_solve_dev(h2f_matrix m, h2f_factor f, const double* b_dev, double* x_dev, int32_t steps) {
     return guard([&] {
+        check_dev_ptr(b_dev, "b_dev");
+        check_dev_ptr(x_dev, "x_dev");
         refined_solve_device(*m->m, *f->f, b_dev, x_dev, steps);
         ctx().sync();
     });
@@ -393,6 +431,30 @@ int h2f_factor_level_arrays(h2f_factor f, int32_t rec, int64_t* clusters, int64_
     });
 }
 
+int h2f_factor_level_fills(h2f_factor f, int32_t rec, int64_t* num_init, int64_t* init_pairs,
+                           int64_t* num_created, int64_t* created) {
+    return guard([&] {
+        const LevelRecord& r = rec_at(f, rec);
+        if (num_init) *num_init = int64_t(r.fill_init.size());
+        if (init_pairs)
+            for (size_t i = 0; i < r.fill_init.size(); ++i) {
+                init_pairs[2 * i] = key_a(r.fill_init[i]);
+                init_pairs[2 * i + 1] = key_b(r.fill_init[i]);
+            }
+        int64_t k = 0;
+        for (size_t b = 0; b < r.fill_created.size(); ++b)
+            for (Key key : r.fill_created[b]) {
+                if (created) {
+                    created[3 * k] = int64_t(b);
+                    created[3 * k + 1] = key_a(key);
+                    created[3 * k + 2] = key_b(key);
+                }
+                ++k;
+            }
+        if (num_created) *num_created = k;
+    });
+}
+
 int h2f_factor_cluster_info(h2f_factor f, int32_t rec, int32_t cluster, h2f_cluster_info* ci) {
     return guard([&] {
         const ClusterFactor& c = cf_at(f, rec, cluster);
@@ -439,6 +501,33 @@ int h2f_factor_top(h2f_factor f, double* top_lu, int32_t* top_piv) {
         if (top_lu) d2h(top_lu, F.top_lu, sizeof(double) * F.top_size * F.top_size);
         if (top_piv) d2h(top_piv, F.top_piv, sizeof(int32_t) * F.top_size);
         ctx().sync();
+    });
+}
+
+int h2f_debug_replay_set(const int64_t* kept_rows, int64_t nkept, const int64_t* created_rows, int64_t ncreated) {
+    return guard([&] {
+        Replay& R = replay();
+        R = Replay{};
+        for (int64_t i = 0; i < nkept; ++i) {
+            const int64_t* r = kept_rows + 3 * i;
+            R.kept[(r[0] << 32) | uint32_t(r[1])] = int(r[2]);
+        }
+        for (int64_t i = 0; i < ncreated; ++i) {
+            const int64_t* r = created_rows + 4 * i;
+            R.created[(r[0] << 32) | uint32_t(r[1])].push_back(canon(int(r[2]), int(r[3])));
+        }
+        R.active = true;
+    });
+}
+
+int h2f_debug_replay_clear(void) {
+    return guard([&] { replay() = Replay{}; });
+}
+
+int h2f_debug_replay_stats(int64_t* kept_forced, int64_t* fill_changed) {
+    return guard([&] {
+        *kept_forced = replay().kept_forced;
+        *fill_changed = replay().fill_changed;
     });
 }
 

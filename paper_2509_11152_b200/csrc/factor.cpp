@@ -30,6 +30,11 @@
 
 namespace h2f {
 
+Replay& replay() {
+    static Replay r;
+    return r;
+}
+
 namespace {
 
 constexpr double PIVOT_RTOL = 1e-14;      // factorization.py:47
@@ -97,6 +102,8 @@ struct Lvl {
     std::vector<TransferW> T;
     Region mem{size_t(256) << 20};
     std::vector<std::vector<int>> batches;
+    std::vector<Key> fill_init;
+    std::vector<std::vector<Key>> fill_created;
     std::vector<ClusterFactor> factors;
 
     int at(int c) const { return pos.at(c); }
@@ -330,6 +337,9 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         std::vector<QrTask> qr_small, qr_big, qr_seg;
         std::vector<SvdTask> svd_small, svd_big;
         int max_n_small = 1;
+        // under a structure replay every singular vector is written (sorted)
+        // and the kept count comes from the replayed run
+        const double svd_thresh = replay().active ? -1.0 : drop;
         // H2F_SMALL_N_MAX (tests) lowers the shared-memory QR/SVD cut-off so
         // the large-n (blocked QR, multi-CTA Jacobi) path runs on small inputs
         int small_n_max = SMEM_DENSE_MAX_N;
@@ -449,13 +459,13 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             double f = 0, b = 0;
             svd_work(svd_small, f, b);
             ProfScope ps(K_JACOBI, f, b);
-            launch_jacobi_smem(upload(svd_small), int32_t(svd_small.size()), max_n_small, drop, st);
+            launch_jacobi_smem(upload(svd_small), int32_t(svd_small.size()), max_n_small, svd_thresh, st);
         }
         if (!svd_big.empty()) {
             double f = 0, b = 0;
             svd_work(svd_big, f, b);
             ProfScope ps(K_JACOBI_BIG, f, b);
-            jacobi_multi_cta(svd_big, drop, scr);
+            jacobi_multi_cta(svd_big, svd_thresh, scr);
         }
     }
     int* kept_h = static_cast<int*>(X.pinned_buf(sizeof(int) * nb));
@@ -464,6 +474,20 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     X.sync();
     tick(HT_SYNC1);
     std::vector<int> kept(kept_h, kept_h + nb);
+    if (replay().active) {
+        Replay& R = replay();
+        for (int bi = 0; bi < nb; ++bi) {
+            if (aug[bi].skip) continue;
+            auto it = R.kept.find((int64_t(L.level) << 32) | uint32_t(batch[bi]));
+            if (it == R.kept.end())
+                throw Error(H2F_E_ARG, "replay: no kept count for cluster " + std::to_string(batch[bi]) +
+                                           " at level " + std::to_string(L.level));
+            if (it->second > std::min(aug[bi].n, aug[bi].wf))
+                throw Error(H2F_E_ARG, "replay: kept count exceeds the fill rank bound");
+            ++R.kept_forced;
+            kept[bi] = it->second;
+        }
+    }
     if (aug_log) {
         for (int bi = 0; bi < nb; ++bi)
             std::fprintf(aug_log, "%d %d %d %d %d %d %d %d\n", L.level, batch_counter, nb, aug[bi].s, aug[bi].k,
@@ -710,6 +734,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     };
     struct Cand {
         Key key;
+        int creator;
         int M, N;
         GemmContrib g;
         int64_t base, ntiles;
@@ -792,6 +817,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             if (u.M <= 0 || u.N <= 0) continue;
             Cand cd;
             cd.key = mkkey(e.ids[u.i], e.ids[u.j]);
+            cd.creator = e.c;
             cd.M = u.M;
             cd.N = u.N;
             cd.g = contrib(e.G + e.offs[u.i], e.W, 1, e.MW + e.offs[u.j], e.W, 0, e.r);
@@ -942,11 +968,21 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 news[it->second].cs.push_back(cd.g);
                 continue;
             }
-            if (std::sqrt(ss_h[i]) > drop) {
+            bool create_it = std::sqrt(ss_h[i]) > drop;
+            if (replay().active) {
+                Replay& R = replay();
+                auto rt = R.created.find((int64_t(L.level) << 32) | uint32_t(cd.creator));
+                const bool want = rt != R.created.end() &&
+                                  std::find(rt->second.begin(), rt->second.end(), cd.key) != rt->second.end();
+                R.fill_changed += want != create_it;
+                create_it = want;
+            }
+            if (create_it) {
                 double* blk = L.mem.alloc_n<double>(int64_t(cd.M) * cd.N);
                 L.F[cd.key] = View{blk, cd.N, cd.M, cd.N};
                 L.link(cd.key, false);
                 made[cd.key] = int(news.size());
+                L.fill_created.back().push_back(cd.key);
                 news.push_back({blk, cd.N, cd.M, cd.N, {cd.g}});
             }
         }
@@ -1201,6 +1237,8 @@ void Factorizer::run(double norm_estimate, const double* v0) {
             if (!L) L = leaf_level(level);
             for (size_t i = 0; i < L->clusters.size(); ++i) L->live[i] = int(L->size[i]);
             attach_couplings(*L);
+            L->fill_init.clear();
+            for (auto& kv : L->F) L->fill_init.push_back(kv.first);
             clock.mark(PH_COLOR);
             // greedy colouring of the D+F graph in ascending id order
             // (factorization.py:330-337, structure.py:137-167)
@@ -1243,6 +1281,7 @@ void Factorizer::run(double norm_estimate, const double* v0) {
                     }
                     remaining.swap(rest);
                     L->batches.push_back(batch);
+                    L->fill_created.emplace_back();
                     process_batch(*L, batch);
                     clock.mark(PH_COLOR);
                 }
@@ -1254,6 +1293,8 @@ void Factorizer::run(double norm_estimate, const double* v0) {
             rec.offset = L->offset;
             rec.size = L->size;
             rec.batches = L->batches;
+            rec.fill_init = L->fill_init;
+            rec.fill_created = L->fill_created;
             rec.csp = sparsity_constant(M, level);
             rec.ncolors = ncolors;
             rec.graph_degree = degree;

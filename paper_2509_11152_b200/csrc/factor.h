@@ -38,6 +38,11 @@ struct LevelRecord {    // factorization.py:150-164
     int csp = 0, ncolors = 0, graph_degree = 0, max_rank = 0;
     double time_s = 0.0;
     std::vector<ClusterFactor> factors;        // parallel to clusters
+    // fill keys: present when the level started (swept up by the transition,
+    // factorization.py:573-588) and created by each batch, in creation order
+    // (factorization.py:502-505) -- the F-key set after batch b is the union
+    std::vector<Key> fill_init;
+    std::vector<std::vector<Key>> fill_created;  // parallel to batches
     std::unordered_map<int, int> pos;          // cluster -> index
     int64_t total() const {
         int64_t t = 0;
@@ -67,6 +72,18 @@ struct Factorization {  // factorization.py:167-193
     Region work{size_t(16) << 20};
     ~Factorization();
 };
+
+// Structure replay (parity diagnostics, h2f_debug_replay_set): the threshold
+// decisions of another run -- kept count per (level, cluster) and the created
+// fill blocks per (level, creating cluster, key) -- replace this run's own,
+// so the floating-point path can be compared on an identical structure.
+struct Replay {
+    std::unordered_map<int64_t, int> kept;            // (level << 32 | cluster) -> kept
+    std::unordered_map<int64_t, std::vector<Key>> created;  // (level << 32 | creator) -> keys
+    int64_t kept_forced = 0, kept_changed = 0, fill_changed = 0;
+    bool active = false;
+};
+Replay& replay();
 
 // throws Error(H2F_E_SINGULAR) with cluster/level set on a vanishing pivot
 Factorization* factorize(H2Mat& m, double eps_lu, double norm_estimate, const double* v0_host);

@@ -133,12 +133,36 @@ class LevelRecord:
         self.graph_degree = info.graph_degree
         self.max_rank = info.max_rank
         self.time_s = info.time_s
+        self._h, self._idx = handle, idx
         factors = {}
         for c in self.clusters:
             ci = L.ClusterInfo()
             L.check(L.lib().h2f_factor_cluster_info(handle.ptr, idx, c, C.byref(ci)))
             factors[c] = ClusterFactor(handle, idx, c, self.level, ci.size, ci.r, ci.num_edges)
         self.factors = factors
+
+    def fill_events(self):
+        """(initial fill keys, [(batch, (a, b)), ...] created in order)
+        (factorization.py:502-505, 573-588)."""
+        ni, nc = C.c_int64(), C.c_int64()
+        L.check(L.lib().h2f_factor_level_fills(self._h.ptr, self._idx, C.byref(ni), None, C.byref(nc), None))
+        init = np.empty((max(ni.value, 1), 2), dtype=np.int64)
+        made = np.empty((max(nc.value, 1), 3), dtype=np.int64)
+        L.check(L.lib().h2f_factor_level_fills(self._h.ptr, self._idx, C.byref(ni), L.ptr(init, L.i64p),
+                                               C.byref(nc), L.ptr(made, L.i64p)))
+        return ([(int(a), int(b)) for a, b in init[:ni.value]],
+                [(int(t), (int(a), int(b))) for t, a, b in made[:nc.value]])
+
+    def fill_keys_after_batches(self):
+        """Sorted F-key set after every batch of this level."""
+        init, made = self.fill_events()
+        keys, out, i = set(init), [], 0
+        for b in range(self.nbatches):
+            while i < len(made) and made[i][0] == b:
+                keys.add(made[i][1])
+                i += 1
+            out.append(sorted(keys))
+        return out
 
 
 class H2Factorization:

@@ -80,8 +80,8 @@ def solve_multi_sharded(fac, B, group=None, solver=None, device=None):
     if solver is None:
         from . import _lib as L
 
-        L.ensure_init()
-        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        # the shard lives on the library's own device (LOCAL_RANK under torchrun)
+        dev = device if device is not None else torch.device("cuda", L.device())
         run = _device_solver(fac)
     else:
         dev = torch.device("cpu")

@@ -11,8 +11,13 @@ fam, n, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 over = {}
 perturb = 0.0
 pseed = 1
+decisions = None
 for a in sys.argv[4:]:
     k, v = a.split('=')
+    if k == "decisions":
+        decisions = v
+        O.DECISIONS = {}
+        continue
     if k == "perturb":
         perturb = float(v)
         continue
@@ -58,4 +63,12 @@ for rec in fac.records:
     save[f"L{rec.level}_blen"] = np.array([len(bb) for bb in rec.batches])
     summary["levels"].append([rec.level, rec.nbatches, rec.max_rank])
 np.savez(out, **save)
+if decisions:
+    D = O.DECISIONS
+    np.savez(decisions,
+             kept=np.array([r[:3] for r in D.get("kept", [])], dtype=np.int64).reshape(-1, 3),
+             kept_sig=np.array([r[3:] for r in D.get("kept", [])], dtype=np.float64).reshape(-1, 2),
+             created=np.array(D.get("created", []), dtype=np.int64).reshape(-1, 4),
+             close=np.array(D.get("close", []), dtype=np.float64).reshape(-1, 5),
+             eps_fill=fac.eps_fill, e_b=eb, e_b_raw=eb0)
 print(json.dumps(summary), flush=True)

@@ -1,0 +1,126 @@
+"""GPU tests of the boundary's contracts beyond the numerics: structure replay
+(the oracle's threshold decisions forced onto the device path), concurrent
+callers (concurrent solves are safe), device-pointer checks of
+the *_dev entry points."""
+import ctypes as C
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2509_11152_b200 as H
+from paper_2509_11152_b200 import _lib as L
+from golden_util import one_thread, problem, rhs, structure_of
+from oracle import h2_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def oracle_decisions(h2, eps_lu):
+    """Run the oracle with its decision recorder on; returns (factor, kept
+    rows, created rows)."""
+    O.DECISIONS = {}
+    try:
+        with one_thread():
+            ofac = O.factorize(h2, eps_lu)
+        d = O.DECISIONS
+    finally:
+        O.DECISIONS = None
+    kept = np.array([r[:3] for r in d.get("kept", [])], dtype=np.int64).reshape(-1, 3)
+    made = np.array(d.get("created", []), dtype=np.int64).reshape(-1, 4)
+    return ofac, kept, made
+
+
+@pytest.mark.parametrize("case", ["laplace3d_4096", "osc2d_4096", "laplace2d_2048", "cov2d_1024"])
+def test_replay_reproduces_oracle_structure(case):
+    """With the oracle's kept counts and fill decisions forced, the device
+    path's batches, ranks and sizes equal the oracle's on every level --
+    including the families whose own decisions are rounding-sensitive -- and
+    the solution then agrees with the oracle's to the factor tolerance."""
+    _, _, _, h2, prm = problem(case)
+    ofac, kept, made = oracle_decisions(h2, prm["eps_lu"])
+    L.replay_set(kept, made)
+    try:
+        fac = H.factorize(h2, prm["eps_lu"])
+        stats = L.replay_stats()
+    finally:
+        L.replay_clear()
+    assert stats["kept_forced"] > 0
+    assert structure_of(fac) == structure_of(ofac)
+    assert fac.top_size == ofac.top_size
+    for rec in fac.records:
+        _, events = rec.fill_events()
+        want = sorted((int(a), int(b)) for lv, _, a, b in made if lv == rec.level)
+        assert sorted(k for _, k in events) == want
+    b = rhs(h2, H.matvec)
+    with one_thread():
+        xo = O.substitute(ofac, b)
+    xg = H.solve(fac, b)
+    assert np.linalg.norm(xg - xo) <= 1e-6 * np.linalg.norm(xo)
+
+
+def test_replay_cleared_restores_own_decisions():
+    _, _, _, h2, prm = problem("laplace3d_4096")
+    f1 = H.factorize(h2, prm["eps_lu"])
+    _, kept, made = oracle_decisions(h2, prm["eps_lu"])
+    # the oracle's fill but no kept counts: the first cluster with fill to
+    # augment has no replayed decision
+    L.replay_set(np.zeros((0, 3), np.int64), made)
+    try:
+        with pytest.raises(ValueError, match="replay"):
+            H.factorize(h2, prm["eps_lu"])
+    finally:
+        L.replay_clear()
+    f2 = H.factorize(h2, prm["eps_lu"])
+    assert structure_of(f1) == structure_of(f2)
+
+
+def test_concurrent_solves_match_serial():
+    """ctypes releases the GIL: four threads solving on one factor at once
+    must give the serial bits (the library serialises its entry points)."""
+    _, _, _, h2, prm = problem("cov2d_4096")
+    fac = H.factorize(h2, prm["eps_lu"])
+    rng = np.random.default_rng(3)
+    bs = [rng.standard_normal(fac.n) for _ in range(4)]
+    Bm = rng.standard_normal((fac.n, 6))
+    want = [H.solve(fac, b) for b in bs]
+    want_m = H.solve_multi(fac, Bm)
+    want_r = H.refined_solve(h2, fac, bs[0])
+    got, errs = {}, []
+
+    def work(i):
+        try:
+            for rep in range(3):
+                got[(i, rep)] = H.solve(fac, bs[i])
+                if i == 0:
+                    got[("m", rep)] = H.solve_multi(fac, Bm)
+                if i == 1:
+                    got[("r", rep)] = H.refined_solve(h2, fac, bs[0])
+        except Exception as exc:  # pragma: no cover - reported below
+            errs.append(exc)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for i in range(4):
+        for rep in range(3):
+            assert np.array_equal(got[(i, rep)], want[i])
+    for rep in range(3):
+        assert np.array_equal(got[("m", rep)], want_m)
+        assert np.array_equal(got[("r", rep)], want_r)
+
+
+def test_dev_entry_points_reject_host_pointers():
+    _, _, _, h2, prm = problem("cov2d_1024")
+    fac = H.factorize(h2, prm["eps_lu"])
+    b = np.ones(fac.n)
+    x = np.zeros(fac.n)
+    lib = L.ensure_init()
+    code = lib.h2f_solve_dev(fac._h.ptr, C.c_void_p(b.ctypes.data), C.c_void_p(x.ctypes.data), 1)
+    assert code == L.H2F_E_ARG
+    assert "host pointer" in L.last_error() or "not a CUDA pointer" in L.last_error()
+    # the context is still usable afterwards
+    assert np.all(np.isfinite(H.solve(fac, b)))

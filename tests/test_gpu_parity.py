@@ -72,6 +72,17 @@ def test_structure_bit_exact(case):
 
 
 @pytest.mark.parametrize("case", ROBUST)
+def test_fill_keys_after_every_batch_match_reference(case):
+    # golden `fills`: sorted F-key set after each batch (make_golden.py elim_spy)
+    g = load(case)
+    _, _, fac = gpu_factor(case)
+    got = []
+    for rec in fac.records:
+        got += [[list(k) for k in ks] for ks in rec.fill_keys_after_batches()]
+    assert got == g["fills"]
+
+
+@pytest.mark.parametrize("case", ROBUST)
 def test_pivots_match_reference(case):
     g = load(case)
     _, _, fac = gpu_factor(case)
