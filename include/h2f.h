@@ -170,6 +170,13 @@ int h2f_solve_dev(h2f_factor f, const double* b_dev, double* x_dev, int64_t nrhs
 int h2f_refined_solve(h2f_matrix m, h2f_factor f, const double* b, double* x, int32_t steps);
 int h2f_refined_solve_dev(h2f_matrix m, h2f_factor f, const double* b_dev, double* x_dev,
                           int32_t steps);
+/* refined_solve for an n x nrhs block (row-major, like solve_multi): block
+ * substitution + block matvec per step (extension: the reference's
+ * refined_solve is single-vector, solve.py:63-77) */
+int h2f_refined_solve_multi(h2f_matrix m, h2f_factor f, const double* b, double* x, int64_t nrhs,
+                            int32_t steps);
+int h2f_refined_solve_multi_dev(h2f_matrix m, h2f_factor f, const double* b_dev, double* x_dev,
+                                int64_t nrhs, int32_t steps);
 
 /* ---- factor introspection (lazy export to host) ---------------------------- */
 int h2f_factor_info_get(h2f_factor f, h2f_factor_info* info);
@@ -210,13 +217,15 @@ int h2f_greedy_coloring(int64_t num_clusters, const int64_t* clusters, int64_t n
  *   created_rows [ncreated][4]  (level, creating cluster, a, b) for every
  *                               fill block the run created  factorization.py:502-505
  * With identical decisions the batches, ranks and fill pattern coincide, so
- * the solutions differ only by floating-point rounding.  stats: number of
- * kept counts taken from the table, fill decisions that differ from this
- * run's own norm test. */
+ * the solutions differ only by floating-point rounding. */
 int h2f_debug_replay_set(const int64_t* kept_rows, int64_t nkept, const int64_t* created_rows,
                          int64_t ncreated);
 int h2f_debug_replay_clear(void);
-int h2f_debug_replay_stats(int64_t* kept_forced, int64_t* fill_changed);
+/* stats[8]: kept counts taken from the table, of which differing from this
+ * run's own count; fill decisions differing from this run's own norm test,
+ * then those by |log10(own norm / tolerance)| in [0, .01), [.01, .1), [.1, .5),
+ * [.5, 1), [1, inf) */
+int h2f_debug_replay_stats(int64_t* stats);
 
 #ifdef __cplusplus
 }

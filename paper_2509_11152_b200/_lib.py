@@ -93,6 +93,9 @@ _SIGS = {
     "h2f_solve_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     "h2f_refined_solve": (C.c_int, [C.c_void_p, C.c_void_p, f64p, f64p, C.c_int32]),
     "h2f_refined_solve_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
+    "h2f_refined_solve_multi": (C.c_int, [C.c_void_p, C.c_void_p, f64p, f64p, C.c_int64, C.c_int32]),
+    "h2f_refined_solve_multi_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                              C.c_int32]),
     "h2f_factor_info_get": (C.c_int, [C.c_void_p, C.POINTER(FactorInfo)]),
     "h2f_factor_level_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(LevelInfo)]),
     "h2f_factor_level_arrays": (C.c_int, [C.c_void_p, C.c_int32, i64p, i64p, i64p, i64p, i64p, i64p]),
@@ -105,7 +108,7 @@ _SIGS = {
     "h2f_greedy_coloring": (C.c_int, [C.c_int64, i64p, C.c_int64, i64p, i32p, i32p, i32p]),
     "h2f_debug_replay_set": (C.c_int, [i64p, C.c_int64, i64p, C.c_int64]),
     "h2f_debug_replay_clear": (C.c_int, []),
-    "h2f_debug_replay_stats": (C.c_int, [i64p, i64p]),
+    "h2f_debug_replay_stats": (C.c_int, [i64p]),
 }
 
 _lib = None
@@ -285,6 +288,8 @@ def replay_clear():
 
 
 def replay_stats():
-    a, b = C.c_int64(), C.c_int64()
-    check(ensure_init().h2f_debug_replay_stats(C.byref(a), C.byref(b)))
-    return {"kept_forced": a.value, "fill_changed": b.value}
+    st = np.zeros(8, dtype=np.int64)
+    check(ensure_init().h2f_debug_replay_stats(ptr(st, i64p)))
+    return {"kept_forced": int(st[0]), "kept_changed": int(st[1]), "fill_changed": int(st[2]),
+            "fill_changed_by_log10_margin": {"<0.01": int(st[3]), "<0.1": int(st[4]), "<0.5": int(st[5]),
+                                             "<1": int(st[6]), ">=1": int(st[7])}}

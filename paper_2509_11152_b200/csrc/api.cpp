@@ -375,6 +375,29 @@ int h2f_refined_solve(h2f_matrix m, h2f_factor f, const double* b, double* x, in
     });
 }
 
+int h2f_refined_solve_multi(h2f_matrix m, h2f_factor f, const double* b, double* x, int64_t nrhs, int32_t steps) {
+    return guard([&] {
+        if (nrhs < 1) throw Error(H2F_E_ARG, "nrhs must be >= 1");
+        const size_t n = size_t(f->f->n) * nrhs;
+        DevBuf db(n), dx(n);
+        H2F_CUDA(cudaMemcpyAsync(db.p, b, n * 8, cudaMemcpyHostToDevice, ctx().stream));
+        refined_solve_device(*m->m, *f->f, db.p, dx.p, steps, int(nrhs));
+        d2h(x, dx.p, n * 8);
+        ctx().sync();
+    });
+}
+
+int h2f_refined_solve_multi_dev(h2f_matrix m, h2f_factor f, const double* b_dev, double* x_dev, int64_t nrhs,
+                                int32_t steps) {
+    return guard([&] {
+        if (nrhs < 1) throw Error(H2F_E_ARG, "nrhs must be >= 1");
+        check_dev_ptr(b_dev, "b_dev");
+        check_dev_ptr(x_dev, "x_dev");
+        refined_solve_device(*m->m, *f->f, b_dev, x_dev, steps, int(nrhs));
+        ctx().sync();
+    });
+}
+
 int h2f_factor_info_get(h2f_factor f, h2f_factor_info* info) {
     return guard([&] {
         const Factorization& F = *f->f;
@@ -524,10 +547,13 @@ int h2f_debug_replay_clear(void) {
     return guard([&] { replay() = Replay{}; });
 }
 
-int h2f_debug_replay_stats(int64_t* kept_forced, int64_t* fill_changed) {
+int h2f_debug_replay_stats(int64_t* stats) {
     return guard([&] {
-        *kept_forced = replay().kept_forced;
-        *fill_changed = replay().fill_changed;
+        const Replay& R = replay();
+        stats[0] = R.kept_forced;
+        stats[1] = R.kept_changed;
+        stats[2] = R.fill_changed;
+        for (int i = 0; i < 5; ++i) stats[3 + i] = R.fill_margin_hist[i];
     });
 }
 

@@ -126,7 +126,15 @@ struct GemmBuild {
             return e ? std::atof(e) : 96.0;
         }();
         const double keff = flops / (double(ntiles) * 2.0 * GEMM_TILE * GEMM_TILE);
-        launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), ntiles, dcta, norms, X.stream, keff < kmax);
+        // K_eff below this: the register-direct short-K kernel
+        static const double kwarp = [] {
+            const char* e = std::getenv("H2F_GEMM_WARP_KMAX");
+            return e ? std::atof(e) : 40.0;
+        }();
+        if (keff < kwarp)
+            launch_gemm_warp(dt, dc, ds, int32_t(tasks.size()), ntiles, norms, X.stream);
+        else
+            launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), ntiles, dcta, norms, X.stream, keff < kmax);
     }
 };
 

@@ -322,9 +322,10 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     // of (I - V V^T) F, so the QR/SVD work on (s-k) instead of s rows.
     clock.mark(PH_AUGMENT);
     std::vector<double*> Q(nb);
-    int* kept_d = scr.alloc_n<int>(nb);
+    // kept counts [0, nb) and degenerate-sigma flags [nb, 2 nb)
+    int* kept_d = scr.alloc_n<int>(2 * nb);
     struct Aug {
-        int s, k, n, wf;
+        int s, k, n, wf, m;
         bool skip;
         View V;
         double *BT, *QV, *U;
@@ -337,9 +338,9 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         std::vector<QrTask> qr_small, qr_big, qr_seg;
         std::vector<SvdTask> svd_small, svd_big;
         int max_n_small = 1;
-        // under a structure replay every singular vector is written (sorted)
-        // and the kept count comes from the replayed run
-        const double svd_thresh = replay().active ? -1.0 : drop;
+        // the Jacobi writes every singular vector (sorted); under a structure
+        // replay the kept count then comes from the replayed run
+        const double svd_thresh = drop;
         // H2F_SMALL_N_MAX (tests) lowers the shared-memory QR/SVD cut-off so
         // the large-n (blocked QR, multi-CTA Jacobi) path runs on small inputs
         int small_n_max = SMEM_DENSE_MAX_N;
@@ -351,7 +352,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         // one-CTA shared-memory Jacobi up to this n; above, the block-cyclic
         // multi-CTA Jacobi (n/16 CTAs per cluster) finishes a batch sooner
         const int svd_smem_max = std::min(small_n_max, env_int("H2F_SVD_SMEM_MAX", 64));
-        H2F_CUDA(cudaMemsetAsync(kept_d, 0, sizeof(int) * nb, st));
+        H2F_CUDA(cudaMemsetAsync(kept_d, 0, sizeof(int) * 2 * nb, st));
         for (int bi = 0; bi < nb; ++bi) {
             const int c = batch[bi], ci = L.at(c);
             Aug& A = aug[bi];
@@ -392,7 +393,8 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             double* R = scr.alloc_n<double>(int64_t(n) * n);
             A.U = scr.alloc_n<double>(int64_t(n) * n);
             const int m = std::min(n, wf);
-            SvdTask sv{R, A.U, m, n, kept_d + bi, 0};
+            A.m = m;
+            SvdTask sv{R, A.U, m, n, kept_d + bi, nb};
             if (n > hh_min_n) {
                 qr_big.push_back(QrTask{Z, R, wf, n, wf, 0, wf, 0});
             } else {
@@ -468,12 +470,13 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             jacobi_multi_cta(svd_big, svd_thresh, scr);
         }
     }
-    int* kept_h = static_cast<int*>(X.pinned_buf(sizeof(int) * nb));
-    H2F_CUDA(cudaMemcpyAsync(kept_h, kept_d, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
+    int* kept_h = static_cast<int*>(X.pinned_buf(sizeof(int) * 2 * nb));
+    H2F_CUDA(cudaMemcpyAsync(kept_h, kept_d, sizeof(int) * 2 * nb, cudaMemcpyDeviceToHost, st));
     tick(HT_AUG);
     X.sync();
     tick(HT_SYNC1);
     std::vector<int> kept(kept_h, kept_h + nb);
+    std::vector<int> degenerate(kept_h + nb, kept_h + 2 * nb);
     if (replay().active) {
         Replay& R = replay();
         for (int bi = 0; bi < nb; ++bi) {
@@ -485,6 +488,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             if (it->second > std::min(aug[bi].n, aug[bi].wf))
                 throw Error(H2F_E_ARG, "replay: kept count exceeds the fill rank bound");
             ++R.kept_forced;
+            R.kept_changed += kept[bi] != it->second;
             kept[bi] = it->second;
         }
     }
@@ -494,11 +498,18 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                          aug[bi].wf, kept[bi], aug[bi].skip ? 1 : 0);
     }
     {
-        // b_aug = [V, V_perp U_kept] re-orthogonalised, then Q~ = [complement | b_aug]
-        CopyBuild keep;
+        // b_aug = [V, V_perp U_kept] re-orthogonalised, then Q~ = [complement | b_aug].
+        // When the Jacobi produced a complete orthonormal U (m == n, no zero
+        // sigma), the complement is V_perp U_rest: orthogonal to V (V_perp is)
+        // and to vbar (U_rest is orthogonal to U_kept) -- an orthonormal
+        // completion like the reference's Householder one (factorization.py:88-99;
+        // the leading r columns are not unique), as one GEMM
+        // instead of a second complete QR.  Otherwise: Householder complement.
+        CopyBuild keep, place;
         GemmBuild gv;
         std::vector<ReorthTask> ro;
         std::vector<ComplementTask> cmp;
+        const bool fast_ok = env_int("H2F_COMPLEMENT_QR", 0) == 0;
         for (int bi = 0; bi < nb; ++bi) {
             Aug& A = aug[bi];
             if (A.skip) continue;
@@ -510,8 +521,14 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             gv.add1(A.BT + int64_t(k) * s, s, kp, s, GEMM_STORE, contrib(A.U, n, 0, A.QV, s, 1, n));
             ro.push_back(ReorthTask{A.V.p, A.BT, scr.alloc_n<double>(int64_t(std::max(k, 1)) * kp), A.V.ld, s, k,
                                     kp, 0});
-            cmp.push_back(ComplementTask{A.BT, scr.alloc_n<double>(int64_t(s) * s), Q[bi],
-                                         scr.alloc_n<double>(int64_t(16) * s), s, k + kp});
+            if (fast_ok && A.m == n && !degenerate[bi]) {
+                const int r = n - kp;
+                if (r > 0) gv.add1(Q[bi], s, s, r, GEMM_STORE, contrib(A.QV, s, 0, A.U + int64_t(kp) * n, n, 1, n));
+                place.add(Q[bi] + r, s, s, k + kp, A.BT, s, 1, COPY_SET);
+            } else {
+                cmp.push_back(ComplementTask{A.BT, scr.alloc_n<double>(int64_t(s) * s), Q[bi],
+                                             scr.alloc_n<double>(int64_t(16) * s), s, k + kp});
+            }
         }
         keep.launch();
         gv.launch(K_GEMM_AUG);
@@ -525,6 +542,38 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             ProfScope ps(K_COMPLEMENT, rf + cf, cb);
             if (!ro.empty()) reorth_batched(ro, scr);
             if (!cmp.empty()) complement(cmp, scr);
+        }
+        place.launch();
+    }
+    if (env_int("H2F_CHECK_Q", 0)) {
+        // development aid: orthogonality of every Q~ of the batch
+        X.sync();
+        for (int bi = 0; bi < nb; ++bi) {
+            const int sz = aug[bi].s;
+            std::vector<double> q(size_t(sz) * sz);
+            H2F_CUDA(cudaMemcpy(q.data(), Q[bi], q.size() * 8, cudaMemcpyDeviceToHost));
+            double worst = 0;
+            for (int a = 0; a < sz; ++a)
+                for (int b = 0; b < sz; ++b) {
+                    double d = 0;
+                    for (int i = 0; i < sz; ++i) d += q[size_t(i) * sz + a] * q[size_t(i) * sz + b];
+                    worst = std::max(worst, std::fabs(d - (a == b ? 1.0 : 0.0)));
+                }
+            if (worst > 1e-10 && !aug[bi].skip && std::getenv("H2F_CHECK_Q_DUMP")) {
+                const Aug& A = aug[bi];
+                std::vector<double> u(size_t(A.n) * A.n), qv(size_t(sz) * sz);
+                H2F_CUDA(cudaMemcpy(u.data(), A.U, u.size() * 8, cudaMemcpyDeviceToHost));
+                H2F_CUDA(cudaMemcpy(qv.data(), A.QV, qv.size() * 8, cudaMemcpyDeviceToHost));
+                FILE* f = std::fopen(std::getenv("H2F_CHECK_Q_DUMP"), "wb");
+                std::fwrite(u.data(), 8, u.size(), f);
+                std::fwrite(qv.data(), 8, qv.size(), f);
+                std::fwrite(q.data(), 8, q.size(), f);
+                std::fclose(f);
+            }
+            if (worst > 1e-10)
+                std::fprintf(stderr, "[check_q] level %d cluster %d s %d k %d n %d m %d wf %d kept %d deg %d skip %d: %.3e\n",
+                             L.level, batch[bi], sz, aug[bi].k, aug[bi].n, aug[bi].m, aug[bi].wf, kept[bi],
+                             degenerate[bi], int(aug[bi].skip), worst);
         }
     }
     for (int bi = 0; bi < nb; ++bi) {
@@ -974,7 +1023,12 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 auto rt = R.created.find((int64_t(L.level) << 32) | uint32_t(cd.creator));
                 const bool want = rt != R.created.end() &&
                                   std::find(rt->second.begin(), rt->second.end(), cd.key) != rt->second.end();
-                R.fill_changed += want != create_it;
+                if (want != create_it) {
+                    ++R.fill_changed;
+                    // how far this run's own norm is from the drop tolerance
+                    const double lr = std::fabs(std::log10(std::max(std::sqrt(ss_h[i]), 1e-300) / drop));
+                    ++R.fill_margin_hist[lr < 0.01 ? 0 : lr < 0.1 ? 1 : lr < 0.5 ? 2 : lr < 1.0 ? 3 : 4];
+                }
                 create_it = want;
             }
             if (create_it) {

@@ -81,6 +81,9 @@ struct Replay {
     std::unordered_map<int64_t, int> kept;            // (level << 32 | cluster) -> kept
     std::unordered_map<int64_t, std::vector<Key>> created;  // (level << 32 | creator) -> keys
     int64_t kept_forced = 0, kept_changed = 0, fill_changed = 0;
+    // changed fill decisions by |log10(own norm / drop tolerance)|:
+    // < 0.01, < 0.1, < 0.5, < 1, >= 1
+    int64_t fill_margin_hist[5] = {0, 0, 0, 0, 0};
     bool active = false;
 };
 Replay& replay();
@@ -89,6 +92,7 @@ Replay& replay();
 Factorization* factorize(H2Mat& m, double eps_lu, double norm_estimate, const double* v0_host);
 
 void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs);
-void refined_solve_device(H2Mat& m, Factorization& f, const double* b_dev, double* x_dev, int steps);
+void refined_solve_device(H2Mat& m, Factorization& f, const double* b_dev, double* x_dev, int steps,
+                          int nrhs = 1);
 
 }  // namespace h2f

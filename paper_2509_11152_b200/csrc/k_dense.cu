@@ -99,6 +99,14 @@ __global__ void __launch_bounds__(DT) qr_r_smem_kernel(const QrTask* __restrict_
     }
 }
 
+// A sweep whose rotations all had |cos angle(x_p, x_q)| <= 1e-7 leaves the rows
+// orthogonal to O(1e-14) (quadratic convergence), below the rotation
+// threshold tol = eps sqrt(n) of a further sweep: such a sweep ends the
+// iteration instead of a final sweep that would rotate nothing.  The rotate
+// helpers return 0 (no rotation), 1 (settling rotation) or 2 (rotation with
+// |cos| > 1e-7, another sweep is needed).
+constexpr double JAC_SETTLE2 = 1e-14;
+
 // Jacobi rotation annihilating the (p, q) inner product: a = |x_p|^2,
 // b = |x_q|^2, g = x_p.x_q.  Rotate iff |g| > tol sqrt(a b) (tested
 // squared); t = tan(theta) = sgn(d) 2g / (|d| + sqrt(d^2 + 4 g^2)), d = b - a
@@ -119,13 +127,14 @@ __device__ __forceinline__ bool jac_rotation(double a, double b, double g, doubl
 // shrinks below 1/64 of its old value is recomputed from the rotated row (the
 // update would lose relative accuracy to cancellation, cf. LAPACK dgesvj).
 // One warp per pair; a and b are warp-uniform.
-__device__ __forceinline__ bool jac_rotate_cached(double* __restrict__ x, double* __restrict__ y, int n, double tol,
-                                                  double& a, double& b) {
+__device__ __forceinline__ int jac_rotate_cached(double* __restrict__ x, double* __restrict__ y, int n, double tol,
+                                                 double& a, double& b) {
     const int lane = threadIdx.x & 31;
     double g = 0.0;
     for (int i = lane; i < n; i += 32) g += x[i] * y[i];
     g = warp_sum(g);
-    if (!(g != 0.0 && a > 0.0 && b > 0.0 && g * g > (tol * tol) * (a * b))) return false;
+    if (!(g != 0.0 && a > 0.0 && b > 0.0 && g * g > (tol * tol) * (a * b))) return 0;
+    const int code = g * g > JAC_SETTLE2 * (a * b) ? 2 : 1;
     const double d = b - a;
     const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(d * d + 4.0 * g * g));
     const double c = rsqrt(1.0 + t * t), sn = c * t;
@@ -144,7 +153,7 @@ __device__ __forceinline__ bool jac_rotate_cached(double* __restrict__ x, double
     if (rb) b2 = warp_sum(by);
     a = a2;
     b = b2;
-    return true;
+    return code;
 }
 
 // circle-method round robin: player list [0, rot...]; pair i of round st
@@ -176,12 +185,13 @@ __device__ void jacobi_sweeps(double* A, int m, int n, int* flag, double* nrm) {
                 rr_pair(pi, st, mm, p, q);
                 if (p >= m || q >= m) continue;
                 double a = nrm[p], b = nrm[q];
-                if (jac_rotate_cached(A + (int64_t)p * n, A + (int64_t)q * n, n, tol, a, b)) {
+                const int rc = jac_rotate_cached(A + (int64_t)p * n, A + (int64_t)q * n, n, tol, a, b);
+                if (rc) {
                     __syncwarp();  // every lane has read nrm[p], nrm[q] before lane 0 rewrites them
                     if (lane == 0) {
                         nrm[p] = a;
                         nrm[q] = b;
-                        *flag = 1;
+                        if (rc == 2) *flag = 1;
                     }
                 }
                 __syncwarp();
@@ -194,10 +204,28 @@ __device__ void jacobi_sweeps(double* A, int m, int n, int* flag, double* nrm) {
     }
 }
 
-// sigma = row norms, count sigma >= thresh, write the kept rows normalised in
-// descending sigma order (first index wins ties)
+// below this a singular value counts as zero: its row cannot be normalised
+constexpr double JAC_TINY = 1e-290;
+// Rows whose sigma is below JAC_RANK_REL * sigma_max carry rounding noise of R,
+// not a direction: when R is numerically rank deficient (e.g. exact zero
+// columns from structurally zero fill rows) such rows are not orthogonal to
+// the others, so the sorted rows are not an orthonormal completion and the
+// caller must fall back to the Householder complement (deg flag).
+constexpr double JAC_RANK_REL = 1e-12;
+
+// sigma_max over sig[0..m) (warp-reduced, every lane of every warp)
+__device__ __forceinline__ double sig_max(const double* sig, int m) {
+    double v = 0.0;
+    for (int j = threadIdx.x & 31; j < m; j += 32) v = fmax(v, sig[j]);
+    return warp_max(v);
+}
+
+// sigma = row norms, count sigma >= thresh, write all m rows normalised in
+// descending sigma order (first index wins ties): rows 0..kept-1 are the kept
+// left singular vectors, the rest complete them to an orthonormal basis when
+// m == n and no sigma is ~0 (otherwise kept_out[deg_off] is set)
 __device__ void jacobi_finish(const double* A, int m, int n, double thresh, double* sig, int* rnk,
-                              int* kept_s, double* U, int* kept_out) {
+                              int* kept_s, double* U, int* kept_out, int deg_off) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int i = warp; i < m; i += nw) {
         const double* ri = A + (int64_t)i * n;
@@ -218,10 +246,13 @@ __device__ void jacobi_finish(const double* A, int m, int n, double thresh, doub
     __syncthreads();
     const int kept = *kept_s;
     if (threadIdx.x == 0) *kept_out = kept;
+    (void)kept;
+    const double smax = sig_max(sig, m);
     for (int i = warp; i < m; i += nw) {
         const int j = rnk[i];
-        if (j >= kept) continue;
-        const double inv = 1.0 / sig[i];
+        const double si = sig[i];
+        if (!(si > JAC_TINY && si > JAC_RANK_REL * smax) && deg_off && lane == 0) kept_out[deg_off] = 1;
+        const double inv = si > JAC_TINY ? 1.0 / si : 0.0;
         const double* ri = A + (int64_t)i * n;
         for (int c = lane; c < n; c += 32) U[(int64_t)j * n + c] = ri[c] * inv;
     }
@@ -241,7 +272,7 @@ __global__ void __launch_bounds__(DT) jacobi_smem_kernel(const SvdTask* __restri
     __syncthreads();
     jacobi_sweeps(A, m, n, &flag, A + m * n + 2 * m);  // after sig[m], rank[m]
     jacobi_finish(A, m, n, thresh, A + m * n, reinterpret_cast<int*>(A + m * n + m), &kept_s, T.U,
-                  T.kept_out);
+                  T.kept_out, T.deg_off);
 }
 
 // rows k..k+kept-1 of BT: re-orthogonalise against V and normalise
@@ -386,7 +417,7 @@ __device__ __forceinline__ void cta_group_barrier(uint32_t* bar, int nct) {
 
 constexpr int JT = 256;  // threads per CTA of the multi-CTA Jacobi
 
-__device__ __forceinline__ bool jac_pair_loop(double* __restrict__ rp, double* __restrict__ rq, int n, double tol) {
+__device__ __forceinline__ int jac_pair_loop(double* __restrict__ rp, double* __restrict__ rq, int n, double tol) {
     const int lane = threadIdx.x & 31;
     double a = 0.0, b = 0.0, g = 0.0;
     for (int i = lane; i < n; i += 32) {
@@ -399,17 +430,17 @@ __device__ __forceinline__ bool jac_pair_loop(double* __restrict__ rp, double* _
     b = warp_sum(b);
     g = warp_sum(g);
     double c, sn;
-    if (!jac_rotation(a, b, g, tol, c, sn)) return false;
+    if (!jac_rotation(a, b, g, tol, c, sn)) return 0;
     for (int i = lane; i < n; i += 32) {
         const double x = __ldcg(rp + i), y = __ldcg(rq + i);
         __stcg(rp + i, c * x - sn * y);
         __stcg(rq + i, sn * x + c * y);
     }
-    return true;
+    return g * g > JAC_SETTLE2 * (a * b) ? 2 : 1;
 }
 
 template <int NPL>
-__device__ __forceinline__ bool jac_pair_reg(double* __restrict__ rp, double* __restrict__ rq, int n, double tol) {
+__device__ __forceinline__ int jac_pair_reg(double* __restrict__ rp, double* __restrict__ rq, int n, double tol) {
     if constexpr (NPL == 0) return jac_pair_loop(rp, rq, n, tol);
     const int lane = threadIdx.x & 31;
     double x[NPL > 0 ? NPL : 1], y[NPL > 0 ? NPL : 1];
@@ -430,7 +461,7 @@ __device__ __forceinline__ bool jac_pair_reg(double* __restrict__ rp, double* __
     b = warp_sum(b);
     g = warp_sum(g);
     double c, sn;
-    if (!jac_rotation(a, b, g, tol, c, sn)) return false;
+    if (!jac_rotation(a, b, g, tol, c, sn)) return 0;
 #pragma unroll
     for (int k = 0; k < NPL; ++k) {
         const int i = lane + 32 * k;
@@ -439,7 +470,7 @@ __device__ __forceinline__ bool jac_pair_reg(double* __restrict__ rp, double* __
             __stcg(rq + i, sn * x[k] + c * y[k]);
         }
     }
-    return true;
+    return g * g > JAC_SETTLE2 * (a * b) ? 2 : 1;
 }
 
 template <int NPL>
@@ -489,7 +520,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_coop_kernel(const CoopSvdTask* _
                 int p, q;
                 rr_pair(pi, st, mm, p, q);
                 if (p >= m || q >= m) continue;
-                rotated |= jac_pair_reg<NPL>(A + (int64_t)p * n, A + (int64_t)q * n, n, tol);
+                rotated |= jac_pair_reg<NPL>(A + (int64_t)p * n, A + (int64_t)q * n, n, tol) == 2;
             }
             cta_group_barrier(CT.bar, nct);
         }
@@ -514,15 +545,18 @@ __global__ void __launch_bounds__(JT, 1) jacobi_coop_kernel(const CoopSvdTask* _
     __syncthreads();
     const int kept = kept_s;
     if (rank == 0 && threadIdx.x == 0) *CT.t.kept_out = kept;
-    // kept rows, normalised, in descending sigma order (first index wins ties)
+    const double smax = sig_max(dsh, m);
+    // all rows, normalised, in descending sigma order (first index wins ties)
     for (int i = gw; i < m; i += gnw) {
         const double si = dsh[i];
         int r = 0;
         for (int j = lane; j < m; j += 32) r += (dsh[j] > si) || (dsh[j] == si && j < i);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-        if (r >= kept) continue;
-        const double inv = 1.0 / si;
+        (void)kept;
+        if (!(si > JAC_TINY && si > JAC_RANK_REL * smax) && CT.t.deg_off && lane == 0)
+            CT.t.kept_out[CT.t.deg_off] = 1;
+        const double inv = si > JAC_TINY ? 1.0 / si : 0.0;
         const double* ri = A + (int64_t)i * n;
         for (int c = lane; c < n; c += 32) CT.t.U[(int64_t)r * n + c] = __ldcg(ri + c) * inv;
     }
@@ -535,8 +569,8 @@ constexpr int JBT = 512;  // threads per CTA of the block-cyclic Jacobi
 // slice of the rows, the dot products are summed over the slices in a fixed
 // order through `red` (double-buffered by the group's call parity `par`).
 template <int W>
-__device__ __forceinline__ bool jac_rotate_split(double* __restrict__ x, double* __restrict__ y, int n, double tol,
-                                                 double& a, double& b, int grp, int sub, double* red, int& par) {
+__device__ __forceinline__ int jac_rotate_split(double* __restrict__ x, double* __restrict__ y, int n, double tol,
+                                                double& a, double& b, int grp, int sub, double* red, int& par) {
     if (W == 1) return jac_rotate_cached(x, y, n, tol, a, b);
     const int lane = threadIdx.x & 31;
     const int len = (n + W - 1) / W, i0 = sub * len, i1 = min(n, i0 + len);
@@ -554,7 +588,8 @@ __device__ __forceinline__ bool jac_rotate_split(double* __restrict__ x, double*
     double g = 0.0;
     for (int i = i0 + lane; i < i1; i += 32) g += x[i] * y[i];
     g = group_sum(g);
-    if (!(g != 0.0 && a > 0.0 && b > 0.0 && g * g > (tol * tol) * (a * b))) return false;
+    if (!(g != 0.0 && a > 0.0 && b > 0.0 && g * g > (tol * tol) * (a * b))) return 0;
+    const int code = g * g > JAC_SETTLE2 * (a * b) ? 2 : 1;
     const double d = b - a;
     const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(d * d + 4.0 * g * g));
     const double c = rsqrt(1.0 + t * t), sn = c * t;
@@ -573,7 +608,7 @@ __device__ __forceinline__ bool jac_rotate_split(double* __restrict__ x, double*
     if (rb) b2 = group_sum(by);
     a = a2;
     b = b2;
-    return true;
+    return code;
 }
 
 // ---- block-cyclic multi-CTA Jacobi ----------------------------------------------
@@ -684,9 +719,10 @@ __global__ void __launch_bounds__(JBT, 1) jacobi_block_kernel(const CoopSvdTask*
                         if (a >= JB || b >= JB) continue;
                         const int ra = blk * JB + a, rb = blk * JB + b;
                         double na = bn[ra], nb = bn[rb];
-                        if (jac_rotate_split<WPP>(bsm + (int64_t)ra * n, bsm + (int64_t)rb * n, n, tol, na, nb, grp, sub,
-                                                  red, par)) {
-                            rotated = true;
+                        const int rc = jac_rotate_split<WPP>(bsm + (int64_t)ra * n, bsm + (int64_t)rb * n, n, tol,
+                                                             na, nb, grp, sub, red, par);
+                        if (rc) {
+                            rotated |= rc == 2;
                             if (lane == 0 && sub == 0) {
                                 bn[ra] = na;
                                 bn[rb] = nb;
@@ -701,9 +737,10 @@ __global__ void __launch_bounds__(JBT, 1) jacobi_block_kernel(const CoopSvdTask*
                 const int i = grp;
                 const int rq = JB + (i + s) % JB;
                 double na = bn[i], nb = bn[rq];
-                if (jac_rotate_split<WPP>(bsm + (int64_t)i * n, bsm + (int64_t)rq * n, n, tol, na, nb, grp, sub, red,
-                                          par)) {
-                    rotated = true;
+                const int rc = jac_rotate_split<WPP>(bsm + (int64_t)i * n, bsm + (int64_t)rq * n, n, tol, na, nb, grp,
+                                                     sub, red, par);
+                if (rc) {
+                    rotated |= rc == 2;
                     if (lane == 0 && sub == 0) {
                         bn[i] = na;
                         bn[rq] = nb;
@@ -746,14 +783,17 @@ __global__ void __launch_bounds__(JBT, 1) jacobi_block_kernel(const CoopSvdTask*
     __syncthreads();
     const int kept = kept_s;
     if (rank == 0 && threadIdx.x == 0) *CT.t.kept_out = kept;
+    const double smax = sig_max(dsh, m);
     for (int i = gw; i < m; i += gnw) {
         const double si = dsh[i];
         int r = 0;
         for (int j = lane; j < m; j += 32) r += (dsh[j] > si) || (dsh[j] == si && j < i);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-        if (r >= kept) continue;
-        const double inv = 1.0 / si;
+        (void)kept;
+        if (!(si > JAC_TINY && si > JAC_RANK_REL * smax) && CT.t.deg_off && lane == 0)
+            CT.t.kept_out[CT.t.deg_off] = 1;
+        const double inv = si > JAC_TINY ? 1.0 / si : 0.0;
         const double* ri = A + (int64_t)i * n;
         for (int c = lane; c < n; c += 32) CT.t.U[(int64_t)r * n + c] = __ldcg(ri + c) * inv;
     }
@@ -1301,7 +1341,7 @@ void launch_absmax(const double* A, int64_t lda, int32_t rows, int32_t cols, dou
                    cudaStream_t st) {
     cudaMemsetAsync(out, 0, sizeof(double), st);
     const int64_t tot = int64_t(rows) * cols;
-    const int grid = int(std::min<int64_t>(148 * 4, std::max<int64_t>(1, (tot + 1023) / 1024)));
+    const int grid = int(std::min<int64_t>(int64_t(sm_count()) * 4, std::max<int64_t>(1, (tot + 1023) / 1024)));
     absmax_kernel<<<grid, 1024, 0, st>>>(A, lda, rows, cols, out);
     count_launch();
 }

@@ -400,6 +400,124 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
     cp_async_wait<0>();
 }
 
+// ---- short-K variant: one 64x64 tile per CTA, each warp streams its own
+// DMMA fragments straight from L2 into registers (no shared-memory staging,
+// no CTA barriers on the math path), __launch_bounds__(128, 3) for 12 warps
+// per SM.  For contractions with K of a few dozen (the leaf-level Schur
+// updates, r = 5..40) the C read-modify-write dominates and the SM needs many
+// independent tiles in flight rather than operand reuse.  Summation order
+// (contributions in order, k-steps of 4 in order, epilogue alpha*acc then
+// C + v, tile norm = thread partials -> warp sums -> warps 0..3) is the same
+// as gemm_tasks_kernel's, so the two produce identical bits.
+template <int TA, int TB>
+__device__ __forceinline__ void warp_contrib(const GemmContrib& P, int M, int N, int r0, int c0, int g, int t,
+                                             double (&acc)[4][4][2]) {
+    const double* __restrict__ A = P.A;
+    const double* __restrict__ B = P.B;
+    const int64_t lda = P.lda, ldb = P.ldb;
+    const int K = P.K;
+#pragma unroll 2
+    for (int kk = 0; kk < K; kk += 4) {
+        const int k = kk + t;
+        const bool kin = k < K;
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int m = r0 + i * 8 + g;
+            a[i] = (kin && m < M) ? __ldg(TA ? A + (int64_t)k * lda + m : A + (int64_t)m * lda + k) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = c0 + j * 8 + g;
+            b[j] = (kin && n < N) ? __ldg(TB ? B + (int64_t)n * ldb + k : B + (int64_t)k * ldb + n) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+}
+
+__global__ void __launch_bounds__(GEMM_THREADS, 3)
+gemm_warp_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restrict__ contribs,
+                 const int64_t* __restrict__ tile_start, int ntasks, int64_t ntiles, double* __restrict__ norms) {
+    __shared__ double red[GEMM_THREADS / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp >> 1, wn = warp & 1;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int ti = find_segment(tile_start, ntasks, tile);
+        const GemmTask T = tasks[ti];
+        const int64_t local = tile - tile_start[ti];
+        const int m0 = (int)(local / T.tiles_n) * BM, n0 = (int)(local % T.tiles_n) * BN;
+        const int r0 = m0 + wm * 32, c0 = n0 + wn * 32;
+        const bool live = r0 < T.M && c0 < T.N;
+        double acc[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        if (live) {
+            for (int64_t c = T.contrib_begin; c < T.contrib_end; ++c) {
+                const GemmContrib P = contribs[c];
+                if (P.K <= 0) continue;
+                switch (P.transA * 2 + P.transB) {
+                case 0: warp_contrib<0, 0>(P, T.M, T.N, r0, c0, g, t, acc); break;
+                case 1: warp_contrib<0, 1>(P, T.M, T.N, r0, c0, g, t, acc); break;
+                case 2: warp_contrib<1, 0>(P, T.M, T.N, r0, c0, g, t, acc); break;
+                default: warp_contrib<1, 1>(P, T.M, T.N, r0, c0, g, t, acc); break;
+                }
+            }
+        }
+        if (T.mode == GEMM_ADD && T.contrib_end == T.contrib_begin) continue;  // C += 0
+        const double alpha = (T.contrib_end > T.contrib_begin) ? contribs[T.contrib_begin].alpha : 1.0;
+        if (T.mode == GEMM_NORM) {
+            double ss = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int row = r0 + i * 8 + g;
+                        const int col = c0 + j * 8 + 2 * t + q;
+                        const double v = alpha * acc[i][j][q];
+                        if (row < T.M && col < T.N) ss += v * v;
+                    }
+            ss = block_sum(ss, red);
+            if (threadIdx.x == 0) norms[T.norm_base + local] = ss;
+            continue;
+        }
+        if (!live) continue;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int row = r0 + i * 8 + g;
+            if (row >= T.M) continue;
+            double* crow = T.C + (int64_t)row * T.ldc;
+            double cv[4][2];
+            if (T.mode == GEMM_ADD) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int col = c0 + j * 8 + 2 * t + q;
+                        cv[j][q] = col < T.N ? __ldcg(crow + col) : 0.0;
+                    }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int col = c0 + j * 8 + 2 * t + q;
+                    if (col < T.N) {
+                        const double v = alpha * acc[i][j][q];
+                        crow[col] = T.mode == GEMM_ADD ? cv[j][q] + v : v;
+                    }
+                }
+        }
+    }
+}
+
 constexpr int CT = 32;  // copy tile
 
 __global__ void __launch_bounds__(256)
@@ -476,13 +594,34 @@ __global__ void __launch_bounds__(128) dmma_peak_kernel(int64_t iters, double* o
 }
 
 int grid_for(int64_t ntiles, int per_sm) {
-    const int64_t cap = (int64_t)148 * per_sm;
+    const int64_t cap = (int64_t)sm_count() * per_sm;
     return (int)(ntiles < cap ? ntiles : cap);
 }
 
 }  // namespace
 
+int sm_count() {
+    static const int n = [] {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+            cudaGetLastError();
+            sms = 148;
+        }
+        return sms;
+    }();
+    return n;
+}
+
 int gemm_grid(int64_t ntiles) { return grid_for(ntiles, 2); }
+
+void launch_gemm_warp(const GemmTask* d_tasks, const GemmContrib* d_contribs, const int64_t* d_tile_start,
+                      int32_t ntasks, int64_t ntiles, double* d_norms, cudaStream_t st) {
+    if (ntiles <= 0) return;
+    gemm_warp_kernel<<<grid_for(ntiles, 12), GEMM_THREADS, 0, st>>>(d_tasks, d_contribs, d_tile_start, ntasks,
+                                                                    ntiles, d_norms);
+    count_launch();
+}
 
 void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
                        const int64_t* d_tile_start, int32_t ntasks, int64_t ntiles,

@@ -264,15 +264,7 @@ __global__ void permute_rows_kernel(const double* __restrict__ src, const int* _
     dst[e] = src[(int64_t)perm[i] * nrhs + rh];
 }
 
-int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return sms;
-}
+
 
 }  // namespace
 

@@ -73,7 +73,8 @@ struct SvdTask {         // one-sided Jacobi on the rows of R (m x n, ld n): wri
     double* U;           // sigma_j >= thresh as rows of U, sorted by sigma desc
     int32_t m, n;
     int32_t* kept_out;   // device int
-    int32_t pad_;
+    int32_t deg_off;     // != 0: kept_out[deg_off] = 1 if some sigma_j is ~0 (all m
+                         // sorted rows are written; rows kept.. complete U)
 };
 
 struct ReorthTask {      // rows k..k+kept-1 of BT: u -= V (V^T u); u /= |u|
@@ -241,6 +242,11 @@ struct GemvContrib {
 // grid of launch_gemm_tasks for ntiles tiles (d_cta_tiles, when given, holds
 // gemm_grid(ntiles)+1 tile boundaries, one range per CTA)
 int gemm_grid(int64_t ntiles);
+int sm_count();  // multiprocessors of the current device (cached)
+// short-K GEMM (same task lists, same bits as launch_gemm_tasks): fragments
+// straight from L2, one 64x64 tile per CTA, 4 CTAs per SM
+void launch_gemm_warp(const GemmTask* d_tasks, const GemmContrib* d_contribs, const int64_t* d_tile_start,
+                      int32_t ntasks, int64_t ntiles, double* d_norms, cudaStream_t st);
 void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
                        const int64_t* d_tile_start, int32_t ntasks, int64_t ntiles,
                        const int64_t* d_cta_tiles, double* d_norms, cudaStream_t st, bool short_k = false);

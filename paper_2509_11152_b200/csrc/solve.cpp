@@ -502,21 +502,22 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
     H2F_CUDA(cudaMemcpyAsync(x_dev, P.yv[0], nb, cudaMemcpyDeviceToDevice, st));
 }
 
-void refined_solve_device(H2Mat& m, Factorization& f, const double* b_dev, double* x_dev, int steps) {
-    // solve.py:63-77
+void refined_solve_device(H2Mat& m, Factorization& f, const double* b_dev, double* x_dev, int steps, int nrhs) {
+    // solve.py:63-77; nrhs > 1 refines every column at once (block matvec
+    // and block substitution; the reference's refined_solve is single-vector)
     cudaStream_t st = ctx().stream;
-    const int64_t n = f.n;
+    const int64_t n = f.n * int64_t(nrhs);
     // refinement temporaries: the factor's work region, rewound on every call
     Region& w = f.work;
     w.reset();
     double* tmp = w.alloc_n<double>(n);
     double* res = w.alloc_n<double>(n);
     double* dx = w.alloc_n<double>(n);
-    solve_device(f, b_dev, x_dev, 1);
+    solve_device(f, b_dev, x_dev, nrhs);
     for (int it = 0; it < steps; ++it) {
-        matvec_device(m, x_dev, tmp, 1);
+        matvec_device(m, x_dev, tmp, nrhs);
         launch_axpby(res, b_dev, 1.0, tmp, -1.0, n, st);
-        solve_device(f, res, dx, 1);
+        solve_device(f, res, dx, nrhs);
         launch_axpby(x_dev, x_dev, 1.0, dx, 1.0, n, st);
     }
 }

@@ -11,7 +11,7 @@ import numpy as np
 from . import _lib as L
 from .h2core import device_matrix
 
-__all__ = ["solve", "solve_multi", "refined_solve"]
+__all__ = ["solve", "solve_multi", "refined_solve", "refined_solve_multi"]
 
 
 def solve(fac, b, threads=1):
@@ -49,4 +49,21 @@ def refined_solve(h2, fac, b, threads=1, steps=1):
     x = np.empty_like(bc)
     L.check(L.lib().h2f_refined_solve(dev.handle, fac.handle.ptr, L.ptr(bc), L.ptr(x), int(steps)),
             "h2f_refined_solve")
+    return x
+
+
+def refined_solve_multi(h2, fac, b, threads=1, steps=1):
+    """refined_solve for an n x q block of right-hand sides: block
+    substitution, then `steps` rounds of (block matvec, block substitution).
+    Column j equals refined_solve(h2, fac, b[:, j]) up to rounding
+    (extension of solve.py:63-77)."""
+    b = np.asarray(b, dtype=np.float64)
+    if b.ndim != 2 or b.shape[0] != fac.n:
+        raise ValueError(f"right-hand side must have shape ({fac.n}, q)")
+    dev = device_matrix(h2)
+    bc = np.ascontiguousarray(b)
+    x = np.empty_like(bc)
+    if bc.size:
+        L.check(L.lib().h2f_refined_solve_multi(dev.handle, fac.handle.ptr, L.ptr(bc), L.ptr(x), b.shape[1],
+                                                int(steps)), "h2f_refined_solve_multi")
     return x

@@ -54,6 +54,8 @@ int main(int argc, char** argv) {
     const char* only = argc > 1 ? argv[1] : nullptr;
     std::vector<Case> cases = {
         {"schur_leaf_r13_47x47_x1", 8000, 47, 47, 1, 13, 1, 0},
+        {"schur_leaf_r13_47x47_x3", 8000, 47, 47, 3, 13, 1, 0},
+        {"schur_r24_60x60_x2", 8000, 60, 60, 2, 24, 1, 0},
         {"schur_r10_64x64_x6", 8000, 64, 64, 6, 10, 1, 0},
         {"schur_r8_48x48_x4", 8000, 48, 48, 4, 8, 1, 0},
         {"schur_r40_110x110_x2", 3000, 110, 110, 2, 40, 1, 0},
@@ -125,33 +127,46 @@ int main(int argc, char** argv) {
         // reference
         naive_kernel<<<dim3(64, cs.ntargets), 256>>>(dT, dCs, cs.ntargets, dRef, dOff);
         CK(cudaDeviceSynchronize());
-        // timed: C = 0 + sum
+        // timed: C = 0 + sum, each kernel variant (0: 3-stage smem pipeline,
+        // 1: C-prefetch pipeline, 2: register-direct short-K)
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         const int reps = 20;
-        float best = 1e30f;
-        for (int r = 0; r < reps; ++r) {
-            CK(cudaMemcpy(dC, dC0, csz * cs.ntargets * 8, cudaMemcpyDeviceToDevice));
-            cudaEventRecord(e0);
-            launch_gemm_tasks(dT, dCs, dS, int(tasks.size()), start.back(), nullptr, nullptr, 0);
-            cudaEventRecord(e1);
-            CK(cudaEventSynchronize(e1));
-            float ms;
-            cudaEventElapsedTime(&ms, e0, e1);
-            best = std::min(best, ms);
+        std::vector<double> first;
+        for (int variant = 0; variant < 3; ++variant) {
+            float best = 1e30f;
+            for (int r = 0; r < reps; ++r) {
+                CK(cudaMemcpy(dC, dC0, csz * cs.ntargets * 8, cudaMemcpyDeviceToDevice));
+                cudaEventRecord(e0);
+                if (variant == 2)
+                    launch_gemm_warp(dT, dCs, dS, int(tasks.size()), start.back(), nullptr, 0);
+                else
+                    launch_gemm_tasks(dT, dCs, dS, int(tasks.size()), start.back(), nullptr, nullptr, 0,
+                                      variant == 1);
+                cudaEventRecord(e1);
+                CK(cudaEventSynchronize(e1));
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                best = std::min(best, ms);
+            }
+            std::vector<double> c(csz * cs.ntargets), ref(csz * cs.ntargets);
+            CK(cudaMemcpy(c.data(), dC, c.size() * 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(ref.data(), dRef, ref.size() * 8, cudaMemcpyDeviceToHost));
+            double err = 0, nrm = 0;
+            for (size_t i = 0; i < c.size(); ++i) {
+                err = std::max(err, std::fabs(c[i] - ref[i]));
+                nrm = std::max(nrm, std::fabs(ref[i]));
+            }
+            bool same = true;
+            if (variant == 0) first = c;
+            else same = (c == first);
+            const double flops = 2.0 * cs.M * cs.N * cs.K * double(npairs);
+            const double bytes = 16.0 * csz * cs.ntargets;
+            std::printf("%-28s v%d %8.3f ms  %7.2f TF/s  C-rmw %7.1f GB/s  rel.err %.2e  bits==v0 %d\n",
+                        cs.name.c_str(), variant, best, flops / best / 1e9, bytes / best / 1e6, err / nrm,
+                        int(same));
         }
-        std::vector<double> c(csz * cs.ntargets), ref(csz * cs.ntargets);
-        CK(cudaMemcpy(c.data(), dC, c.size() * 8, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(ref.data(), dRef, ref.size() * 8, cudaMemcpyDeviceToHost));
-        double err = 0, nrm = 0;
-        for (size_t i = 0; i < c.size(); ++i) {
-            err = std::max(err, std::fabs(c[i] - ref[i]));
-            nrm = std::max(nrm, std::fabs(ref[i]));
-        }
-        const double flops = 2.0 * cs.M * cs.N * cs.K * double(npairs);
-        std::printf("%-28s %8.3f ms  %7.2f TF/s  rel.err %.2e\n", cs.name.c_str(), best, flops / best / 1e9,
-                    err / nrm);
         cudaFree(dAB);
         cudaFree(dC);
         cudaFree(dC0);

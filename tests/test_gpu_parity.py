@@ -223,6 +223,29 @@ def test_large_n_path_matches_shared_memory_path(case, monkeypatch):
 
 
 @pytest.mark.parametrize("case", ["cov2d_4096", "cov3d_2048"])
+def test_householder_complement_path_matches_jacobi_completion(case, monkeypatch):
+    """Q~'s leading columns come from the Jacobi's complete U (V_perp U_rest)
+    by default and from a second complete Householder QR as the fallback
+    (H2F_COMPLEMENT_QR=1, also used for numerically rank-deficient fill):
+    both are orthonormal completions, the structure is the reference's and
+    the solutions agree to the factor tolerance."""
+    g = load(case)
+    _, _, _, h2, prm = problem(case)
+    monkeypatch.setenv("H2F_COMPLEMENT_QR", "1")
+    fac_q = H.factorize(h2, prm["eps_lu"])
+    monkeypatch.delenv("H2F_COMPLEMENT_QR")
+    _, _, fac = gpu_factor(case)
+    assert structure_of(fac_q) == golden_structure(g) == structure_of(fac)
+    for rec in fac_q.records[:2]:
+        for f in rec.factors.values():
+            assert np.abs(f.q.T @ f.q - np.eye(f.q.shape[0])).max() <= 1e-12 * f.q.shape[0]
+    b = rhs(h2, H.matvec)
+    x1 = H.refined_solve(h2, fac_q, b)
+    x2 = H.refined_solve(h2, fac, b)
+    assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x2)
+
+
+@pytest.mark.parametrize("case", ["cov2d_4096", "cov3d_2048"])
 def test_blocked_lu_and_dmma_trsm_paths(case, monkeypatch):
     """Force the large-r elimination kernels (cooperative-panel LU, blocked
     DMMA TRSM; used for r > 192 / r >= 48) onto every cluster: pivots and the
