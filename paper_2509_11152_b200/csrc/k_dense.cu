@@ -138,19 +138,25 @@ __device__ __forceinline__ int jac_rotate_cached(double* __restrict__ x, double*
     const double d = b - a;
     const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(d * d + 4.0 * g * g));
     const double c = rsqrt(1.0 + t * t), sn = c * t;
-    double ax = 0.0, by = 0.0;
     for (int i = lane; i < n; i += 32) {
         const double u = x[i], v = y[i];
-        const double xu = c * u - sn * v, yv = sn * u + c * v;
-        x[i] = xu;
-        y[i] = yv;
-        ax += xu * xu;
-        by += yv * yv;
+        x[i] = c * u - sn * v;
+        y[i] = sn * u + c * v;
     }
     double a2 = a - t * g, b2 = b + t * g;
+    // the FP64 pipe bounds this loop: the norms are recomputed from the rotated
+    // rows (a second pass) only when the update formula loses accuracy
     const bool ra = !(a2 >= a * (1.0 / 64.0)), rb = !(b2 >= b * (1.0 / 64.0));
-    if (ra) a2 = warp_sum(ax);
-    if (rb) b2 = warp_sum(by);
+    if (ra | rb) {
+        __syncwarp();
+        double ax = 0.0, by = 0.0;
+        for (int i = lane; i < n; i += 32) {
+            ax += x[i] * x[i];
+            by += y[i] * y[i];
+        }
+        if (ra) a2 = warp_sum(ax);
+        if (rb) b2 = warp_sum(by);
+    }
     a = a2;
     b = b2;
     return code;
@@ -593,19 +599,24 @@ __device__ __forceinline__ int jac_rotate_split(double* __restrict__ x, double* 
     const double d = b - a;
     const double t = (d >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(d) + sqrt(d * d + 4.0 * g * g));
     const double c = rsqrt(1.0 + t * t), sn = c * t;
-    double ax = 0.0, by = 0.0;
     for (int i = i0 + lane; i < i1; i += 32) {
         const double u = x[i], v = y[i];
-        const double xu = c * u - sn * v, yv = sn * u + c * v;
-        x[i] = xu;
-        y[i] = yv;
-        ax += xu * xu;
-        by += yv * yv;
+        x[i] = c * u - sn * v;
+        y[i] = sn * u + c * v;
     }
     double a2 = a - t * g, b2 = b + t * g;
+    // rare exact recompute (second pass over the slice), uniform over the group
     const bool ra = !(a2 >= a * (1.0 / 64.0)), rb = !(b2 >= b * (1.0 / 64.0));
-    if (ra) a2 = group_sum(ax);
-    if (rb) b2 = group_sum(by);
+    if (ra | rb) {
+        __syncwarp();
+        double ax = 0.0, by = 0.0;
+        for (int i = i0 + lane; i < i1; i += 32) {
+            ax += x[i] * x[i];
+            by += y[i] * y[i];
+        }
+        if (ra) a2 = group_sum(ax);
+        if (rb) b2 = group_sum(by);
+    }
     a = a2;
     b = b2;
     return code;
@@ -1232,14 +1243,29 @@ int jacobi_coop_capacity(int max_n, int max_m) {
 
 
 int jacobi_block_rows(int n) {
-    // H2F_JACOBI_JB4_MIN_N: use 4-row blocks (twice the CTAs per task) from this n on
+    // H2F_JACOBI_JB: force the rows per block (4, 8 or 16: one warp per row
+    // pair, measured slower on config-2 shapes: the FP64 pipe of the fewer
+    // CTAs saturates); default 8, 4 from H2F_JACOBI_JB4_MIN_N
+    static const int forced = [] {
+        const char* e = std::getenv("H2F_JACOBI_JB");
+        return e ? std::atoi(e) : 0;
+    }();
     static const int jb4_min = [] {
         const char* e = std::getenv("H2F_JACOBI_JB4_MIN_N");
         return e ? std::atoi(e) : 512;
     }();
+    auto fits = [n](int jb) { return size_t(2 * jb) * n * 8 <= size_t(220) * 1024; };
+    if ((forced == 16 || forced == 8 || forced == 4) && fits(forced)) return forced;
     if (n >= jb4_min) return 4;
-    return (size_t(16) * n * 8 <= size_t(200) * 1024) ? 8 : 4;
+    return fits(8) ? 8 : 4;
 }
+
+namespace {
+const void* jacobi_block_fn(int jb) {
+    return jb == 16 ? (const void*)jacobi_block_kernel<16>
+                    : jb == 8 ? (const void*)jacobi_block_kernel<8> : (const void*)jacobi_block_kernel<4>;
+}
+}  // namespace
 
 size_t jacobi_block_smem(int max_n, int max_m) {
     const int jb = jacobi_block_rows(max_n);
@@ -1248,7 +1274,7 @@ size_t jacobi_block_smem(int max_n, int max_m) {
 
 int jacobi_block_capacity(int max_n, int max_m) {
     const size_t smem = jacobi_block_smem(max_n, max_m);
-    const void* fn = jacobi_block_rows(max_n) == 8 ? (const void*)jacobi_block_kernel<8> : (const void*)jacobi_block_kernel<4>;
+    const void* fn = jacobi_block_fn(jacobi_block_rows(max_n));
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0, dev = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, JBT, smem);
@@ -1261,7 +1287,7 @@ cudaError_t launch_jacobi_block(const CoopSvdTask* d_tasks, int32_t total_ctas, 
                                 int32_t max_n, int32_t max_m, double thresh, cudaStream_t st) {
     if (total_ctas <= 0) return cudaSuccess;
     const size_t smem = jacobi_block_smem(max_n, max_m);
-    const void* fn = jacobi_block_rows(max_n) == 8 ? (const void*)jacobi_block_kernel<8> : (const void*)jacobi_block_kernel<4>;
+    const void* fn = jacobi_block_fn(jacobi_block_rows(max_n));
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {(void*)&d_tasks, (void*)&d_cta_task, (void*)&thresh};
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(total_ctas), dim3(JBT), args, smem, st);

@@ -61,14 +61,14 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
 // pointer stride, so the per-copy cost is one cp.async plus one add; VEC
 // moves 16-byte pairs when the operand is 16-byte aligned.  Out-of-range
 // elements are zero-filled (src-size 0/8), so tails contribute exact zeros.
-template <bool KMAJOR, bool VEC>
+template <bool KMAJOR, bool VEC, int NT>
 __device__ __forceinline__ void stage_operand(const double* __restrict__ X, int64_t ld, int K, int R, int r0, int k0,
                                               double* __restrict__ S) {
     const int tid = threadIdx.x;
     if (!KMAJOR) {
         constexpr int W = VEC ? 2 : 1;             // doubles per copy
         constexpr int PER_ROW = BK2 / W;           // copies per tile row
-        constexpr int ROWS_STEP = GEMM_THREADS / PER_ROW;
+        constexpr int ROWS_STEP = NT / PER_ROW;
         const int kc = (tid % PER_ROW) * W, rb = tid / PER_ROW;
         const int kv = K - k0 - kc;                // valid k in this copy (<= 0: none)
         const int bytes = kv >= W ? 8 * W : (kv > 0 ? 8 * kv : 0);
@@ -84,7 +84,7 @@ __device__ __forceinline__ void stage_operand(const double* __restrict__ X, int6
     } else {
         constexpr int W = VEC ? 2 : 1;
         constexpr int PER_K = 64 / W;               // copies per k row
-        constexpr int K_STEP = GEMM_THREADS / PER_K;
+        constexpr int K_STEP = NT / PER_K;
         const int rc = (tid % PER_K) * W, kb = tid / PER_K;
         const int rv = R - r0 - rc;
         const int bytes = rv >= W ? 8 * W : (rv > 0 ? 8 * rv : 0);
@@ -100,54 +100,57 @@ __device__ __forceinline__ void stage_operand(const double* __restrict__ X, int6
     }
 }
 
-template <bool KMAJOR>
+template <bool KMAJOR, int NT>
 __device__ __forceinline__ void stage_any(const double* X, int64_t ld, int K, int R, int r0, int k0, double* S) {
     const bool vec = ((reinterpret_cast<uintptr_t>(X) | (uintptr_t)(ld * 8)) & 15) == 0;
-    if (vec) stage_operand<KMAJOR, true>(X, ld, K, R, r0, k0, S);
-    else stage_operand<KMAJOR, false>(X, ld, K, R, r0, k0, S);
+    if (vec) stage_operand<KMAJOR, true, NT>(X, ld, K, R, r0, k0, S);
+    else stage_operand<KMAJOR, false, NT>(X, ld, K, R, r0, k0, S);
 }
 
 // stage one BK2 chunk of contribution P (k offset k0) into As/Bs
+template <int NT>
 __device__ __forceinline__ void stage_chunk(const GemmContrib& P, int M, int N, int m0, int n0, int k0,
                                             double* As, double* Bs) {
-    if (P.transA) stage_any<true>(P.A, P.lda, P.K, M, m0, k0, As);   // stored K x M: [k][m]
-    else stage_any<false>(P.A, P.lda, P.K, M, m0, k0, As);           // stored M x K: [m][k]
-    if (P.transB) stage_any<false>(P.B, P.ldb, P.K, N, n0, k0, Bs);  // stored N x K: [n][k]
-    else stage_any<true>(P.B, P.ldb, P.K, N, n0, k0, Bs);            // stored K x N: [k][n]
+    if (P.transA) stage_any<true, NT>(P.A, P.lda, P.K, M, m0, k0, As);   // stored K x M: [k][m]
+    else stage_any<false, NT>(P.A, P.lda, P.K, M, m0, k0, As);           // stored M x K: [m][k]
+    if (P.transB) stage_any<false, NT>(P.B, P.ldb, P.K, N, n0, k0, Bs);  // stored N x K: [n][k]
+    else stage_any<true, NT>(P.B, P.ldb, P.K, N, n0, k0, Bs);            // stored K x N: [k][n]
 }
 
-template <bool TA, bool TB>
+// warp tile 32 x (8 NJ): NJ = 4 for 4 warps per 64x64 tile (2 x 2 warps),
+// NJ = 2 for 8 warps (2 x 4 warps, twice the warps per SM for the DMMA pipe)
+template <bool TA, bool TB, int NJ>
 __device__ __forceinline__ void mma_kstep(const double* __restrict__ As, const double* __restrict__ Bs,
-                                          double (&acc)[4][4][2], int wm, int wn, int g, int t, int kk) {
-    double a[4], b[4];
+                                          double (&acc)[4][NJ][2], int wm, int wn, int g, int t, int kk) {
+    double a[4], b[NJ];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int m = wm * 32 + i * 8 + g;
         a[i] = TA ? As[(kk + t) * LDM2 + m] : As[m * LDK2 + kk + t];
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int n = wn * 32 + j * 8 + g;
+    for (int j = 0; j < NJ; ++j) {
+        const int n = wn * (8 * NJ) + j * 8 + g;
         b[j] = TB ? Bs[n * LDK2 + kk + t] : Bs[(kk + t) * LDM2 + n];
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
 }
 
 // kvalid: k steps of the chunk that carry data (the last chunk of a
 // contribution is zero-filled past K; its zero steps are skipped).  Full
 // chunks take the straight-line path so the fragment loads of step k+1
 // overlap the DMMAs of step k.
-template <bool TA, bool TB>
+template <bool TA, bool TB, int NJ>
 __device__ __forceinline__ void mma_chunk(const double* __restrict__ As, const double* __restrict__ Bs,
-                                          double (&acc)[4][4][2], int wm, int wn, int g, int t, int kvalid) {
+                                          double (&acc)[4][NJ][2], int wm, int wn, int g, int t, int kvalid) {
     if (kvalid >= BK2) {
 #pragma unroll
-        for (int kk = 0; kk < BK2; kk += 4) mma_kstep<TA, TB>(As, Bs, acc, wm, wn, g, t, kk);
+        for (int kk = 0; kk < BK2; kk += 4) mma_kstep<TA, TB, NJ>(As, Bs, acc, wm, wn, g, t, kk);
     } else {
-        for (int kk = 0; kk < kvalid; kk += 4) mma_kstep<TA, TB>(As, Bs, acc, wm, wn, g, t, kk);
+        for (int kk = 0; kk < kvalid; kk += 4) mma_kstep<TA, TB, NJ>(As, Bs, acc, wm, wn, g, t, kk);
     }
 }
 
@@ -172,20 +175,23 @@ struct ChunkMeta {
 // shared memory (cp.async) when the tile's first chunk is consumed, so its
 // read latency overlaps the tile's math instead of the epilogue (pays off for
 // short-K tiles, where the read-modify-write of C dominates)
-template <int NS, bool PREC>
-__global__ void __launch_bounds__(GEMM_THREADS, 2)
+template <int NS, bool PREC, int NT>
+__global__ void __launch_bounds__(NT, 2)
 gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restrict__ contribs,
                   const int64_t* __restrict__ tile_start, int ntasks, int64_t ntiles,
                   const int64_t* __restrict__ cta_tiles, double* __restrict__ norms) {
     constexpr int STAGES = NS;
+    constexpr int NW = NT / 32;          // warps: 2 x (NW/2) over the 64x64 tile
+    constexpr int NJ = 16 / NW;          // 8-column fragments per warp (4 or 2)
+    constexpr int WN = 8 * NJ;           // warp tile width
     extern __shared__ __align__(16) double gsm[];
-    __shared__ double red[GEMM_THREADS / 32];
+    __shared__ double red[NW];
     __shared__ ChunkMeta meta[STAGES];
     double* Cs = gsm + 2 * STAGES * STAGE_ELEMS;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int wm = warp >> 1, wn = warp & 1;
+    const int wm = warp / (NW / 2), wn = warp % (NW / 2);
 
     // tile range of this CTA: host cost-balanced boundaries (tiles differ in
     // their number of K chunks by orders of magnitude), else an even split
@@ -249,7 +255,7 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
             m.local = p_local;
             const int len0 = min(BK2, P.K - p_pk);
             const int total = len0;
-            stage_chunk(P, p_M, p_N, p_m0, p_n0, m.k0, As, As + STAGE_ELEMS);
+            stage_chunk<NT>(P, p_M, p_N, p_m0, p_n0, m.k0, As, As + STAGE_ELEMS);
             p_pk += len0;
             if (p_pk >= P.K) {
                 p_pk = 0;
@@ -267,11 +273,11 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
         cp_async_commit();
     };
 
-    double acc[4][4][2];
+    double acc[4][NJ][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) issue(st);
@@ -290,23 +296,25 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
                 const bool vec = ((reinterpret_cast<uintptr_t>(T.C) | (uintptr_t)(T.ldc * 8)) & 15) == 0;
                 const int rmax = T.M - m.m0;
                 if (vec) {
+                    constexpr int RS = NT / 32;
                     const int c2 = (threadIdx.x & 31) * 2, rb = threadIdx.x >> 5;
                     const int cv = T.N - m.n0 - c2;
                     const int bytes = cv >= 2 ? 16 : (cv > 0 ? 8 : 0);
                     const double* src = T.C + (int64_t)(m.m0 + rb) * T.ldc + m.n0 + c2;
 #pragma unroll
-                    for (int r = 0; r < BM; r += 4) {
+                    for (int r = 0; r < BM; r += RS) {
                         cp_async<16>(Cs + (r + rb) * LDC + c2, src, r + rb < rmax ? bytes : 0);
-                        src += 4 * T.ldc;
+                        src += RS * T.ldc;
                     }
                 } else {
+                    constexpr int RS = NT / 64;
                     const int c1 = threadIdx.x & 63, rb = threadIdx.x >> 6;
                     const int bytes = c1 < T.N - m.n0 ? 8 : 0;
                     const double* src = T.C + (int64_t)(m.m0 + rb) * T.ldc + m.n0 + c1;
 #pragma unroll 8
-                    for (int r = 0; r < BM; r += 2) {
+                    for (int r = 0; r < BM; r += RS) {
                         cp_async<8>(Cs + (r + rb) * LDC + c1, src, r + rb < rmax ? bytes : 0);
-                        src += 2 * T.ldc;
+                        src += RS * T.ldc;
                     }
                 }
                 cp_async_commit();
@@ -319,10 +327,10 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
             // k slots past the chunk's data hold zeros: skip them
             const int kv = m.kv;
             switch (P.transA * 2 + P.transB) {
-            case 0: mma_chunk<false, false>(As, Bs, acc, wm, wn, g, t, kv); break;
-            case 1: mma_chunk<false, true>(As, Bs, acc, wm, wn, g, t, kv); break;
-            case 2: mma_chunk<true, false>(As, Bs, acc, wm, wn, g, t, kv); break;
-            default: mma_chunk<true, true>(As, Bs, acc, wm, wn, g, t, kv); break;
+            case 0: mma_chunk<false, false, NJ>(As, Bs, acc, wm, wn, g, t, kv); break;
+            case 1: mma_chunk<false, true, NJ>(As, Bs, acc, wm, wn, g, t, kv); break;
+            case 2: mma_chunk<true, false, NJ>(As, Bs, acc, wm, wn, g, t, kv); break;
+            default: mma_chunk<true, true, NJ>(As, Bs, acc, wm, wn, g, t, kv); break;
             }
         }
         if (!m.last) continue;
@@ -335,11 +343,11 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < NJ; ++j)
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         const int row = m.m0 + wm * 32 + i * 8 + g;
-                        const int col = m.n0 + wn * 32 + j * 8 + 2 * t + q;
+                        const int col = m.n0 + wn * WN + j * 8 + 2 * t + q;
                         const double v = alpha * acc[i][j][q];
                         if (row < T.M && col < T.N) ss += v * v;
                     }
@@ -350,27 +358,27 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
             // all loads of the tile's C first (one memory round trip), then
             // the stores: the compiler cannot hoist loads over possibly
             // aliasing stores on its own
-            double cv[4][4][2];
+            double cv[4][NJ][2];
             if (PREC && T.mode == GEMM_ADD) {
                 cp_async_wait<0>();
                 __syncthreads();
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
+                    for (int j = 0; j < NJ; ++j)
 #pragma unroll
                         for (int q = 0; q < 2; ++q)
-                            cv[i][j][q] = Cs[(wm * 32 + i * 8 + g) * LDC + wn * 32 + j * 8 + 2 * t + q];
+                            cv[i][j][q] = Cs[(wm * 32 + i * 8 + g) * LDC + wn * WN + j * 8 + 2 * t + q];
             } else if (T.mode == GEMM_ADD) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int row = m.m0 + wm * 32 + i * 8 + g;
                     const double* crow = T.C + (int64_t)row * T.ldc;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
+                    for (int j = 0; j < NJ; ++j)
 #pragma unroll
                         for (int q = 0; q < 2; ++q) {
-                            const int col = m.n0 + wn * 32 + j * 8 + 2 * t + q;
+                            const int col = m.n0 + wn * WN + j * 8 + 2 * t + q;
                             cv[i][j][q] = (row < T.M && col < T.N) ? crow[col] : 0.0;
                         }
                 }
@@ -381,10 +389,10 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
                 if (row >= T.M) continue;
                 double* crow = T.C + (int64_t)row * T.ldc;
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < NJ; ++j)
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
-                        const int col = m.n0 + wn * 32 + j * 8 + 2 * t + q;
+                        const int col = m.n0 + wn * WN + j * 8 + 2 * t + q;
                         if (col < T.N) {
                             const double v = alpha * acc[i][j][q];
                             crow[col] = T.mode == GEMM_ADD ? cv[i][j][q] + v : v;
@@ -395,7 +403,7 @@ gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restr
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     }
     cp_async_wait<0>();
 }
@@ -629,20 +637,43 @@ void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
     if (ntiles <= 0) return;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(gemm_tasks_kernel<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(gemm_tasks_kernel<3, false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)gemm_smem<3, false>());
-        cudaFuncSetAttribute(gemm_tasks_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(gemm_tasks_kernel<2, true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)gemm_smem<2, true>());
+        cudaFuncSetAttribute(gemm_tasks_kernel<3, false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)gemm_smem<3, false>());
+        cudaFuncSetAttribute(gemm_tasks_kernel<2, true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)gemm_smem<2, true>());
         configured = true;
     }
     static const bool force_prec = std::getenv("H2F_GEMM_PREC") != nullptr;
     static const bool no_prec = std::getenv("H2F_GEMM_NOPREC") != nullptr;
-    if ((short_k || force_prec) && !no_prec)
-        gemm_tasks_kernel<2, true><<<gemm_grid(ntiles), GEMM_THREADS, gemm_smem<2, true>(), st>>>(
-            d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_cta_tiles, d_norms);
-    else
-        gemm_tasks_kernel<3, false><<<gemm_grid(ntiles), GEMM_THREADS, gemm_smem<3, false>(), st>>>(
-            d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_cta_tiles, d_norms);
+    // CTA width: 4 warps of 32x32 (default); H2F_GEMM_NT=256 runs 8 warps of
+    // 32x16 on the same tile (measured 5-10% slower on the factorization's
+    // shapes: the DMMA inner loop alone reaches 36.8 TF/s at 8 warps/SM,
+    // profiles/r02_dmma_probe.txt, the losses are in the chunk pipeline)
+    static const int nt = [] {
+        const char* e = std::getenv("H2F_GEMM_NT");
+        return e && std::atoi(e) == 256 ? 256 : 128;
+    }();
+    const bool prec = (short_k || force_prec) && !no_prec;
+    const int grid = gemm_grid(ntiles);
+    if (nt == 256) {
+        if (prec)
+            gemm_tasks_kernel<2, true, 256><<<grid, 256, gemm_smem<2, true>(), st>>>(
+                d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_cta_tiles, d_norms);
+        else
+            gemm_tasks_kernel<3, false, 256><<<grid, 256, gemm_smem<3, false>(), st>>>(
+                d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_cta_tiles, d_norms);
+    } else {
+        if (prec)
+            gemm_tasks_kernel<2, true, 128><<<grid, 128, gemm_smem<2, true>(), st>>>(
+                d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_cta_tiles, d_norms);
+        else
+            gemm_tasks_kernel<3, false, 128><<<grid, 128, gemm_smem<3, false>(), st>>>(
+                d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_cta_tiles, d_norms);
+    }
     count_launch();
 }
 
