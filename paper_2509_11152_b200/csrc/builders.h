@@ -131,10 +131,11 @@ struct GemmBuild {
             const char* e = std::getenv("H2F_GEMM_WARP_KMAX");
             return e ? std::atof(e) : 40.0;
         }();
+        const int role = kid == K_GEMM_SCHUR ? 1 : 0;
         if (keff < kwarp)
-            launch_gemm_warp(dt, dc, ds, int32_t(tasks.size()), ntiles, norms, X.stream);
+            launch_gemm_warp(dt, dc, ds, int32_t(tasks.size()), ntiles, norms, X.stream, role);
         else
-            launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), ntiles, dcta, norms, X.stream, keff < kmax);
+            launch_gemm_tasks(dt, dc, ds, int32_t(tasks.size()), ntiles, dcta, norms, X.stream, keff < kmax, role);
     }
 };
 

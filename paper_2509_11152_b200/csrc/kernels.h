@@ -246,10 +246,12 @@ int sm_count();  // multiprocessors of the current device (cached)
 // short-K GEMM (same task lists, same bits as launch_gemm_tasks): fragments
 // straight from L2, one 64x64 tile per CTA, 4 CTAs per SM
 void launch_gemm_warp(const GemmTask* d_tasks, const GemmContrib* d_contribs, const int64_t* d_tile_start,
-                      int32_t ntasks, int64_t ntiles, double* d_norms, cudaStream_t st);
+                      int32_t ntasks, int64_t ntiles, double* d_norms, cudaStream_t st, int role = 0);
+// role 1 = the Schur-complement launches (a separate kernel symbol, same code)
 void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
                        const int64_t* d_tile_start, int32_t ntasks, int64_t ntiles,
-                       const int64_t* d_cta_tiles, double* d_norms, cudaStream_t st, bool short_k = false);
+                       const int64_t* d_cta_tiles, double* d_norms, cudaStream_t st, bool short_k = false,
+                       int role = 0);
 void launch_copy_tasks(const CopyTask* d_tasks, const int64_t* d_tile_start, int32_t ntasks,
                        int64_t ntiles, cudaStream_t st);
 void launch_qr_r_smem(const QrTask* d_tasks, int32_t ntasks, int32_t max_n, cudaStream_t st);
