@@ -17,6 +17,7 @@ Reference behaviour restated (file:line under /root/reference/pkg/src/h2factor):
   Chebyshev bases      h2core.py:39-94
   build_h2             h2core.py:128-174
   recompression        h2core.py:177-269
+  low-rank update      h2core.py:333-392 (absorb_low_rank), kernels.py:89-96
 """
 
 from __future__ import annotations
@@ -45,6 +46,8 @@ __all__ = [
     "h2_nbytes",
     "build_problem",
     "rhs_for",
+    "make_low_rank_factor",
+    "absorb_low_rank",
 ]
 
 # --------------------------------------------------------------------------
@@ -64,6 +67,11 @@ PROBLEMS = {
     "helmholtz3d": dict(family="helmholtz3d", dim=3, m=64, p0=4, eta=0.7,
                         alpha_r=1e-2, eps=1e-7, eps_lu=1e-6, corr_length=0.1,
                         kappa=3.0),
+    # 3D covariance with a seeded rank-32 symmetric update W W^T folded into
+    # the representation before factorization (harness.py:68-70, 185-189)
+    "lru_cov3d": dict(family="exp_covariance", dim=3, m=128, p0=4, eta=0.9,
+                      alpha_r=1e-2, eps=1e-8, eps_lu=1e-7, corr_length=0.2,
+                      kappa=3.0, lru_rank=32),
 }
 
 
@@ -539,6 +547,64 @@ def orthogonalize_recompress(h2, eps):
     return h2
 
 
+# --------------------------------------------------------------------------
+# symmetric low-rank update (h2core.py:333-392, kernels.py:89-96)
+# --------------------------------------------------------------------------
+
+def make_low_rank_factor(n, rank, seed):
+    """n x rank Philox(seed) normals / sqrt(n) (kernels.py:89-96)."""
+    return np.random.Generator(np.random.Philox(seed)).standard_normal((n, rank)) / np.sqrt(n)
+
+
+def _range_basis(resid, scale):
+    # orthonormal basis of resid's numerically significant range
+    if resid.shape[1] == 0:
+        return np.zeros((resid.shape[0], 0))
+    u, sig, _ = np.linalg.svd(resid, full_matrices=False)
+    return u[:, :int(np.sum(sig > 1e-12 * max(scale, 1e-300)))]
+
+
+def absorb_low_rank(h2, w, eps):
+    """A <- A + W W^T inside the H2 representation, in place, then
+    recompression at eps.  Dense blocks take the explicit term; every
+    cluster's basis is widened (bottom-up, in coefficient space above the
+    leaves) until it reproduces its rows of W exactly, and the coupling
+    blocks take the projected cross terms."""
+    w = np.asarray(w, dtype=np.float64)
+    if w.ndim != 2 or w.shape[0] != h2.n:
+        raise ValueError("update factor must be n x r")
+    tree, part = h2.tree, h2.partition
+    for (s, t) in list(h2.dense):
+        h2.dense[(s, t)] = h2.dense[(s, t)] + w[tree.begin[s]:tree.end[s]] @ w[tree.begin[t]:tree.end[t]].T
+    if part.top_level is None:
+        return h2
+    coef = {}     # cluster -> its rows of W in its (widened) basis coordinates
+    for lv in range(tree.depth, part.top_level - 1, -1):
+        widened = {}
+        for c in tree.levels[lv]:
+            if tree.is_leaf(c):
+                rows = w[tree.begin[c]:tree.end[c]]
+            else:
+                a, b = tree.children(c)
+                rows = np.vstack([coef[a], coef[b]])
+            basis = _stacked_basis(h2, c)
+            inside = basis.T @ rows
+            extra = _range_basis(rows - basis @ inside, float(np.linalg.norm(rows)))
+            _store_basis(h2, c, np.hstack([basis, extra]))
+            h2.rank[c] += extra.shape[1]
+            widened[c] = extra.shape[1]
+            coef[c] = np.vstack([inside, extra.T @ rows])
+        for c in tree.levels[lv]:
+            if widened[c] and c in h2.transfer:
+                t = h2.transfer[c]
+                h2.transfer[c] = np.vstack([t, np.zeros((widened[c], t.shape[1]))])
+    for (s, t), blk in list(h2.coupling.items()):
+        grown = np.zeros((h2.rank[s], h2.rank[t]))
+        grown[:blk.shape[0], :blk.shape[1]] = blk
+        h2.coupling[(s, t)] = grown + coef[s] @ coef[t].T
+    return orthogonalize_recompress(h2, eps)
+
+
 def h2_nbytes(h2):
     return sum(blk.nbytes for store in
                (h2.leaf_basis, h2.transfer, h2.coupling, h2.dense)
@@ -564,7 +630,14 @@ def build_problem(name, n, **overrides):
         return _build(prm, n)
 
 
+# wall seconds of the last build's stages (construction, compression and,
+# for the low-rank row, the update) -- the harness reports them separately
+LAST_BUILD_TIMINGS = {}
+
+
 def _build(prm, n):
+    import time
+    t0 = time.perf_counter()
     points, counts = generate_uniform_grid(n, prm["dim"])
     h = 1.0 / max(counts)
     tree = build_cluster_tree(points, prm["m"])
@@ -574,7 +647,14 @@ def _build(prm, n):
                       diag_value=default_diag_value(prm["family"], h),
                       alpha_r=prm["alpha_r"])
     h2 = build_h2(tree, part, spec, prm["p0"])
+    t1 = time.perf_counter()
     h2 = orthogonalize_recompress(h2, prm["eps"])
+    t2 = time.perf_counter()
+    LAST_BUILD_TIMINGS.clear()
+    LAST_BUILD_TIMINGS.update(construction=t1 - t0, compression=t2 - t1)
+    if prm.get("lru_rank", 0) > 0:
+        h2 = absorb_low_rank(h2, make_low_rank_factor(n, prm["lru_rank"], prm.get("seed", 7)), prm["eps"])
+        LAST_BUILD_TIMINGS["low_rank_update"] = time.perf_counter() - t2
     return tree, part, spec, h2, prm
 
 

@@ -21,9 +21,9 @@ import numpy as np  # noqa: E402
 
 import h2factor.factorization as fz  # noqa: E402
 from h2factor.geometry import build_cluster_tree, generate_uniform_grid  # noqa: E402
-from h2factor.h2core import build_h2, matvec, orthogonalize_recompress  # noqa: E402
+from h2factor.h2core import absorb_low_rank, build_h2, matvec, orthogonalize_recompress  # noqa: E402
 from h2factor.harness import PROBLEMS  # noqa: E402
-from h2factor.kernels import KernelSpec, default_diag_value  # noqa: E402
+from h2factor.kernels import KernelSpec, default_diag_value, make_low_rank_factor  # noqa: E402
 from h2factor.solve import refined_solve, solve  # noqa: E402
 from h2factor.structure import dual_tree_traversal  # noqa: E402
 
@@ -38,6 +38,12 @@ CASES = {
     "laplace3d_4096": ("helmholtz3d", 4096, {"kappa": 0.0}),
     "osc2d_4096": ("helmholtz3d", 4096, {"dim": 2, "p0": 8, "eta": 0.9}),
     "cov3d_e8_4096": ("cov3d", 4096, {"eps_lu": 1e-8, "eps": 1e-9}),
+    # round 2: config 1 itself, the config-2 / config-3 families at 16k, the
+    # low-rank-update row
+    "cov2d_16384": ("cov2d", 16384, {}),
+    "laplace3d_16384": ("helmholtz3d", 16384, {"kappa": 0.0}),
+    "cov3d_e8_16384": ("cov3d", 16384, {"eps_lu": 1e-8, "eps": 1e-9}),
+    "lru_cov3d_4096": ("lru_cov3d", 4096, {}),
 }
 
 
@@ -61,6 +67,8 @@ def build(problem, n, over):
                       diag_value=default_diag_value(prm["family"], 1.0 / max(counts)),
                       alpha_r=prm["alpha_r"])
     h2 = orthogonalize_recompress(build_h2(tree, part, spec, prm["p0"]), prm["eps"])
+    if prm.get("lru_rank", 0) > 0:  # harness.py:185-189, seed 7
+        h2 = absorb_low_rank(h2, make_low_rank_factor(n, prm["lru_rank"], 7), prm["eps"])
     return h2, prm
 
 

@@ -19,8 +19,9 @@ from oracle import h2_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-ROBUST = ["cov2d_1024", "cov3d_2048", "cov2d_4096", "cov3d_e8_4096"]
-SENSITIVE = ["laplace2d_2048", "helmholtz3d_2048", "laplace3d_4096", "osc2d_4096"]
+ROBUST = ["cov2d_1024", "cov3d_2048", "cov2d_4096", "cov3d_e8_4096", "cov2d_16384", "cov3d_e8_16384"]
+SENSITIVE = ["laplace2d_2048", "helmholtz3d_2048", "laplace3d_4096", "osc2d_4096", "laplace3d_16384",
+             "lru_cov3d_4096"]
 
 _fac_cache = {}
 
@@ -323,9 +324,9 @@ def test_solve_multi_block_path_matches_single_vector_path(case, q):
 def test_device_harness_report_matches_reference_schema():
     """The device harness (reference harness.run, harness.py:197-249) returns
     the reference report keys; e_b and the digest follow the GPU path."""
-    from paper_2509_11152_b200.harness import run
+    from paper_2509_11152_b200.harness import ExperimentConfig, run
 
-    rep = run("cov2d", 1024)
+    rep = run(ExperimentConfig.from_problem("cov2d", 1024))
     for key in ["version", "config", "n", "e_b", "solution_digest", "h2_bytes", "factor_bytes",
                 "kmax_construction", "kmax_factorization", "csp_max", "timings", "phases", "levels", "ranks"]:
         assert key in rep

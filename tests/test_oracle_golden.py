@@ -10,7 +10,7 @@ from golden_util import CASES, golden_structure, h2_digest, load, one_thread, pr
 from oracle import h2_oracle as O
 
 FAST = ["cov2d_1024", "cov3d_2048", "laplace2d_2048", "helmholtz3d_2048"]
-SLOW = ["cov2d_4096", "laplace3d_4096", "osc2d_4096", "cov3d_e8_4096"]
+SLOW = ["cov2d_4096", "laplace3d_4096", "osc2d_4096", "cov3d_e8_4096", "cov2d_16384", "lru_cov3d_4096"]
 
 
 @pytest.mark.parametrize("case", list(CASES))
