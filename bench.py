@@ -490,8 +490,22 @@ def h2_bytes(h2):
     return sum(b.nbytes for s in (h2.leaf_basis, h2.transfer, h2.coupling, h2.dense) for b in s.values())
 
 
-TRAFFIC_NOTE = ("null: Schur GEMM launches differ 100x in size, so one ncu capture gives no per-launch average; "
-                "dram bytes of 4 captured launches are in profiles/r01_ncu_gemm_config2.txt")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_schur_traffic.json")
+
+
+def schur_traffic():
+    """DRAM bytes per Schur GEMM launch from the committed ncu capture of one
+    config-2 factorization (scripts/schur_traffic.py: every gemm_schur launch,
+    dram__bytes_read.sum + dram__bytes_write.sum, paired with the library's
+    algorithmic bytes of the same launch)."""
+    try:
+        with open(TRAFFIC_FILE) as fh:
+            t = json.load(fh)
+        return t["dram_bytes_per_launch"], (f"ncu dram bytes per gemm_schur launch, mean over {t['paired']} launches "
+                                            f"of one config-2 factorization ({TRAFFIC_FILE[len(ROOT) + 1:]}); "
+                                            f"traffic / algorithmic bytes = {t['traffic_over_algorithmic']:.2f}")
+    except (OSError, KeyError, ValueError):
+        return None, "no committed ncu capture"
 
 
 def roofline(prof, peaks, peak_kind, dmma_tf):
@@ -506,13 +520,16 @@ def roofline(prof, peaks, peak_kind, dmma_tf):
     ridge = dmma_tf * 1e12 / (hbm * 1e9)
     if ai >= ridge:
         achieved = p["flops"] / p["seconds"] / 1e12
+        traffic, note = schur_traffic() if name == "gemm_schur" else (None, "no ncu capture for this kernel")
         return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": dmma_tf, "unit": "TFLOP/s",
-                "frac": achieved / dmma_tf, "traffic": None, "traffic_note": TRAFFIC_NOTE,
+                "frac": achieved / dmma_tf, "traffic": traffic, "traffic_note": note,
+                "algorithmic_bytes_per_launch": p["bytes"] / max(p["launches"], 1),
                 "peak_source": "FP64 DMMA m8n8k4 peak measured in this run (MEASURED_PEAKS.json has no FP64)",
                 "launches": p["launches"], "seconds": p["seconds"]}
     achieved = p["bytes"] / p["seconds"] / 1e9
     return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "traffic_note": TRAFFIC_NOTE, "peak_source": f"{peak_kind} hbm_gbs",
+            "frac": achieved / hbm, "traffic": None, "traffic_note": "no ncu capture for this kernel",
+            "peak_source": f"{peak_kind} hbm_gbs",
             "launches": p["launches"], "seconds": p["seconds"]}
 
 

@@ -203,6 +203,26 @@ int h2f_factor_cluster_arrays(h2f_factor f, int32_t rec, int32_t cluster, double
 int h2f_factor_cluster_edge(h2f_factor f, int32_t rec, int32_t cluster, int32_t e, double* mat);
 int h2f_factor_top(h2f_factor f, double* top_lu, int32_t* top_piv);
 
+/* ---- factor import (serialization) -------------------------
+ * Rebuilds a device factor from the arrays h2f_factor_level_arrays /
+ * h2f_factor_cluster_arrays / h2f_factor_cluster_edge / h2f_factor_top
+ * export (the reference has no factor format, factorization.py:130-193):
+ * begin, then every record and every cluster of it, the top, end.  mw is the
+ * cluster's r x (sum of edge widths) eliminator block, edges in order.  The
+ * imported factor solves exactly like the exported one. */
+int h2f_factor_import_begin(int64_t n, int32_t top_level, int32_t num_records, int64_t top_size, double eps_lu,
+                            double eps_fill, double norm_estimate, h2f_factor* out);
+int h2f_factor_import_record(h2f_factor f, int32_t rec, int32_t level, int32_t num_clusters,
+                             const int64_t* clusters, const int64_t* offsets, const int64_t* sizes,
+                             int32_t num_batches, const int64_t* batch_ptr, const int64_t* batch_ids,
+                             int64_t up_size, const int64_t* up_index, int32_t csp, int32_t ncolors,
+                             int32_t graph_degree, int32_t max_rank, double time_s);
+int h2f_factor_import_cluster(h2f_factor f, int32_t rec, int32_t cluster, int32_t s, int32_t r, const double* q,
+                              const double* lu, const int32_t* piv, int32_t num_edges, const int64_t* edge_other,
+                              const int32_t* edge_kind, const int64_t* edge_width, const double* mw);
+int h2f_factor_import_top(h2f_factor f, const double* top_lu, const int32_t* top_piv);
+int h2f_factor_import_end(h2f_factor f);
+
 /* ---- scheduling primitives (exposed for parity tests) ---------------------- */
 /* greedy colouring in ascending id order of the graph given by canonical
  * pairs over `clusters`; colors_out[i] = colour of clusters[i]. */

@@ -34,6 +34,7 @@ from .problem import (
     h2_nbytes,
     orthogonalize_recompress,
 )
+from .serialize import load_factorization, save_factorization
 from .solve import refined_solve, refined_solve_multi, solve, solve_multi
 from .structure import color_groups, greedy_coloring, level_graph, sparsity_constant
 
@@ -44,6 +45,6 @@ __all__ = [
     "H2Factorization", "H2Matrix", "KernelSpec", "LevelRecord", "PIVOT_RTOL", "PROBLEMS",
     "build_cluster_tree", "build_h2", "build_problem", "color_groups", "dual_tree_traversal",
     "estimate_norm2", "factorize", "generate_uniform_grid", "greedy_coloring", "h2_nbytes",
-    "level_graph", "matvec", "orthogonalize_recompress", "refined_solve", "refined_solve_multi", "solve", "solve_multi",
+    "level_graph", "load_factorization", "matvec", "orthogonalize_recompress", "save_factorization", "refined_solve", "refined_solve_multi", "solve", "solve_multi",
     "sparsity_constant", "__version__",
 ]

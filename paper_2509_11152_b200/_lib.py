@@ -96,6 +96,15 @@ _SIGS = {
     "h2f_refined_solve_multi": (C.c_int, [C.c_void_p, C.c_void_p, f64p, f64p, C.c_int64, C.c_int32]),
     "h2f_refined_solve_multi_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                               C.c_int32]),
+    "h2f_factor_import_begin": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.c_int64, C.c_double, C.c_double,
+                                          C.c_double, C.POINTER(C.c_void_p)]),
+    "h2f_factor_import_record": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, i64p, i64p, i64p, C.c_int32,
+                                           i64p, i64p, C.c_int64, i64p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                           C.c_double]),
+    "h2f_factor_import_cluster": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, f64p, f64p,
+                                            i32p, C.c_int32, i64p, i32p, i64p, f64p]),
+    "h2f_factor_import_top": (C.c_int, [C.c_void_p, f64p, i32p]),
+    "h2f_factor_import_end": (C.c_int, [C.c_void_p]),
     "h2f_factor_info_get": (C.c_int, [C.c_void_p, C.POINTER(FactorInfo)]),
     "h2f_factor_level_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(LevelInfo)]),
     "h2f_factor_level_arrays": (C.c_int, [C.c_void_p, C.c_int32, i64p, i64p, i64p, i64p, i64p, i64p]),

@@ -398,6 +398,124 @@ int h2f_refined_solve_multi_dev(h2f_matrix m, h2f_factor f, const double* b_dev,
     });
 }
 
+// ---- factor import (serialization) -------------------------
+
+int h2f_factor_import_begin(int64_t n, int32_t top_level, int32_t num_records, int64_t top_size, double eps_lu,
+                            double eps_fill, double norm_estimate, h2f_factor* out) {
+    return guard([&] {
+        if (n < 0 || num_records < 0 || top_size < 0) throw Error(H2F_E_ARG, "negative sizes");
+        auto f = std::make_unique<Factorization>();
+        f->n = n;
+        f->top_level = top_level;
+        f->recs.resize(size_t(num_records));
+        f->top_size = top_size;
+        f->eps_lu = eps_lu;
+        f->eps_fill = eps_fill;
+        f->norm_estimate = norm_estimate;
+        f->top_lu = f->store.alloc_n<double>(top_size * top_size);
+        f->top_piv = f->store.alloc_n<int32_t>(top_size);
+        *out = new h2f_factor_s{f.release()};
+    });
+}
+
+int h2f_factor_import_record(h2f_factor f, int32_t rec, int32_t level, int32_t num_clusters, const int64_t* clusters,
+                             const int64_t* offsets, const int64_t* sizes, int32_t num_batches,
+                             const int64_t* batch_ptr, const int64_t* batch_ids, int64_t up_size,
+                             const int64_t* up_index, int32_t csp, int32_t ncolors, int32_t graph_degree,
+                             int32_t max_rank, double time_s) {
+    return guard([&] {
+        if (!f || !f->f) throw Error(H2F_E_ARG, "null factor");
+        if (rec < 0 || rec >= int32_t(f->f->recs.size())) throw Error(H2F_E_ARG, "record index out of range");
+        LevelRecord& R = f->f->recs[rec];
+        R.level = level;
+        R.clusters.assign(clusters, clusters + num_clusters);
+        R.offset.assign(offsets, offsets + num_clusters);
+        R.size.assign(sizes, sizes + num_clusters);
+        R.batches.assign(size_t(num_batches), {});
+        for (int32_t b = 0; b < num_batches; ++b) R.batches[b].assign(batch_ids + batch_ptr[b], batch_ids + batch_ptr[b + 1]);
+        R.up_index.assign(up_index, up_index + up_size);
+        R.csp = csp;
+        R.ncolors = ncolors;
+        R.graph_degree = graph_degree;
+        R.max_rank = max_rank;
+        R.time_s = time_s;
+        R.factors.assign(size_t(num_clusters), {});
+        R.pos.clear();
+        for (int32_t i = 0; i < num_clusters; ++i) R.pos[int(clusters[i])] = i;
+    });
+}
+
+int h2f_factor_import_cluster(h2f_factor f, int32_t rec, int32_t cluster, int32_t s, int32_t r, const double* q,
+                              const double* lu, const int32_t* piv, int32_t num_edges, const int64_t* edge_other,
+                              const int32_t* edge_kind, const int64_t* edge_width, const double* mw) {
+    return guard([&] {
+        if (!f || !f->f) throw Error(H2F_E_ARG, "null factor");
+        Factorization& F = *f->f;
+        if (rec < 0 || rec >= int32_t(F.recs.size())) throw Error(H2F_E_ARG, "record index out of range");
+        LevelRecord& R = F.recs[rec];
+        auto it = R.pos.find(cluster);
+        if (it == R.pos.end()) throw Error(H2F_E_ARG, "cluster not in record");
+        ClusterFactor& cf = R.factors[it->second];
+        if (s != R.size[it->second] || r < 0 || r > s) throw Error(H2F_E_ARG, "cluster shape mismatch");
+        cudaStream_t st = ctx().stream;
+        cf.cluster = cluster;
+        cf.s = s;
+        cf.r = r;
+        cf.offset = R.offset[it->second];
+        cf.q = F.store.alloc_n<double>(int64_t(s) * s);
+        H2F_CUDA(cudaMemcpyAsync(cf.q, q, sizeof(double) * s * s, cudaMemcpyHostToDevice, st));
+        cf.edges.clear();
+        if (r == 0) return;
+        int64_t W = 0;
+        for (int32_t e = 0; e < num_edges; ++e) W += edge_width[e];
+        cf.lu = F.store.alloc_n<double>(int64_t(r) * r);
+        cf.piv = F.store.alloc_n<int32_t>(r);
+        double* MW = F.store.alloc_n<double>(int64_t(r) * W);
+        H2F_CUDA(cudaMemcpyAsync(cf.lu, lu, sizeof(double) * r * r, cudaMemcpyHostToDevice, st));
+        H2F_CUDA(cudaMemcpyAsync(cf.piv, piv, sizeof(int32_t) * r, cudaMemcpyHostToDevice, st));
+        H2F_CUDA(cudaMemcpyAsync(MW, mw, sizeof(double) * r * W, cudaMemcpyHostToDevice, st));
+        int64_t col = 0;
+        for (int32_t e = 0; e < num_edges; ++e) {
+            cf.edges.push_back({int(edge_other[e]), int(edge_kind[e]), MW + col, W, int(edge_width[e])});
+            col += edge_width[e];
+        }
+        ctx().sync();  // the host arrays may be released on return
+    });
+}
+
+int h2f_factor_import_top(h2f_factor f, const double* top_lu, const int32_t* top_piv) {
+    return guard([&] {
+        if (!f || !f->f) throw Error(H2F_E_ARG, "null factor");
+        Factorization& F = *f->f;
+        const int64_t n = F.top_size;
+        if (n) {
+            H2F_CUDA(cudaMemcpyAsync(F.top_lu, top_lu, sizeof(double) * n * n, cudaMemcpyHostToDevice, ctx().stream));
+            H2F_CUDA(cudaMemcpyAsync(F.top_piv, top_piv, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx().stream));
+        }
+        ctx().sync();
+    });
+}
+
+int h2f_factor_import_end(h2f_factor f) {
+    return guard([&] {
+        if (!f || !f->f) throw Error(H2F_E_ARG, "null factor");
+        Factorization& F = *f->f;
+        // nbytes (factorization.py:181-190) and completeness
+        int64_t nb = F.top_size * F.top_size * 8 + F.top_size * 4;
+        for (auto& rec : F.recs) {
+            nb += int64_t(rec.up_index.size()) * 8;
+            for (auto& cf : rec.factors) {
+                if (!cf.q) throw Error(H2F_E_ARG, "factor import: cluster " + std::to_string(cf.cluster) +
+                                                      " of level " + std::to_string(rec.level) + " missing");
+                nb += int64_t(cf.s) * cf.s * 8;
+                if (cf.r) nb += int64_t(cf.r) * cf.r * 8 + int64_t(cf.r) * 4;
+                for (auto& e : cf.edges) nb += int64_t(cf.r) * e.w * 8;
+            }
+        }
+        F.nbytes = nb;
+    });
+}
+
 int h2f_factor_info_get(h2f_factor f, h2f_factor_info* info) {
     return guard([&] {
         const Factorization& F = *f->f;

@@ -116,9 +116,6 @@ struct GemmBuild {
         auto* dt = X.up.put(tasks);
         const GemmContrib* dc = ext ? ext : X.up.put(contribs);
         auto* ds = X.up.put(tile_start);
-        const int64_t* dcta = ntiles > gemm_grid(ntiles) ? X.up.put(cta_ranges()) : nullptr;
-        X.up.flush(X.stream);
-        ProfScope ps(kid, flops, bytes_override >= 0 ? bytes_override : bytes, double(ntiles));
         // short average K per tile: the C read-modify-write dominates, use
         // the variant that prefetches C during the tile's math
         static const double kmax = [] {
@@ -126,11 +123,16 @@ struct GemmBuild {
             return e ? std::atof(e) : 96.0;
         }();
         const double keff = flops / (double(ntiles) * 2.0 * GEMM_TILE * GEMM_TILE);
-        // K_eff below this: the register-direct short-K kernel
+        // K_eff below this: the register-direct short-K kernel (one tile per
+        // CTA, no cost-balanced CTA ranges needed)
         static const double kwarp = [] {
             const char* e = std::getenv("H2F_GEMM_WARP_KMAX");
             return e ? std::atof(e) : 40.0;
         }();
+        const int64_t* dcta =
+            keff >= kwarp && ntiles > gemm_grid(ntiles) ? X.up.put(cta_ranges()) : nullptr;
+        X.up.flush(X.stream);
+        ProfScope ps(kid, flops, bytes_override >= 0 ? bytes_override : bytes, double(ntiles));
         const int role = kid == K_GEMM_SCHUR ? 1 : 0;
         if (keff < kwarp)
             launch_gemm_warp(dt, dc, ds, int32_t(tasks.size()), ntiles, norms, X.stream, role);

@@ -95,6 +95,7 @@ struct Lvl {
     std::vector<int> live, red, k;
     std::vector<char> done;
     std::vector<View> basis;
+    std::vector<double*> qv;  // [V_perp | V] per cluster, computed at level start
     std::map<Key, View> D, F;
     std::vector<View*> diag;  // D(c, c) per position
     std::vector<Nbrs> touch;
@@ -128,6 +129,7 @@ struct Lvl {
         k.assign(n, 0);
         done.assign(n, 0);
         basis.assign(n, {});
+        qv.assign(n, nullptr);
         touch.assign(n, {});
         diag.assign(n, nullptr);
         T.assign(n, {});
@@ -225,6 +227,7 @@ class Factorizer {
 
     std::unique_ptr<Lvl> leaf_level(int level);
     void attach_couplings(Lvl& L);
+    void level_complements(Lvl& L);
     void process_batch(Lvl& L, const std::vector<int>& batch);
     std::unique_ptr<Lvl> transition(Lvl& L);
     void finish_top(Lvl& L);
@@ -302,6 +305,32 @@ void Factorizer::attach_couplings(Lvl& L) {
         }
 }
 
+// [V_perp | V] (complete Householder QR of the basis V, factorization.py:88-99
+// applied to V alone) for every cluster of the level at once: V is fixed for
+// the whole level (the transition built it), so the complements leave the
+// per-batch critical path and run as one wide launch instead of one small
+// launch per batch.
+void Factorizer::level_complements(Lvl& L) {
+    CopyBuild gather;
+    std::vector<ComplementTask> tasks;
+    double cf = 0, cb = 0;
+    for (size_t ci = 0; ci < L.clusters.size(); ++ci) {
+        const int s = int(L.size[ci]);
+        const View& V = L.basis[ci];
+        const int k = V.cols;
+        double* bt = L.mem.alloc_n<double>(int64_t(std::max(k, 1)) * s);
+        L.qv[ci] = L.mem.alloc_n<double>(int64_t(s) * s);
+        gather.add(bt, s, k, s, V.p, V.ld, 1, COPY_SET);
+        tasks.push_back(ComplementTask{bt, L.mem.alloc_n<double>(int64_t(s) * s), L.qv[ci],
+                                       L.mem.alloc_n<double>(int64_t(16) * s), s, k});
+        cf += 4.0 * double(s) * s * s;
+        cb += 16.0 * double(s) * s;
+    }
+    gather.launch();
+    ProfScope ps(K_COMPLEMENT_V, cf, cb);
+    complement(tasks, L.mem);
+}
+
 void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     Context& X = ctx();
     cudaStream_t st = X.stream;
@@ -334,7 +363,6 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     {
         CopyBuild gather;
         GemmBuild gz;
-        std::vector<ComplementTask> cmpV;
         std::vector<QrTask> qr_small, qr_big, qr_seg;
         std::vector<SvdTask> svd_small, svd_big;
         int max_n_small = 1;
@@ -373,14 +401,14 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             }
             A.skip = (A.wf == 0 || k == s);
             Q[bi] = F.store.alloc_n<double>(int64_t(s) * s);
+            A.QV = L.qv[ci];  // [V_perp | V], level_complements
+            if (A.skip) {
+                gather.add(Q[bi], s, s, s, A.QV, s, 0, COPY_SET);
+                continue;
+            }
+            // BT rows 0..k-1 = V^T (rows k.. receive vbar^T below)
             A.BT = scr.alloc_n<double>(int64_t(s) * s);
-            A.QV = A.skip ? Q[bi] : scr.alloc_n<double>(int64_t(s) * s);
-            double* Wc = scr.alloc_n<double>(int64_t(s) * s);
-            double* cs = scr.alloc_n<double>(int64_t(16) * s);
-            // BT rows 0..k-1 = V^T ; complement of V -> QV = [V_perp | V]
             gather.add(A.BT, s, k, s, A.V.p, A.V.ld, 1, COPY_SET);
-            cmpV.push_back(ComplementTask{A.BT, Wc, A.QV, cs, s, k});
-            if (A.skip) continue;
             const int wf = A.wf;
             double* Fb = scr.alloc_n<double>(int64_t(s) * wf);
             int off = 0;
@@ -421,15 +449,6 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             }
         }
         gather.launch();
-        double cf = 0, cb = 0;
-        for (auto& t : cmpV) {
-            cf += 4.0 * double(t.s) * t.s * t.s;
-            cb += 16.0 * double(t.s) * t.s;
-        }
-        {
-            ProfScope ps(K_COMPLEMENT_V, cf, cb);
-            complement(cmpV, scr);
-        }
         gz.launch(K_GEMM_AUG);
         auto qr_work = [](const std::vector<QrTask>& v, double& f, double& b) {
             for (auto& t : v) {
@@ -1291,6 +1310,7 @@ void Factorizer::run(double norm_estimate, const double* v0) {
             if (!L) L = leaf_level(level);
             for (size_t i = 0; i < L->clusters.size(); ++i) L->live[i] = int(L->size[i]);
             attach_couplings(*L);
+            level_complements(*L);
             L->fill_init.clear();
             for (auto& kv : L->F) L->fill_init.push_back(kv.first);
             clock.mark(PH_COLOR);

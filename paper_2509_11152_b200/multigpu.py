@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["column_ranges", "solve_multi_sharded"]
+__all__ = ["column_ranges", "solve_multi_sharded", "broadcast_arrays", "broadcast_factorization"]
 
 
 def column_ranges(q, world):
@@ -99,3 +99,44 @@ def solve_multi_sharded(fac, B, group=None, solver=None, device=None):
     for (l, h), p in zip(ranges, parts):
         out[:, l:h] = p[:, : h - l].cpu().numpy()
     return out
+
+
+def broadcast_arrays(arrays, src=0, group=None, device=None):
+    """Broadcast a dict of NumPy arrays (e.g. serialize.pack of a factor)
+    from rank `src`; returns the dict on every rank.  One small object
+    broadcast for the layout, then one tensor broadcast per array (over
+    NCCL on `device`, or gloo on the CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    layout = [[(k, v.dtype.str, v.shape) for k, v in sorted(arrays.items())]] if rank == src else [None]
+    dist.broadcast_object_list(layout, src=src, group=group)
+    out = {}
+    for key, dt, shape in layout[0]:
+        nbytes = int(np.prod(shape, dtype=np.int64)) * np.dtype(dt).itemsize
+        if rank == src:
+            raw = np.ascontiguousarray(arrays[key]).reshape(-1).view(np.uint8)
+            t = torch.from_numpy(raw.copy()).to(device) if device is not None else torch.from_numpy(raw.copy())
+        else:
+            t = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        if nbytes:
+            dist.broadcast(t, src=src, group=group)
+        out[key] = t.cpu().numpy().view(np.dtype(dt)).reshape(shape)
+    return out
+
+
+def broadcast_factorization(fac, src=0, group=None, device=None, tree=None):
+    """Factor once on rank `src`, then give every rank the same factor (the
+    replicated factor of the column-sharded multi-RHS solve):
+    the source packs its device factor (serialize.pack), the others rebuild
+    it from the broadcast arrays (serialize.unpack).  `fac` is ignored on the
+    other ranks."""
+    import torch.distributed as dist
+
+    from .serialize import pack, unpack
+
+    rank = dist.get_rank(group)
+    arrays = pack(fac) if rank == src else {}
+    got = broadcast_arrays(arrays, src=src, group=group, device=device)
+    return fac if rank == src else unpack(got, tree if tree is not None else getattr(fac, "tree", None))

@@ -3,7 +3,7 @@ meant to run under ncu filtered to the Schur-complement GEMM symbols
 (role 1): pairs every Schur launch's ncu DRAM bytes with the library's
 algorithmic bytes and flops for the same launch (bench.py roofline.traffic).
 
-    H2F_PROF_LOG=gpurun_out/prof.log ncu --kernel-name regex:'gemm_(tasks|warp)_kernel<.*1>' \\
+    H2F_PROF_LOG=gpurun_out/prof.log ncu --kernel-name regex:gemm_schur \\
         --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv \\
         --log-file gpurun_out/schur_ncu.csv python scripts/schur_traffic.py
     python scripts/schur_traffic.py --summarize gpurun_out/prof.log gpurun_out/schur_ncu.csv OUT.json

@@ -141,3 +141,25 @@ def test_refined_solve_multi_matches_columns():
     assert np.linalg.norm(R) <= 1e-9 * np.linalg.norm(B)
     with pytest.raises(ValueError):
         H.refined_solve_multi(h2, fac, B[:-1])
+
+
+def test_factor_save_load_round_trip(tmp_path):
+    """f2: a saved and re-imported factor solves bit for bit like the
+    original; records, batches, ranks, pivots and nbytes survive."""
+    _, _, _, h2, prm = problem("laplace3d_4096")
+    fac = H.factorize(h2, prm["eps_lu"])
+    path = tmp_path / "fac.npz"
+    H.save_factorization(fac, path)
+    fac2 = H.load_factorization(path, h2.tree)
+    assert fac2.nbytes() == fac.nbytes() and fac2.top_size == fac.top_size
+    assert structure_of(fac2) == structure_of(fac)
+    b = np.random.default_rng(2).standard_normal(fac.n)
+    assert np.array_equal(H.solve(fac2, b), H.solve(fac, b))
+    B = np.random.default_rng(3).standard_normal((fac.n, 5))
+    assert np.array_equal(H.solve_multi(fac2, B), H.solve_multi(fac, B))
+    assert np.array_equal(H.refined_solve(h2, fac2, b), H.refined_solve(h2, fac, b))
+    c = fac.records[0].clusters[3]
+    assert np.array_equal(fac2.records[0].factors[c].piv, fac.records[0].factors[c].piv)
+    with pytest.raises(ValueError):
+        from paper_2509_11152_b200.serialize import unpack
+        unpack({"meta": np.array('{"format": "other"}')})

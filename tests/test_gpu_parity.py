@@ -84,9 +84,18 @@ def test_fill_keys_after_every_batch_match_reference(case):
 
 
 @pytest.mark.parametrize("case", ROBUST)
-def test_pivots_match_reference(case):
+def test_pivots_match_reference(case, monkeypatch):
+    """LU pivots depend on the redundant columns of Q~, which are not unique
+    (any orthonormal completion of b_aug).  With the
+    reference's construction -- a complete Householder QR of b_aug,
+    H2F_COMPLEMENT_QR=1 -- every pivot sequence equals the reference's; the
+    default completion (V_perp U_rest from the Jacobi) is checked by
+    test_default_completion_pivots_and_solution."""
     g = load(case)
-    _, _, fac = gpu_factor(case)
+    _, _, _, h2, prm = problem(case)
+    monkeypatch.setenv("H2F_COMPLEMENT_QR", "1")
+    fac = H.factorize(h2, prm["eps_lu"])
+    monkeypatch.delenv("H2F_COMPLEMENT_QR")
     mism, total = 0, 0
     for lv, rec in zip(g["levels"], fac.records):
         for c, f in rec.factors.items():
@@ -96,6 +105,25 @@ def test_pivots_match_reference(case):
             mism += got != want
     assert np.array_equal(fac.top_piv.astype(np.int64), g["top_piv"])
     assert mism == 0, f"{mism} of {total} clusters pivot differently"
+
+
+@pytest.mark.parametrize("case", ROBUST)
+def test_default_completion_pivots_and_solution(case):
+    """Default Q~ completion: the integer structure is the reference's (see
+    test_structure_bit_exact); pivot sequences may differ where the
+    redundant rotation moves a partial-pivoting choice (measured: 5 of 504
+    clusters at configs[0]), the solution stays the reference's to 1e-8."""
+    g = load(case)
+    h2, prm, fac = gpu_factor(case)
+    mism, total = 0, 0
+    for lv, rec in zip(g["levels"], fac.records):
+        for c, f in rec.factors.items():
+            total += 1
+            mism += (None if f.piv is None else f.piv.tolist()) != lv["piv"][str(c)]
+    assert mism <= max(1, total // 50), f"{mism} of {total}"
+    b = rhs(h2, H.matvec)
+    x = H.refined_solve(h2, fac, b, steps=1)
+    assert np.linalg.norm(x - g["x"]) <= 1e-8 * np.linalg.norm(g["x"])
 
 
 @pytest.mark.parametrize("case", ROBUST + SENSITIVE)
@@ -256,9 +284,11 @@ def test_blocked_lu_and_dmma_trsm_paths(case, monkeypatch):
     _, _, _, h2, prm = problem(case)
     monkeypatch.setenv("H2F_LU_BLOCKED_MIN", "0")
     monkeypatch.setenv("H2F_TRSM_DMMA_MIN", "1")
+    monkeypatch.setenv("H2F_COMPLEMENT_QR", "1")  # the reference's Q~ construction: pivots comparable
     fac_b = H.factorize(h2, prm["eps_lu"])
     monkeypatch.delenv("H2F_LU_BLOCKED_MIN")
     monkeypatch.delenv("H2F_TRSM_DMMA_MIN")
+    monkeypatch.delenv("H2F_COMPLEMENT_QR")
     _, _, fac = gpu_factor(case)
     assert structure_of(fac_b) == golden_structure(g)
     for lv, rec in zip(g["levels"], fac_b.records):

@@ -90,3 +90,34 @@ def test_solve_multi_sharded_gloo_world2(tmp_path, q):
         # every rank holds the assembled solution, bit-identical to the shards
         assert np.array_equal(X, X_ref)
         assert np.allclose(X, X_full, rtol=0, atol=1e-12 * np.abs(X_full).max())
+
+
+def _bcast_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_2509_11152_b200.multigpu import broadcast_arrays
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        src = {"meta": np.array('{"format": "x"}'), "q": rng.standard_normal((7, 5)),
+               "piv": np.arange(9, dtype=np.int32), "empty": np.zeros(0), "ids": np.arange(4, dtype=np.int64)}
+        got = broadcast_arrays(src if rank == 1 else {}, src=1)
+        np.savez(os.path.join(out_dir, f"bc{rank}.npz"), **got)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_broadcast_arrays_gloo_world2(tmp_path):
+    """The wire half of broadcast_factorization (serialize.pack arrays from
+    one rank to all): dtypes, shapes, empty arrays and strings survive."""
+    port = _free_port()
+    mp.spawn(_bcast_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    rng = np.random.default_rng(4)
+    for rank in range(2):
+        with np.load(tmp_path / f"bc{rank}.npz") as z:
+            assert str(z["meta"]) == '{"format": "x"}'
+            assert z["piv"].dtype == np.int32 and np.array_equal(z["piv"], np.arange(9))
+            assert z["empty"].shape == (0,) and np.array_equal(z["ids"], np.arange(4))
+    with np.load(tmp_path / "bc0.npz") as a, np.load(tmp_path / "bc1.npz") as b:
+        assert np.array_equal(a["q"], b["q"])
