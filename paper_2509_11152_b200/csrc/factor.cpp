@@ -1243,6 +1243,16 @@ void Factorizer::top_factor(double* A, int64_t n) {
     Context& X = ctx();
     cudaStream_t st = X.stream;
     if (n == 0) return;
+    if (const char* path = std::getenv("H2F_DUMP_TOP")) {
+        // development aid: the assembled dense top matrix before its LU
+        X.sync();
+        std::vector<double> h(size_t(n) * n);
+        H2F_CUDA(cudaMemcpy(h.data(), A, h.size() * 8, cudaMemcpyDeviceToHost));
+        if (FILE* f = std::fopen(path, "wb")) {
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
+    }
     double* red = scratch[0].alloc_n<double>(2);
     blocked_lu(A, n, F.top_piv, scratch[0], red, K_TOP_PANEL, K_TOP_MISC, K_GEMM_TOP);
     double* h = static_cast<double*>(X.pinned_buf(16));

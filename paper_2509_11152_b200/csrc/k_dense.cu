@@ -1242,6 +1242,13 @@ int jacobi_coop_capacity(int max_n, int max_m) {
 }
 
 
+namespace {
+const void* jacobi_block_fn(int jb) {
+    return jb == 16 ? (const void*)jacobi_block_kernel<16>
+                    : jb == 8 ? (const void*)jacobi_block_kernel<8> : (const void*)jacobi_block_kernel<4>;
+}
+}  // namespace
+
 int jacobi_block_rows(int n) {
     // H2F_JACOBI_JB: force the rows per block (4, 8 or 16: one warp per row
     // pair, measured slower on config-2 shapes: the FP64 pipe of the fewer
@@ -1260,12 +1267,7 @@ int jacobi_block_rows(int n) {
     return fits(8) ? 8 : 4;
 }
 
-namespace {
-const void* jacobi_block_fn(int jb) {
-    return jb == 16 ? (const void*)jacobi_block_kernel<16>
-                    : jb == 8 ? (const void*)jacobi_block_kernel<8> : (const void*)jacobi_block_kernel<4>;
-}
-}  // namespace
+
 
 size_t jacobi_block_smem(int max_n, int max_m) {
     const int jb = jacobi_block_rows(max_n);
@@ -1275,9 +1277,18 @@ size_t jacobi_block_smem(int max_n, int max_m) {
 int jacobi_block_capacity(int max_n, int max_m) {
     const size_t smem = jacobi_block_smem(max_n, max_m);
     const void* fn = jacobi_block_fn(jacobi_block_rows(max_n));
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // a shared-memory request above the device limit means "cannot be
+    // resident": capacity 0, and the caller takes the pairwise kernel --
+    // checked here so no sticky launch error is left behind
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
     int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, JBT, smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, JBT, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return per_sm * sms;

@@ -289,7 +289,10 @@ bool launch_coop_panel_lu(double* A, int64_t lda, int32_t n, int32_t k0, int32_t
     cudaMemsetAsync(S.bar, 0, 2 * sizeof(unsigned), st);
     void* args[] = {(void*)&A, (void*)&lda, (void*)&n, (void*)&k0, (void*)&nb, (void*)&piv, (void*)&S};
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)coop_panel_lu_kernel, dim3(G), dim3(PT), args, smem, st);
-    if (e != cudaSuccess) return false;
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // handled: the caller falls back to the one-CTA panel; keep no sticky error
+        return false;
+    }
     count_launch();
     return true;
 }

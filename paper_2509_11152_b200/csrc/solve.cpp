@@ -134,6 +134,7 @@ struct SolvePlan {
     int32_t* top_sync = nullptr;
     double* scratch = nullptr;
     double* work = nullptr;
+    int64_t last_use = 0;
     Region mem{size_t(16) << 20};
 };
 
@@ -141,10 +142,27 @@ Factorization::~Factorization() = default;
 
 namespace {
 
+// plans are cached per nrhs; at most kMaxPlans stay alive (least recently
+// used evicted -- each holds O(n nrhs) of vectors in its own region), so
+// solves with many different column counts do not grow the arena
+constexpr size_t kMaxPlans = 3;
+
 SolvePlan& get_plan(Factorization& f, int nrhs) {
+    static int64_t clock = 0;
     auto it = f.plans.find(nrhs);
-    if (it != f.plans.end()) return *it->second;
+    if (it != f.plans.end()) {
+        it->second->last_use = ++clock;
+        return *it->second;
+    }
+    while (f.plans.size() >= kMaxPlans) {
+        auto victim = f.plans.begin();
+        for (auto jt = f.plans.begin(); jt != f.plans.end(); ++jt)
+            if (jt->second->last_use < victim->second->last_use) victim = jt;
+        ctx().sync();  // no launch of the victim's task lists is in flight
+        f.plans.erase(victim);
+    }
     auto plan = std::make_shared<SolvePlan>();
+    plan->last_use = ++clock;
     SolvePlan& P = *plan;
     P.nrhs = nrhs;
     int64_t scratch_rows = 0, work_max = 0;

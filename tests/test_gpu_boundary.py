@@ -163,3 +163,20 @@ def test_factor_save_load_round_trip(tmp_path):
     with pytest.raises(ValueError):
         from paper_2509_11152_b200.serialize import unpack
         unpack({"meta": np.array('{"format": "other"}')})
+
+
+def test_solve_plans_bounded_for_many_column_counts():
+    """a solve plan per nrhs used to stay cached forever; the
+    cache is now LRU-bounded, so ragged column counts do not grow the arena."""
+    _, _, _, h2, prm = problem("cov2d_1024")
+    fac = H.factorize(h2, prm["eps_lu"])
+    rng = np.random.default_rng(9)
+    in_use = {}
+    for q in range(5, 41):
+        B = rng.standard_normal((fac.n, q))
+        X = H.solve_multi(fac, B)
+        assert np.allclose(H.matvec(h2, X), B, rtol=0, atol=1e-6 * np.abs(B).max())
+        in_use[q] = L.memory_stats()["in_use"]
+    # 28 more distinct column counts after q = 12: bounded by the 3 live plans
+    per_plan = max(in_use[8] - in_use[7], 1)
+    assert in_use[40] - in_use[12] <= 3 * per_plan + (64 << 20), (in_use[12], in_use[40], per_plan)
