@@ -44,6 +44,10 @@ struct View {
     double* p = nullptr;
     int64_t ld = 0;
     int rows = 0, cols = 0;
+    // Schur-target slot of the current batch (valid when stamp == the batch
+    // number); written only by the one bucket thread that owns the view
+    mutable int64_t stamp = -1;
+    mutable int slot = -1;
 };
 
 struct CouplingW {    // coupling block with logical zero padding (factorization.py:396-403)
@@ -906,27 +910,23 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
 #pragma omp parallel for schedule(static, 1) if (NBK > 1)
     for (int b = 0; b < NBK; ++b) {
         Bucket& B = bk[b];
-        size_t mine = 0;  // updates of this bucket: bounds its distinct targets
-        for (size_t ei = 0; ei < el.size(); ++ei) mine += size_t(boff[ei][b + 1] - boff[ei][b]);
-        size_t cap = 1024;
-        while (cap < 2 * mine + 16) cap <<= 1;
-        std::vector<std::pair<const View*, int>> table(cap, {nullptr, -1});
-        const size_t mask = cap - 1;
+        // slot per target view, first seen = first slot (reference order): the
+        // view carries its slot, stamped with this batch's number
+        const int64_t bstamp = batch_counter;
         for (size_t ei = 0; ei < el.size(); ++ei)
             for (int64_t k = boff[ei][b]; k < boff[ei][b + 1]; ++k) {
                 const Upd& u = upd[ei][k];
                 if (u.M <= 0 || u.N <= 0) continue;
-                size_t h = ((reinterpret_cast<uintptr_t>(u.v) >> 4) * 0x9E3779B97F4A7C15ull >> 20) & mask;
-                while (table[h].first && table[h].first != u.v) h = (h + 1) & mask;
                 int t;
-                if (!table[h].first) {
+                if (u.v->stamp != bstamp) {
                     t = int(B.th.size());
-                    table[h] = {u.v, t};
+                    u.v->stamp = bstamp;
+                    u.v->slot = t;
                     B.th.push_back({u.C, u.ldc, u.M, u.N, 0});
                     B.ksum.push_back(0.0);
                     B.chunks.push_back(0);
                 } else {
-                    t = table[h].second;
+                    t = u.v->slot;
                     const THdr& th = B.th[t];
                     if (th.C != u.C || th.M != u.M || th.N != u.N || th.ldc != u.ldc) B.bad = true;
                 }

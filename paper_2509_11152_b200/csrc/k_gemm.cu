@@ -568,13 +568,15 @@ __device__ __forceinline__ void gemm_warp_body(const GemmTask* __restrict__ task
     }
 }
 
-__global__ void __launch_bounds__(GEMM_THREADS, 3)
+template <int MINB>
+__global__ void __launch_bounds__(GEMM_THREADS, MINB)
 gemm_warp_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restrict__ contribs,
                  const int64_t* __restrict__ tile_start, int ntasks, int64_t ntiles, double* __restrict__ norms) {
     gemm_warp_body(tasks, contribs, tile_start, ntasks, ntiles, norms);
 }
 
-__global__ void __launch_bounds__(GEMM_THREADS, 3)
+template <int MINB>
+__global__ void __launch_bounds__(GEMM_THREADS, MINB)
 gemm_schur_warp_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restrict__ contribs,
                        const int64_t* __restrict__ tile_start, int ntasks, int64_t ntiles,
                        double* __restrict__ norms) {
@@ -681,8 +683,17 @@ int gemm_grid(int64_t ntiles) { return grid_for(ntiles, 2); }
 void launch_gemm_warp(const GemmTask* d_tasks, const GemmContrib* d_contribs, const int64_t* d_tile_start,
                       int32_t ntasks, int64_t ntiles, double* d_norms, cudaStream_t st, int role) {
     if (ntiles <= 0) return;
-    auto fn = role == 1 ? gemm_schur_warp_kernel : gemm_warp_kernel;
-    fn<<<grid_for(ntiles, 12), GEMM_THREADS, 0, st>>>(d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_norms);
+    // resident CTAs per SM (registers: 168 at 3, 128 with spills at 4, 96 at 5)
+    static const int minb = [] {
+        const char* e = std::getenv("H2F_GEMM_WARP_MINB");
+        const int v = e ? std::atoi(e) : 3;
+        return v == 4 || v == 5 ? v : 3;
+    }();
+    auto fn = minb == 5 ? (role == 1 ? gemm_schur_warp_kernel<5> : gemm_warp_kernel<5>)
+            : minb == 4 ? (role == 1 ? gemm_schur_warp_kernel<4> : gemm_warp_kernel<4>)
+                        : (role == 1 ? gemm_schur_warp_kernel<3> : gemm_warp_kernel<3>);
+    fn<<<grid_for(ntiles, 4 * minb), GEMM_THREADS, 0, st>>>(d_tasks, d_contribs, d_tile_start, ntasks, ntiles,
+                                                             d_norms);
     count_launch();
 }
 

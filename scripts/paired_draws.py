@@ -24,7 +24,8 @@ sys.path.insert(0, ".")
 
 fam, n, seeds_arg, out = sys.argv[1], int(sys.argv[2]), sys.argv[3], sys.argv[4]
 seeds = [int(s) for s in seeds_arg.split(",")]
-over_args = [a for a in sys.argv[5:] if not a.startswith(("jobs=", "vmem_gb="))]
+over_args = [a for a in sys.argv[5:] if not a.startswith(("jobs=", "vmem_gb=", "replay="))]
+do_replay = next((a.split("=")[1] for a in sys.argv[5:] if a.startswith("replay=")), "1") != "0"
 jobs = int(next((a.split("=")[1] for a in sys.argv[5:] if a.startswith("jobs=")), "8"))
 # per-oracle address-space cap (a runaway oracle dies alone instead of
 # taking the box down)
@@ -146,6 +147,7 @@ while len(replayed) < len(seeds):
                              "e_b_raw": summ["e_b_raw"], "e_b": summ["e_b"], "top": summ["top"],
                              "levels": summ["levels"], "wall_s": round(secs, 1)}) + "\n")
         fo.flush()
-        b = operator(s)
-        arm(s, "replay", b, np.load(f"{work}/dec_{s}.npz"))
+        if do_replay:
+            b = operator(s)
+            arm(s, "replay", b, np.load(f"{work}/dec_{s}.npz"))
 fo.close()
