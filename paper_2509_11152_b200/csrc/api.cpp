@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "builders.h"
+#include "coloring.h"
 #include "dense.h"
 #include "factor.h"
 
@@ -700,20 +701,10 @@ int h2f_greedy_coloring(int64_t num_clusters, const int64_t* clusters, int64_t n
             a.erase(std::unique(a.begin(), a.end()), a.end());
             deg = std::max(deg, int(a.size()));
         }
-        std::vector<int32_t> col(ids.size(), -1);
-        int ncol = 0;
-        for (size_t i : order) {
-            std::vector<char> used;
-            for (size_t j : adj[i])
-                if (col[j] >= 0) {
-                    if (size_t(col[j]) >= used.size()) used.resize(col[j] + 1, 0);
-                    used[col[j]] = 1;
-                }
-            int c = 0;
-            while (size_t(c) < used.size() && used[c]) ++c;
-            col[i] = c;
-            ncol = std::max(ncol, c + 1);
-        }
+        std::vector<int> col;
+        const int ncol = greedy_coloring(order, ids.size(), [&](size_t i, auto visit) {
+            for (size_t j : adj[i]) visit(j);
+        }, col);
         std::copy(col.begin(), col.end(), colors_out);
         *num_colors = ncol;
         *max_degree = deg;

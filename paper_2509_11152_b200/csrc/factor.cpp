@@ -25,6 +25,7 @@
 #include <set>
 
 #include "builders.h"
+#include "coloring.h"
 #include "dense.h"
 #include "factor.h"
 
@@ -1326,24 +1327,18 @@ void Factorizer::run(double norm_estimate, const double* v0) {
             clock.mark(PH_COLOR);
             // greedy colouring of the D+F graph in ascending id order
             // (factorization.py:330-337, structure.py:137-167)
+            // (the routine h2f_greedy_coloring exports, coloring.h)
             const size_t nc = L->clusters.size();
-            std::vector<int> color(nc, -1);
-            int ncolors = 0, degree = 0;
+            std::vector<size_t> order(nc);
+            int degree = 0;
             for (size_t i = 0; i < nc; ++i) {
-                std::vector<char> used;
+                order[i] = i;  // level clusters are in ascending id order
                 degree = std::max(degree, int(L->touch[i].size()));
-                for (auto& kv : L->touch[i]) {
-                    const int j = L->at(kv.first);
-                    if (color[j] >= 0) {
-                        if (size_t(color[j]) >= used.size()) used.resize(color[j] + 1, 0);
-                        used[color[j]] = 1;
-                    }
-                }
-                int cc = 0;
-                while (size_t(cc) < used.size() && used[cc]) ++cc;
-                color[i] = cc;
-                ncolors = std::max(ncolors, cc + 1);
             }
+            std::vector<int> color;
+            const int ncolors = greedy_coloring(order, nc, [&](size_t i, auto visit) {
+                for (auto& kv : L->touch[i]) visit(size_t(L->at(kv.first)));
+            }, color);
             std::vector<std::vector<int>> groups(ncolors);
             for (size_t i = 0; i < nc; ++i) groups[color[i]].push_back(L->clusters[i]);
             for (auto& grp : groups) {

@@ -6,7 +6,7 @@ This is the INPUT side of the hot path ("next" row
 f1).  It runs on the host in NumPy/SciPy, exactly like the reference, so
 that the operator handed to the B200 factorization is bit-for-bit the one
 the reference would factor on the same machine (checked against the
-reference in tests/test_problem_golden.py).  Nothing here is timed as part
+reference in tests/test_oracle_golden.py::test_builder_matches_reference_input).  Nothing here is timed as part
 of the path.
 
 Reference behaviour restated (file:line under /root/reference/pkg/src/h2factor):

@@ -100,6 +100,7 @@ def _bcast_worker(rank, world, port, out_dir):
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        rng = np.random.default_rng(4)
         src = {"meta": np.array('{"format": "x"}'), "q": rng.standard_normal((7, 5)),
                "piv": np.arange(9, dtype=np.int32), "empty": np.zeros(0), "ids": np.arange(4, dtype=np.int64)}
         got = broadcast_arrays(src if rank == 1 else {}, src=1)
@@ -113,11 +114,10 @@ def test_broadcast_arrays_gloo_world2(tmp_path):
     one rank to all): dtypes, shapes, empty arrays and strings survive."""
     port = _free_port()
     mp.spawn(_bcast_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
-    rng = np.random.default_rng(4)
+    q = np.random.default_rng(4).standard_normal((7, 5))
     for rank in range(2):
         with np.load(tmp_path / f"bc{rank}.npz") as z:
+            assert np.array_equal(z["q"], q)
             assert str(z["meta"]) == '{"format": "x"}'
             assert z["piv"].dtype == np.int32 and np.array_equal(z["piv"], np.arange(9))
             assert z["empty"].shape == (0,) and np.array_equal(z["ids"], np.arange(4))
-    with np.load(tmp_path / "bc0.npz") as a, np.load(tmp_path / "bc1.npz") as b:
-        assert np.array_equal(a["q"], b["q"])
