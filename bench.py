@@ -44,6 +44,8 @@ CONFIGS = {
                  "(configs[4] at the largest single-GPU factor)"),
 }
 DEFAULT_CONFIG = int(os.environ.get("H2F_BENCH_CONFIG", "2"))
+# the reference's own refined e_b on the same (unperturbed) operator, BASELINE.md §2
+REF_EB = {1: 7.69e-12, 2: 1.2017267347649086e-03, 4: 7.6e4}
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
@@ -375,8 +377,13 @@ def run_b200(args, cfg):
         "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(round(launches)),
         "roofline": roof,
+        "roofline_hbm_phases": hbm_phases(prof, load_peaks()[0]),
         "clocks": clk,
         "backward_error": e_b,
+        "backward_error_reference": REF_EB.get(next(k for k, v in CONFIGS.items() if v is cfg)),
+        "backward_error_note": ("refined e_b = ||A x - b|| / ||b|| of the last timed step (harness.py:215); at "
+                                "N=131072 it is chaotic for both implementations under 1e-14 operator "
+                                "perturbations (DESIGN.md §5, profiles/r02_draws_config2*.jsonl)"),
         "fp64_dmma_tflops_measured": dmma_tf,
         "input_build_s": t_build,
         "phase_seconds_last": None,
@@ -506,6 +513,25 @@ def schur_traffic():
                                             f"traffic / algorithmic bytes = {t['traffic_over_algorithmic']:.2f}")
     except (OSError, KeyError, ValueError):
         return None, "no committed ncu capture"
+
+
+def hbm_phases(prof, peaks):
+    """The HBM-bound phases next to the dominant kernel: the
+    H2 matvec (31 per step: 30 power iterations + the refinement residual)
+    and the substitution sweeps of the refined solve (2 per step), each as
+    algorithmic bytes / device seconds against the measured copy bandwidth."""
+    hbm = float(peaks.get("hbm_gbs", 6550.0))
+    out = {}
+    groups = {"matvec": ["matvec_gemv"],
+              "substitution": ["solve_fwd_clusters", "solve_bwd_clusters", "solve_fwd_scatter", "solve_top"]}
+    for name, ks in groups.items():
+        sec = sum(prof[k]["seconds"] for k in ks if k in prof)
+        byt = sum(prof[k]["bytes"] for k in ks if k in prof)
+        if sec > 0:
+            out[name] = {"bound": "hbm", "achieved": byt / sec / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": byt / sec / 1e9 / hbm, "seconds": sec, "gbytes": byt / 1e9,
+                         "kernels": [k for k in ks if k in prof]}
+    return out
 
 
 def roofline(prof, peaks, peak_kind, dmma_tf):

@@ -14,7 +14,7 @@ import re
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libh2f.so")
+LIB_PATH = os.environ.get("H2F_LIB", os.path.join(HERE, "libh2f.so"))  # H2F_LIB: development builds
 HEADER = os.path.join(os.path.dirname(HERE), "include", "h2f.h")
 
 H2F_OK, H2F_E_ARG, H2F_E_CUDA, H2F_E_NOMEM, H2F_E_SINGULAR, H2F_E_INTERNAL = range(6)

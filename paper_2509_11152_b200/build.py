@@ -14,13 +14,15 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libh2f.so")
+# development builds: H2F_BUILD_DIR / H2F_LIB_OUT elsewhere, H2F_NVCC_DEFS extra -D flags
+OUT = os.environ.get("H2F_BUILD_DIR", os.path.join(HERE, "_build"))
+LIB = os.environ.get("H2F_LIB_OUT", os.path.join(HERE, "libh2f.so"))
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-Wno-deprecated-gpu-targets", "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-I", CSRC,
-          "-I", os.path.join(os.path.dirname(HERE), "include")]
+          "-I", os.path.join(os.path.dirname(HERE), "include")] + \
+    [f"-D{d}" for d in os.environ.get("H2F_NVCC_DEFS", "").split(",") if d]
 SOURCES = ["k_gemm.cu", "k_dense.cu", "k_hh.cu", "dense.cpp", "k_solve.cu", "k_top.cu", "runtime.cpp", "h2mat.cpp", "factor.cpp",
            "solve.cpp", "api.cpp"]
 

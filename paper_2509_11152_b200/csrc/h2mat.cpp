@@ -86,9 +86,23 @@ int sparsity_constant(const H2Mat& m, int level) {
 }
 
 MatvecPlan& matvec_plan(H2Mat& m, int nrhs) {
+    // cached per nrhs, at most 3 alive (least recently used evicted: each
+    // holds O(n nrhs) of vectors in its own region)
+    static int64_t clock = 0;
     auto it = m.plans.find(nrhs);
-    if (it != m.plans.end()) return *it->second;
+    if (it != m.plans.end()) {
+        it->second->last_use = ++clock;
+        return *it->second;
+    }
+    while (m.plans.size() >= 3) {
+        auto victim = m.plans.begin();
+        for (auto jt = m.plans.begin(); jt != m.plans.end(); ++jt)
+            if (jt->second->last_use < victim->second->last_use) victim = jt;
+        ctx().sync();  // no launch of the victim's task lists is in flight
+        m.plans.erase(victim);
+    }
     auto plan = std::make_unique<MatvecPlan>();
+    plan->last_use = ++clock;
     MatvecPlan& P = *plan;
     P.nrhs = nrhs;
     const int64_t n = m.n;
@@ -221,6 +235,7 @@ MatvecPlan& matvec_plan(H2Mat& m, int nrhs) {
         if (b.tasks.empty()) continue;
         GemvLaunch L;
         L.ntasks = int32_t(b.tasks.size());
+        for (auto& t : b.tasks) L.max_rows = std::max(L.max_rows, t.rows);
         for (auto& t : b.tasks)
             for (int64_t ci = t.contrib_begin; ci < t.contrib_end; ++ci) {
                 const double e = double(t.rows) * b.contribs[ci].cols;
@@ -245,7 +260,7 @@ MatvecPlan& matvec_plan(H2Mat& m, int nrhs) {
 static void run_plan(MatvecPlan& P) {
     for (auto& L : P.launches) {
         ProfScope ps(K_MATVEC, L.flops, L.bytes);
-        launch_gemv_tasks(L.tasks, L.ntasks, L.contribs, P.nrhs, ctx().stream);
+        launch_gemv_tasks(L.tasks, L.ntasks, L.contribs, P.nrhs, ctx().stream, L.max_rows);
     }
 }
 

@@ -22,6 +22,7 @@ struct GemvLaunch {
     GemvTask* tasks;
     GemvContrib* contribs;
     int32_t ntasks;
+    int32_t max_rows = 0;  // largest output segment (shared-memory accumulator size)
     double flops = 0, bytes = 0;
 };
 
@@ -35,6 +36,7 @@ struct MatvecPlan {
     double* est = nullptr;       // power-iteration estimates
     std::vector<GemvLaunch> launches;
     Region mem;
+    int64_t last_use = 0;
 };
 
 struct H2Mat {

@@ -12,6 +12,7 @@
 // shared by several clusters of a batch is updated without atomics and in a
 // fixed order (run-to-run bitwise deterministic).
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -410,16 +411,16 @@ __device__ __forceinline__ void gemm_tasks_body(const GemmTask* __restrict__ tas
 
 // two symbols, one body: gemm_schur_kernel carries the Schur-complement
 // launches so the dominant kernel is identifiable in ncu launch lists
-template <int NS, bool PREC, int NT>
-__global__ void __launch_bounds__(NT, 2)
+template <int NS, bool PREC, int NT, int MINB = 2>
+__global__ void __launch_bounds__(NT, MINB)
 gemm_tasks_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restrict__ contribs,
                   const int64_t* __restrict__ tile_start, int ntasks, int64_t ntiles,
                   const int64_t* __restrict__ cta_tiles, double* __restrict__ norms) {
     gemm_tasks_body<NS, PREC, NT>(tasks, contribs, tile_start, ntasks, ntiles, cta_tiles, norms);
 }
 
-template <int NS, bool PREC, int NT>
-__global__ void __launch_bounds__(NT, 2)
+template <int NS, bool PREC, int NT, int MINB = 2>
+__global__ void __launch_bounds__(NT, MINB)
 gemm_schur_kernel(const GemmTask* __restrict__ tasks, const GemmContrib* __restrict__ contribs,
                   const int64_t* __restrict__ tile_start, int ntasks, int64_t ntiles,
                   const int64_t* __restrict__ cta_tiles, double* __restrict__ norms) {
@@ -683,36 +684,30 @@ int gemm_grid(int64_t ntiles) { return grid_for(ntiles, 2); }
 void launch_gemm_warp(const GemmTask* d_tasks, const GemmContrib* d_contribs, const int64_t* d_tile_start,
                       int32_t ntasks, int64_t ntiles, double* d_norms, cudaStream_t st, int role) {
     if (ntiles <= 0) return;
-    // resident CTAs per SM (registers: 168 at 3, 128 with spills at 4, 96 at 5)
-    static const int minb = [] {
-        const char* e = std::getenv("H2F_GEMM_WARP_MINB");
-        const int v = e ? std::atoi(e) : 3;
-        return v == 4 || v == 5 ? v : 3;
-    }();
-    auto fn = minb == 5 ? (role == 1 ? gemm_schur_warp_kernel<5> : gemm_warp_kernel<5>)
-            : minb == 4 ? (role == 1 ? gemm_schur_warp_kernel<4> : gemm_warp_kernel<4>)
-                        : (role == 1 ? gemm_schur_warp_kernel<3> : gemm_warp_kernel<3>);
-    fn<<<grid_for(ntiles, 4 * minb), GEMM_THREADS, 0, st>>>(d_tasks, d_contribs, d_tile_start, ntasks, ntiles,
-                                                             d_norms);
+    // 3 resident CTAs per SM (168 registers; measured: forcing 4 or 5 CTAs
+    // costs spills and is 5-40 % slower on every kbench shape)
+    auto fn = role == 1 ? gemm_schur_warp_kernel<3> : gemm_warp_kernel<3>;
+    fn<<<grid_for(ntiles, 12), GEMM_THREADS, 0, st>>>(d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_norms);
     count_launch();
 }
 
 namespace {
-template <int NS, bool PREC, int NT>
+template <int NS, bool PREC, int NT, int MINB = 2>
 void launch_tasks_variant(const GemmTask* d_tasks, const GemmContrib* d_contribs, const int64_t* d_tile_start,
                           int32_t ntasks, int64_t ntiles, const int64_t* d_cta_tiles, double* d_norms,
                           cudaStream_t st, int role) {
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(gemm_tasks_kernel<NS, PREC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(gemm_tasks_kernel<NS, PREC, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)gemm_smem<NS, PREC>());
-        cudaFuncSetAttribute(gemm_schur_kernel<NS, PREC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(gemm_schur_kernel<NS, PREC, NT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)gemm_smem<NS, PREC>());
         configured = true;
     }
-    auto fn = role == 1 ? gemm_schur_kernel<NS, PREC, NT> : gemm_tasks_kernel<NS, PREC, NT>;
-    fn<<<gemm_grid(ntiles), NT, gemm_smem<NS, PREC>(), st>>>(d_tasks, d_contribs, d_tile_start, ntasks, ntiles,
-                                                            d_cta_tiles, d_norms);
+    auto fn = role == 1 ? gemm_schur_kernel<NS, PREC, NT, MINB> : gemm_tasks_kernel<NS, PREC, NT, MINB>;
+    const int grid = MINB == 2 ? gemm_grid(ntiles) : grid_for(ntiles, MINB);
+    fn<<<grid, NT, gemm_smem<NS, PREC>(), st>>>(d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_cta_tiles,
+                                                d_norms);
 }
 }  // namespace
 
@@ -736,6 +731,8 @@ void launch_gemm_tasks(const GemmTask* d_tasks, const GemmContrib* d_contribs,
         if (prec) launch_tasks_variant<2, true, 256>(H2F_GEMM_ARGS);
         else launch_tasks_variant<3, false, 256>(H2F_GEMM_ARGS);
     } else {
+        // (measured and dropped: a 2-stage pipeline at 3 CTAs per SM, 5-15 %
+        // slower on every kbench shape)
         if (prec) launch_tasks_variant<2, true, 128>(H2F_GEMM_ARGS);
         else launch_tasks_variant<3, false, 128>(H2F_GEMM_ARGS);
     }

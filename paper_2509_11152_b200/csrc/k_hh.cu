@@ -39,8 +39,12 @@ __device__ __forceinline__ void group_barrier(uint32_t* bar, int n) {
     if (threadIdx.x == 0) {
         // monotonic arrival counter (zeroed before the launch): the k-th
         // barrier completes when the counter reaches k * n -- one release
-        // atomic per CTA, acquire polling, no reset round trip
+        // atomic per CTA, acquire polling, no reset round trip (the release /
+        // acquire pair orders the CTA's writes, which bar.sync has ordered
+        // before thread 0's atomic; H2F_BARRIER_FENCES keeps explicit fences)
+#ifdef H2F_BARRIER_FENCES
         __threadfence();
+#endif
         uint32_t old;
         asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
         const uint32_t target = (old / uint32_t(n) + 1u) * uint32_t(n);
@@ -48,7 +52,9 @@ __device__ __forceinline__ void group_barrier(uint32_t* bar, int n) {
         do {
             asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
         } while (int32_t(cur - target) < 0);
+#ifdef H2F_BARRIER_FENCES
         __threadfence();
+#endif
     }
     __syncthreads();
 }

@@ -248,6 +248,49 @@ gemv_tasks_kernel(const GemvTask* __restrict__ tasks, const GemvContrib* __restr
     }
 }
 
+// nrhs = 1 variant with coalesced loads in both orientations: the output
+// segment is accumulated in shared memory, contribution by contribution (in
+// order, one writer per element: deterministic); y += A x reads rows of A
+// (a warp per output row, lanes along the row), y += A^T x reads columns of A
+// as rows of the stored block (a thread per output element, consecutive
+// threads on consecutive addresses) -- the one-warp-per-output form walked a
+// column with lane stride lda, a quarter of every sector wasted.
+constexpr int GV_T = 128;
+
+__global__ void __launch_bounds__(GV_T)
+gemv1_tasks_kernel(const GemvTask* __restrict__ tasks, const GemvContrib* __restrict__ contribs) {
+    const GemvTask T = tasks[blockIdx.x];
+    extern __shared__ double acc[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < T.rows; i += GV_T) acc[i] = 0.0;
+    __syncthreads();
+    for (int64_t ci = T.contrib_begin; ci < T.contrib_end; ++ci) {
+        const GemvContrib P = contribs[ci];
+        if (P.trans) {
+            for (int i = threadIdx.x; i < T.rows; i += GV_T) {
+                const double* a = P.A + i;
+                double part = 0.0;
+#pragma unroll 4
+                for (int j = 0; j < P.cols; ++j) part += __ldg(a + (int64_t)j * P.lda) * __ldg(P.x + j);
+                acc[i] += P.alpha * part;
+            }
+        } else {
+            for (int i = warp; i < T.rows; i += GV_T / 32) {
+                const double* ai = P.A + (int64_t)i * P.lda;
+                double part = 0.0;
+                for (int j = lane; j < P.cols; j += 32) part += __ldg(ai + j) * __ldg(P.x + j);
+                part = warp_sum(part);
+                if (lane == 0) acc[i] += P.alpha * part;
+            }
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < T.rows; i += GV_T) {
+        double* d = T.y + i;
+        if (T.mode == COPY_ADD) *d += acc[i]; else *d = acc[i];
+    }
+}
+
 constexpr int NPART = 256;
 
 __global__ void sumsq_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
@@ -321,9 +364,20 @@ void launch_scatter_rows(const double* src, const int64_t* idx, int64_t n, int32
 }
 
 void launch_gemv_tasks(const GemvTask* d_tasks, int32_t ntasks, const GemvContrib* d_contribs,
-                       int32_t nrhs, cudaStream_t st) {
+                       int32_t nrhs, cudaStream_t st, int32_t max_rows) {
     if (ntasks <= 0) return;
-    gemv_tasks_kernel<<<ntasks, 128, 0, st>>>(d_tasks, d_contribs, nrhs);
+    static const bool v1 = [] {
+        const char* e = std::getenv("H2F_GEMV1");
+        return !(e && std::atoi(e) == 0);
+    }();
+    if (v1 && nrhs == 1 && max_rows > 0 && max_rows <= 6144) {
+        const size_t smem = sizeof(double) * size_t(max_rows);
+        if (smem > 48 * 1024) cudaFuncSetAttribute(gemv1_tasks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   int(smem));
+        gemv1_tasks_kernel<<<ntasks, GV_T, smem, st>>>(d_tasks, d_contribs);
+    } else {
+        gemv_tasks_kernel<<<ntasks, 128, 0, st>>>(d_tasks, d_contribs, nrhs);
+    }
     count_launch();
 }
 

@@ -338,8 +338,10 @@ void launch_top_solve(const double* lu, const int32_t* perm, int32_t n, double* 
                       double* tmp, int32_t* sync, cudaStream_t st);
 
 // matvec / vectors
+// max_rows > 0 (largest output segment of the launch) enables the
+// shared-memory accumulating, coalesced nrhs = 1 kernel
 void launch_gemv_tasks(const GemvTask* d_tasks, int32_t ntasks, const GemvContrib* d_contribs,
-                       int32_t nrhs, cudaStream_t st);
+                       int32_t nrhs, cudaStream_t st, int32_t max_rows = 0);
 void launch_norm2(const double* x, int64_t n, double* partial, double* out, cudaStream_t st);
 void launch_scale_by_inv(double* x, const double* w, int64_t n, const double* s,
                          cudaStream_t st);
@@ -349,5 +351,6 @@ void launch_axpby(double* y, const double* a, double alpha, const double* b, dou
 double bench_dmma(int64_t iters, cudaStream_t st);
 int64_t kernel_launch_count();
 void count_launch();
+void add_launches(int64_t n);  // kernels replayed inside a CUDA graph
 
 }  // namespace h2f

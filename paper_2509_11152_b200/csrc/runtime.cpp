@@ -18,6 +18,7 @@ inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t kernel_launch_count() { return g_launches.load(); }
+void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // ---------------------------------------------------------------- Arena
 void Arena::init(size_t bytes) {

@@ -135,6 +135,12 @@ struct SolvePlan {
     double* scratch = nullptr;
     double* work = nullptr;
     int64_t last_use = 0;
+    cudaGraphExec_t graph = nullptr;  // captured single-vector sweeps (solve_device)
+    int64_t graph_launches = 0;
+    int uses = 0;
+    ~SolvePlan() {
+        if (graph) cudaGraphExecDestroy(graph);
+    }
     Region mem{size_t(16) << 20};
 };
 
@@ -456,19 +462,11 @@ void top_solve_blocked(Factorization& f, SolvePlan& P, cudaStream_t st) {
 
 }  // namespace
 
-void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs) {
-    SolvePlan& P = get_plan(f, nrhs);
-    cudaStream_t st = ctx().stream;
-    const size_t nb = sizeof(double) * f.n * nrhs;
-    if (f.recs.empty()) {
-        // solve.py:46-47
-        H2F_CUDA(cudaMemcpyAsync(P.ytop, b_dev, nb, cudaMemcpyDeviceToDevice, st));
-        launch_top_solve(f.top_lu, P.top_perm, int(f.top_size), P.ytop, nrhs, P.ttop, P.top_sync, st);
-        H2F_CUDA(cudaMemcpyAsync(x_dev, P.ytop, nb, cudaMemcpyDeviceToDevice, st));
-        return;
-    }
+namespace {
+
+// the substitution proper on the plan's own buffers: P.yv[0] (b in, x out)
+void solve_sweeps(Factorization& f, SolvePlan& P, int nrhs, cudaStream_t st) {
     const size_t R = P.levels.size();
-    H2F_CUDA(cudaMemcpyAsync(P.yv[0], b_dev, nb, cudaMemcpyDeviceToDevice, st));
     for (size_t li = 0; li < R; ++li) {
         auto& L = P.levels[li];
         for (auto& B : L.batches) {
@@ -516,6 +514,50 @@ void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs
             launch_solve_tasks(B.tk[2], B.ntk[2], B.cl, B.edges, P.yv[li], P.scratch, P.work, nrhs, st);
             launch_solve_tasks(B.tk[3], B.ntk[3], B.cl, B.edges, P.yv[li], P.scratch, P.work, nrhs, st);
         }
+    }
+}
+
+}  // namespace
+
+void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs) {
+    SolvePlan& P = get_plan(f, nrhs);
+    cudaStream_t st = ctx().stream;
+    const size_t nb = sizeof(double) * f.n * nrhs;
+    if (f.recs.empty()) {
+        // solve.py:46-47
+        H2F_CUDA(cudaMemcpyAsync(P.ytop, b_dev, nb, cudaMemcpyDeviceToDevice, st));
+        launch_top_solve(f.top_lu, P.top_perm, int(f.top_size), P.ytop, nrhs, P.ttop, P.top_sync, st);
+        H2F_CUDA(cudaMemcpyAsync(x_dev, P.ytop, nb, cudaMemcpyDeviceToDevice, st));
+        return;
+    }
+    H2F_CUDA(cudaMemcpyAsync(P.yv[0], b_dev, nb, cudaMemcpyDeviceToDevice, st));
+    // The single-vector sweeps (thousands of small launches, every task list
+    // pre-uploaded into the plan) are captured once into a CUDA graph and
+    // replayed: no per-launch host cost and no launch gaps on the device.
+    // Not with the per-kernel profiler on (its events must stay per launch)
+    // nor for the block path (its top solve uploads task lists per call).
+    static const bool graphs = [] {
+        const char* e = std::getenv("H2F_SOLVE_GRAPH");
+        return !(e && std::atoi(e) == 0);
+    }();
+    // capturing + instantiating costs about one direct run, so a plan is
+    // captured on its third use (a refined solve uses its plan twice)
+    if (graphs && nrhs < SOLVE_GEMM_MIN_RHS && !ctx().prof.on && ++P.uses >= 3) {
+        if (!P.graph) {
+            const int64_t l0 = kernel_launch_count();
+            cudaGraph_t g = nullptr;
+            H2F_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            solve_sweeps(f, P, nrhs, st);
+            H2F_CUDA(cudaStreamEndCapture(st, &g));
+            H2F_CUDA(cudaGraphInstantiate(&P.graph, g, 0));
+            cudaGraphDestroy(g);
+            P.graph_launches = kernel_launch_count() - l0;
+            add_launches(-P.graph_launches);  // counted when the graph runs
+        }
+        H2F_CUDA(cudaGraphLaunch(P.graph, st));
+        add_launches(P.graph_launches);
+    } else {
+        solve_sweeps(f, P, nrhs, st);
     }
     H2F_CUDA(cudaMemcpyAsync(x_dev, P.yv[0], nb, cudaMemcpyDeviceToDevice, st));
 }
