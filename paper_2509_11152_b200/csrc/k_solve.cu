@@ -151,7 +151,7 @@ solve_tasks_kernel(const SolveTask* __restrict__ tasks, const SolveCluster* __re
         for (int k = T.begin + warp; k < T.end; k += STW)
             for (int rh = 0; rh < nrhs; ++rh) {
                 double acc = 0.0;
-                for (int64_t ei = C.edge_begin; ei < C.edge_end; ++ei) {
+                for (int64_t ei = T.e0; ei < T.e1; ++ei) {
                     const SolveEdge E = edges[ei];
                     const int e0 = (int)(E.soff - C.soff);
                     const int lo = max(e0, T.c0), hi = min(e0 + E.w, T.c1);

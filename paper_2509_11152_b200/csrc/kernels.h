@@ -207,6 +207,7 @@ enum SolveTaskKind : int32_t {
 struct SolveTask {
     int32_t cl, kind, begin, end;
     int32_t c0, c1;      // ST_GATHER: eliminator column range [c0, c1)
+    int32_t e0, e1;      // ST_GATHER: the cluster's edges overlapping [c0, c1) (absolute edge indices)
 };
 constexpr int SOLVE_GATHER_COLS = 2048;  // column chunk of one ST_GATHER task
 constexpr int SOLVE_ROT_T_COLS = 64;

@@ -257,10 +257,18 @@ SolvePlan& get_plan(Factorization& f, int nrhs) {
                         tk[1].push_back({ci, ST_PROD, int32_t(j), int32_t(std::min<int64_t>(sc.W, j + SOLVE_PROD_COLS)),
                                          0, 0});
                     tk[2].push_back({ci, ST_USOLVE, 0, cf.r, 0, 0});
-                    for (int64_t c0 = 0; c0 < std::max<int64_t>(sc.W, 1); c0 += SOLVE_GATHER_COLS)
+                    for (int64_t c0 = 0; c0 < std::max<int64_t>(sc.W, 1); c0 += SOLVE_GATHER_COLS) {
+                        const int64_t c1 = std::min<int64_t>(sc.W, c0 + SOLVE_GATHER_COLS);
+                        // the edges are consecutive column slices: only those
+                        // overlapping [c0, c1) are scanned by the task
+                        int64_t ea = sc.edge_begin, eb = sc.edge_begin;
+                        while (ea < sc.edge_end && edges[ea].soff - sc.soff + edges[ea].w <= c0) ++ea;
+                        eb = ea;
+                        while (eb < sc.edge_end && edges[eb].soff - sc.soff < c1) ++eb;
                         for (int i = 0; i < cf.r; i += SOLVE_ROW_SLICE)
                             tk[2].push_back({ci, ST_GATHER, i, std::min(cf.r, i + SOLVE_ROW_SLICE), int32_t(c0),
-                                             int32_t(std::min<int64_t>(sc.W, c0 + SOLVE_GATHER_COLS))});
+                                             int32_t(c1), int32_t(ea), int32_t(eb)});
+                    }
                 } else {
                     // nothing eliminated: the rotated vector passes through
                     tk[1].push_back({ci, ST_LSOLVE, 0, 0, 0, 0});
