@@ -44,6 +44,7 @@ CASES = {
     "laplace3d_16384": ("helmholtz3d", 16384, {"kappa": 0.0}),
     "cov3d_e8_16384": ("cov3d", 16384, {"eps_lu": 1e-8, "eps": 1e-9}),
     "lru_cov3d_4096": ("lru_cov3d", 4096, {}),
+    "osc2d_65536": ("helmholtz3d", 65536, {"dim": 2, "p0": 8, "eta": 0.9}),
 }
 
 

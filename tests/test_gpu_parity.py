@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 ROBUST = ["cov2d_1024", "cov3d_2048", "cov2d_4096", "cov3d_e8_4096", "cov2d_16384", "cov3d_e8_16384"]
 SENSITIVE = ["laplace2d_2048", "helmholtz3d_2048", "laplace3d_4096", "osc2d_4096", "laplace3d_16384",
-             "lru_cov3d_4096"]
+             "lru_cov3d_4096", "osc2d_65536"]
 
 _fac_cache = {}
 
