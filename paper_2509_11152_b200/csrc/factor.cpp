@@ -24,6 +24,8 @@
 #include <numeric>
 #include <set>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "builders.h"
 #include "coloring.h"
 #include "dense.h"
@@ -152,13 +154,21 @@ struct Lvl {
     }
 };
 
-// phase accounting from CUDA events (sums to the device-side wall time)
+// phase accounting from CUDA events (sums to the device-side wall time); the
+// same marks open NVTX ranges named after the reference's phase keys
+// (factorization.py:130-193 phase_seconds), visible to nsys / ncu --nvtx
 class PhaseClock {
   public:
     ~PhaseClock() {
+        if (open_) nvtxRangePop();
         for (auto& e : marks_) cudaEventDestroy(e.first);
     }
     void mark(int phase) {
+        static const char* names[PH_COUNT] = {"norm", "extract", "color", "augment", "project", "partial_lu",
+                                              "transition", "top"};
+        if (open_) nvtxRangePop();
+        open_ = phase >= 0 && phase < PH_COUNT;
+        if (open_) nvtxRangePushA(names[phase]);
         cudaEvent_t e;
         H2F_CUDA(cudaEventCreate(&e));
         H2F_CUDA(cudaEventRecord(e, ctx().stream));
@@ -178,6 +188,7 @@ class PhaseClock {
 
   private:
     std::vector<std::pair<cudaEvent_t, int>> marks_;
+    bool open_ = false;
 };
 
 int env_int(const char* name, int dflt) {
