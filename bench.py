@@ -265,6 +265,24 @@ def run_reference(args, cfg):
 # B200 arm
 # ---------------------------------------------------------------------------
 
+def device_construction(cfg, h2, H):
+    """The same operator built on the device (construct.py, SURVEY.md §8f
+    f1), once, outside the timed steps: wall seconds from the point set
+    (host tree + partition included) and agreement with the host-built h2."""
+    from paper_2509_11152_b200.construct import build_problem_device
+
+    t0 = time.perf_counter()
+    _, _, _, hd, _ = build_problem_device(cfg["problem"], cfg["n"], **cfg["over"])
+    total = time.perf_counter() - t0
+    x = np.random.default_rng(0).standard_normal(cfg["n"])
+    yh = H.matvec(h2, x)
+    out = {"seconds": total, **{k: float(v) for k, v in hd.build_seconds.items()},
+           "ranks_equal_host": all(hd.rank.get(c) == k for c, k in h2.rank.items()),
+           "matvec_rel_diff_host": float(np.linalg.norm(H.matvec(hd, x) - yh) / np.linalg.norm(yh)),
+           "note": "not in the timed step (its input is the host-built operator, as the reference's)"}
+    del hd
+    return out
+
 def run_b200(args, cfg):
     world, rank, local, dist = dist_setup(want_nccl=True)
     os.environ["H2F_DEVICE"] = str(local)
@@ -363,6 +381,7 @@ def run_b200(args, cfg):
         del fac
     t_e2e = max_over_ranks(float(np.mean(e2e_times)), dist, dev)
 
+    dcons = device_construction(cfg, h2, H)
     peaks, peak_kind = load_peaks()
     roof = roofline(prof, peaks, peak_kind, dmma_tf)
     line = {
@@ -386,6 +405,7 @@ def run_b200(args, cfg):
                                 "perturbations (DESIGN.md §5, profiles/r02_draws_config2*.jsonl)"),
         "fp64_dmma_tflops_measured": dmma_tf,
         "input_build_s": t_build,
+        "device_construction": dcons,
         "phase_seconds_last": None,
         "kernels": {k: {"ms": v["seconds"] * 1e3 / prof_steps, "launches": v["launches"] // prof_steps,
                         "gflop": v["flops"] / 1e9 / prof_steps, "gbytes": v["bytes"] / 1e9 / prof_steps}

@@ -159,6 +159,40 @@ int h2f_matvec(h2f_matrix m, const double* x, double* y, int64_t nrhs);
 int h2f_matvec_dev(h2f_matrix m, const double* x_dev, double* y_dev, int64_t nrhs);
 int h2f_norm2(h2f_matrix m, const double* v0, int32_t iters, double* est);
 
+/* ---- device construction --------------------------------
+ * build_h2 + orthogonalize_recompress (h2core.py:128-269) on the device from
+ * the points (tree order), the cluster tree with its boxes and the block
+ * partition; the operator never exists on the host.  Pair lists as in
+ * h2f_matrix_desc.  Tolerance contract, not bit-exact. */
+typedef struct {
+    int64_t n;
+    int32_t dim;             /* 1..3                                             */
+    int32_t depth, top_level;
+    int32_t p0;              /* Chebyshev degree at the leaves: p = p0 + (depth - level) / 2 */
+    int64_t num_nodes;
+    const int64_t* parent;
+    const int64_t* child_left, *child_right, *level, *begin, *end;
+    const double* points;    /* n x dim, tree order                              */
+    const double* box_lo, *box_hi;  /* num_nodes x dim                           */
+    const int64_t* adm_pairs;   const int64_t* adm_ptr;
+    const int64_t* inner_pairs; const int64_t* inner_ptr;
+    const int64_t* dense_pairs; const int64_t* dense_ptr;
+    int32_t family;          /* 0 exp_covariance, 1 laplace2d, 2 helmholtz3d (kernels.py:44-86) */
+    int32_t pad_;
+    double corr_length, kappa, diag_value, alpha_r;
+    double eps;              /* recompression tolerance; <= 0: interpolation bases only */
+} h2f_build_desc;
+
+/* rank[num_nodes] receives the final ranks (-1: no basis); seconds[2] =
+ * construction, compression wall seconds */
+int h2f_matrix_build(const h2f_build_desc* desc, h2f_matrix* out, int64_t* rank, double* seconds);
+/* offsets of a matrix's blocks in its value array, in the description's
+ * order (leaf/transfer per node, coupling/dense per pair), and the values
+ * themselves (nvals doubles) -- the export of a device-built operator */
+int h2f_matrix_layout(h2f_matrix m, int64_t* leaf_basis_off, int64_t* transfer_off, int64_t* coupling_off,
+                      int64_t* dense_off, int64_t* nvals);
+int h2f_matrix_values(h2f_matrix m, double* vals);
+
 /* ---- factorization ------------------------------------------------------- */
 /* norm_estimate < 0: run h2f_norm2 with start vector v0 (n values, already
  * normalised, e.g. Philox(20240901) as in h2core.py:320-322). */

@@ -37,6 +37,22 @@ class MatrixDesc(C.Structure):
     ]
 
 
+class BuildDesc(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("dim", C.c_int32), ("depth", C.c_int32), ("top_level", C.c_int32),
+        ("p0", C.c_int32), ("num_nodes", C.c_int64),
+        ("parent", i64p), ("child_left", i64p), ("child_right", i64p), ("level", i64p),
+        ("begin", i64p), ("end", i64p),
+        ("points", f64p), ("box_lo", f64p), ("box_hi", f64p),
+        ("adm_pairs", i64p), ("adm_ptr", i64p),
+        ("inner_pairs", i64p), ("inner_ptr", i64p),
+        ("dense_pairs", i64p), ("dense_ptr", i64p),
+        ("family", C.c_int32), ("pad_", C.c_int32),
+        ("corr_length", C.c_double), ("kappa", C.c_double), ("diag_value", C.c_double),
+        ("alpha_r", C.c_double), ("eps", C.c_double),
+    ]
+
+
 class KernelProfile(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("seconds", C.c_double),
                 ("flops", C.c_double), ("bytes", C.c_double)]
@@ -83,6 +99,9 @@ _SIGS = {
     "h2f_matrix_create": (C.c_int, [C.POINTER(MatrixDesc), f64p, C.POINTER(C.c_void_p)]),
     "h2f_matrix_destroy": (C.c_int, [C.c_void_p]),
     "h2f_matrix_nbytes": (C.c_int, [C.c_void_p, i64p]),
+    "h2f_matrix_build": (C.c_int, [C.POINTER(BuildDesc), C.POINTER(C.c_void_p), i64p, f64p]),
+    "h2f_matrix_layout": (C.c_int, [C.c_void_p, i64p, i64p, i64p, i64p, i64p]),
+    "h2f_matrix_values": (C.c_int, [C.c_void_p, f64p]),
     "h2f_matvec": (C.c_int, [C.c_void_p, f64p, f64p, C.c_int64]),
     "h2f_matvec_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     "h2f_norm2": (C.c_int, [C.c_void_p, f64p, C.c_int32, f64p]),

@@ -24,7 +24,7 @@ COMMON = ["-Wno-deprecated-gpu-targets", "-O3", "-std=c++17", "-lineinfo", "-Xco
           "-I", os.path.join(os.path.dirname(HERE), "include")] + \
     [f"-D{d}" for d in os.environ.get("H2F_NVCC_DEFS", "").split(",") if d]
 SOURCES = ["k_gemm.cu", "k_dense.cu", "k_hh.cu", "dense.cpp", "k_solve.cu", "k_top.cu", "runtime.cpp", "h2mat.cpp", "factor.cpp",
-           "solve.cpp", "api.cpp"]
+           "solve.cpp", "api.cpp", "k_build.cu", "build.cpp"]
 
 
 def _obj(src):

@@ -271,6 +271,34 @@ int h2f_matrix_destroy(h2f_matrix m) {
     });
 }
 
+int h2f_matrix_build(const h2f_build_desc* desc, h2f_matrix* out, int64_t* rank, double* seconds) {
+    return guard([&] {
+        if (!desc || !out) throw Error(H2F_E_ARG, "null argument");
+        H2Mat* m = h2mat_build(desc, rank, seconds);
+        *out = new h2f_matrix_s{m};
+    });
+}
+
+int h2f_matrix_layout(h2f_matrix m, int64_t* leaf_basis_off, int64_t* transfer_off, int64_t* coupling_off,
+                      int64_t* dense_off, int64_t* nvals) {
+    return guard([&] {
+        const H2Mat& M = *m->m;
+        if (leaf_basis_off) std::copy(M.leaf_basis_off.begin(), M.leaf_basis_off.end(), leaf_basis_off);
+        if (transfer_off) std::copy(M.transfer_off.begin(), M.transfer_off.end(), transfer_off);
+        if (coupling_off) std::copy(M.coupling_list.begin(), M.coupling_list.end(), coupling_off);
+        if (dense_off) std::copy(M.dense_list.begin(), M.dense_list.end(), dense_off);
+        if (nvals) *nvals = M.nvals;
+    });
+}
+
+int h2f_matrix_values(h2f_matrix m, double* vals) {
+    return guard([&] {
+        if (!vals) throw Error(H2F_E_ARG, "null argument");
+        d2h(vals, m->m->vals, size_t(m->m->nvals) * 8);
+        ctx().sync();
+    });
+}
+
 int h2f_matrix_nbytes(h2f_matrix m, int64_t* bytes) {
     return guard([&] { *bytes = m->m->nvals * 8; });
 }

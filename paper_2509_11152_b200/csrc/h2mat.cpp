@@ -18,7 +18,9 @@ H2Mat::~H2Mat() {
     if (vals && ctx_ready()) dfree(vals);
 }
 
-H2Mat* h2mat_create(const h2f_matrix_desc* d, const double* host_vals) {
+namespace {
+
+std::unique_ptr<H2Mat> h2mat_structure(const h2f_matrix_desc* d) {
     if (!d || d->n <= 0 || d->num_nodes <= 0) throw Error(H2F_E_ARG, "empty H2 matrix description");
     auto m = std::make_unique<H2Mat>();
     m->n = d->n;
@@ -65,11 +67,32 @@ H2Mat* h2mat_create(const h2f_matrix_desc* d, const double* host_vals) {
         }
     }
     m->nvals = d->nvals;
+    m->coupling_list.assign(d->coupling_off, d->coupling_off + d->adm_ptr[nlev]);
+    m->dense_list.assign(d->dense_off, d->dense_off + d->dense_ptr[nlev]);
+    return m;
+}
+
+}  // namespace
+
+H2Mat* h2mat_create(const h2f_matrix_desc* d, const double* host_vals) {
+    auto m = h2mat_structure(d);
     m->vals = static_cast<double*>(dalloc(sizeof(double) * std::max<int64_t>(d->nvals, 1)));
     if (d->nvals)
         H2F_CUDA(cudaMemcpyAsync(m->vals, host_vals, sizeof(double) * d->nvals, cudaMemcpyHostToDevice,
                                  ctx().stream));
     ctx().sync();
+    return m.release();
+}
+
+H2Mat* h2mat_create_device(const h2f_matrix_desc* d, double* dev_vals) {
+    std::unique_ptr<H2Mat> m;
+    try {
+        m = h2mat_structure(d);
+    } catch (...) {
+        dfree(dev_vals);
+        throw;
+    }
+    m->vals = dev_vals;
     return m.release();
 }
 

@@ -49,6 +49,8 @@ struct H2Mat {
     std::vector<std::unordered_set<Key>> adm_set, dense_set;          // dense = inner | leaves
     std::vector<int64_t> leaf_basis_off, transfer_off;     // per node, -1 absent
     std::unordered_map<Key, int64_t> coupling_off, dense_off;
+    // offsets in the description's pair order (h2f_matrix_layout)
+    std::vector<int64_t> coupling_list, dense_list;
     double* vals = nullptr;                                 // device
     int64_t nvals = 0;
     std::map<int, std::unique_ptr<MatvecPlan>> plans;
@@ -65,6 +67,10 @@ struct H2Mat {
 };
 
 H2Mat* h2mat_create(const h2f_matrix_desc* d, const double* host_vals);
+// takes ownership of dev_vals (an arena allocation of d->nvals doubles)
+H2Mat* h2mat_create_device(const h2f_matrix_desc* d, double* dev_vals);
+// device construction + recompression from points, tree and partition (build.cpp)
+H2Mat* h2mat_build(const h2f_build_desc* d, int64_t* rank_out, double* seconds);
 MatvecPlan& matvec_plan(H2Mat& m, int nrhs);
 // y_dev = A x_dev (both n x nrhs row-major device buffers), stream-ordered
 void matvec_device(H2Mat& m, const double* x_dev, double* y_dev, int nrhs);

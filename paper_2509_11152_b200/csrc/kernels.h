@@ -349,6 +349,60 @@ void launch_scale_by_inv(double* x, const double* w, int64_t n, const double* s,
 void launch_axpby(double* y, const double* a, double alpha, const double* b, double beta,
                   int64_t n, cudaStream_t st);
 
+// ---- device H2 construction (k_build.cu) -----------------------------------------
+enum KernelFamily : int32_t { KF_EXP_COV = 0, KF_LAPLACE2D = 1, KF_HELMHOLTZ3D = 2 };
+
+struct KernelParams {     // kernels.py:44-86 families; diag_base = the entry at r = 0
+    int32_t family, dim;
+    double corr_length, kappa, diag_base, alpha_r;
+};
+
+struct EvalTask {         // out(i, j) = K(|X_i - Y_j|), row-major ldo
+    const double* X;     // rows x dim
+    const double* Y;     // cols x dim
+    double* out;
+    int64_t ldo;
+    int64_t row0, col0;  // global point indices (diag: same index -> diag_base + alpha_r)
+    int32_t rows, cols;
+    int32_t diag, pad_;
+};
+
+struct GridTask {         // p^dim Chebyshev points of the box [lo, hi]
+    double lo[3], hi[3];
+    double* out;          // p^dim x dim
+    int32_t p, pad_;
+};
+
+struct InterpTask {       // Lagrange interpolation of npts points in the box's p-grid
+    const double* pts;    // npts x dim
+    double lo[3], hi[3];
+    double* out;          // npts x p^dim, row-major ldo
+    int64_t ldo;
+    int32_t p, pad_;
+};
+
+struct RowNormOut {       // out[j] = |P[j, 0:len]|
+    const double* P;
+    double* out;
+    int64_t ldp;
+    int32_t len, pad_;
+};
+
+struct DiagTask {         // D = diag(w), n x n
+    const double* w;
+    double* D;
+    int32_t n, pad_;
+};
+
+void launch_eval_tasks(const EvalTask* d_tasks, const int64_t* d_tile_start, int32_t ntasks, int64_t ntiles,
+                       const KernelParams& kp, cudaStream_t st);
+void launch_grid_tasks(const GridTask* d_tasks, int32_t ntasks, int32_t dim, cudaStream_t st);
+void launch_interp_tasks(const InterpTask* d_tasks, const int64_t* d_pt_start, int32_t ntasks, int64_t npts,
+                         int32_t dim, cudaStream_t st);
+void launch_row_norms(const RowNormOut* d_tasks, const int64_t* d_row_start, int32_t ntasks, int64_t nrows,
+                      cudaStream_t st);
+void launch_set_diag(const DiagTask* d_tasks, int32_t ntasks, cudaStream_t st);
+
 double bench_dmma(int64_t iters, cudaStream_t st);
 int64_t kernel_launch_count();
 void count_launch();

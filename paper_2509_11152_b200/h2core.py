@@ -113,7 +113,11 @@ def as_i64(a):
 
 
 def device_matrix(h2):
-    """Upload h2 once and cache the handle on the object."""
+    """Upload h2 once and cache the handle on the object (a DeviceH2 from
+    construct.py already lives on the device)."""
+    built = getattr(h2, "_h2f_built", None)
+    if built is not None:
+        return built
     dev = getattr(h2, "_h2f_device", None)
     if dev is not None and dev.key == _fingerprint(h2):
         return dev

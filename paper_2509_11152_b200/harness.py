@@ -77,6 +77,9 @@ class ExperimentConfig:
     deterministic: bool = True
     oracle_cap: int = 4096
     out: str | None = None
+    # build the operator on the device (construct.py)
+    # instead of the reference's host construction
+    device_build: bool = False
 
     @classmethod
     def from_problem(cls, problem, n, **overrides):
@@ -98,8 +101,19 @@ class ExperimentConfig:
 
 def _operator(config):
     from . import problem as P
+    if config.device_build and not config.lru_rank:
+        from .construct import build_problem_device
+        tree, part, spec, h2, prm = build_problem_device(config.problem, config.n, **config.builder_overrides())
+        bs = h2.build_seconds
+        return tree, spec, h2, prm, {"construction": bs["host_structure"] + bs["construction"],
+                                     "compression": bs["compression"]}
     tree, part, spec, h2, prm = build_problem(config.problem, config.n, **config.builder_overrides())
     return tree, spec, h2, prm, dict(P.LAST_BUILD_TIMINGS)
+
+
+def _h2_bytes(h2):
+    built = getattr(h2, "_h2f_built", None)
+    return built.nbytes if built is not None else int(h2_nbytes(h2))
 
 
 def _profile_columns(prof):
@@ -161,7 +175,7 @@ def run(config, profile=False, keep_solution=False):
         "n": config.n,
         "e_b": e_b,
         "solution_digest": hashlib.sha256(x.tobytes()).hexdigest(),
-        "h2_bytes": int(h2_nbytes(h2)),
+        "h2_bytes": _h2_bytes(h2),
         "factor_bytes": int(fac.nbytes()),
         "kmax_construction": int(max(h2.rank.values())) if h2.rank else 0,
         "kmax_factorization": int(fac.max_rank()),

@@ -74,3 +74,33 @@ def test_grid_counts():
     assert H.generate_uniform_grid(2 ** 20, 3)[1] == (128, 128, 64)
     assert H.generate_uniform_grid(1023, 2)[1] == (33, 31)
     assert H.generate_uniform_grid(2 ** 17, 3)[1] == (64, 64, 32)
+
+
+def test_struct_layouts_match_header(tmp_path):
+    # the ctypes mirrors of the C-ABI structs have the header's size and
+    # field offsets (compiled with the host C compiler)
+    import ctypes as C
+    import os
+    import subprocess
+
+    structs = {"h2f_matrix_desc": L.MatrixDesc, "h2f_build_desc": L.BuildDesc, "h2f_factor_info": L.FactorInfo,
+               "h2f_status": L.Status}
+    lines = ["#include <stddef.h>", "#include <stdio.h>", '#include "h2f.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for f in py._fields_:
+            lines.append(f'printf("{cname} {f[0]} %zu\\n", offsetof({cname}, {f[0]}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        s, f, v = line.split()
+        got[(s, f)] = int(v)
+    for cname, py in structs.items():
+        assert got[(cname, "sizeof")] == C.sizeof(py), cname
+        for f in py._fields_:
+            assert got[(cname, f[0])] == getattr(py, f[0]).offset, (cname, f[0])
