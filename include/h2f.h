@@ -186,6 +186,12 @@ typedef struct {
 /* rank[num_nodes] receives the final ranks (-1: no basis); seconds[2] =
  * construction, compression wall seconds */
 int h2f_matrix_build(const h2f_build_desc* desc, h2f_matrix* out, int64_t* rank, double* seconds);
+/* absorb_low_rank (h2core.py:342-405): a new operator for A + W W^T (W is
+ * n x r row-major, tree order), bases widened to reproduce W, then
+ * recompressed at eps on the device; m is not modified.  seconds[2] =
+ * update, recompression. */
+int h2f_matrix_absorb_low_rank(h2f_matrix m, const double* w, int32_t r, double eps, h2f_matrix* out,
+                               int64_t* rank, double* seconds);
 /* offsets of a matrix's blocks in its value array, in the description's
  * order (leaf/transfer per node, coupling/dense per pair), and the values
  * themselves (nvals doubles) -- the export of a device-built operator */

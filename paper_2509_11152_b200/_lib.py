@@ -100,6 +100,8 @@ _SIGS = {
     "h2f_matrix_destroy": (C.c_int, [C.c_void_p]),
     "h2f_matrix_nbytes": (C.c_int, [C.c_void_p, i64p]),
     "h2f_matrix_build": (C.c_int, [C.POINTER(BuildDesc), C.POINTER(C.c_void_p), i64p, f64p]),
+    "h2f_matrix_absorb_low_rank": (C.c_int, [C.c_void_p, f64p, C.c_int32, C.c_double, C.POINTER(C.c_void_p),
+                                             i64p, f64p]),
     "h2f_matrix_layout": (C.c_int, [C.c_void_p, i64p, i64p, i64p, i64p, i64p]),
     "h2f_matrix_values": (C.c_int, [C.c_void_p, f64p]),
     "h2f_matvec": (C.c_int, [C.c_void_p, f64p, f64p, C.c_int64]),

@@ -27,7 +27,7 @@ from . import _lib as L
 from . import problem as P
 from .h2core import as_i64
 
-__all__ = ["DeviceH2", "build_h2_device", "build_problem_device", "FAMILY_CODES"]
+__all__ = ["DeviceH2", "build_h2_device", "build_problem_device", "absorb_low_rank_device", "FAMILY_CODES"]
 
 FAMILY_CODES = {"exp_covariance": 0, "laplace2d": 1, "helmholtz3d": 2}
 
@@ -134,6 +134,33 @@ def build_h2_device(tree, partition, spec, p0, eps):
     return h2
 
 
+def absorb_low_rank_device(h2, w, eps):
+    """absorb_low_rank(h2, w, eps) (h2core.py:342-405) on the device: a new
+    DeviceH2 for A + W W^T, recompressed at eps.  h2 (host H2Matrix or
+    DeviceH2) is not modified -- unlike the reference, which updates in
+    place, the device operator is immutable.  W: n x r in tree order."""
+    from .h2core import device_matrix
+
+    w = np.ascontiguousarray(np.asarray(w, dtype=np.float64))
+    if w.ndim != 2 or w.shape[0] != h2.n:
+        raise ValueError("update factor must be n x r")
+    lib = L.ensure_init()
+    src = device_matrix(h2)
+    handle = C.c_void_p()
+    rank = np.empty(len(h2.tree.parent), dtype=np.int64)
+    secs = np.zeros(2)
+    L.check(lib.h2f_matrix_absorb_low_rank(src.handle, L.ptr(w), int(w.shape[1]), float(eps), C.byref(handle),
+                                           L.ptr(rank, L.i64p), L.ptr(secs)), "h2f_matrix_absorb_low_rank")
+    nb = C.c_int64()
+    L.check(lib.h2f_matrix_nbytes(handle, C.byref(nb)), "h2f_matrix_nbytes")
+    built = _BuiltMatrix(handle, int(h2.n), int(nb.value))
+    ranks = {int(c): int(k) for c, k in enumerate(rank) if k >= 0}
+    out = DeviceH2(h2.tree, h2.partition, ranks, built,
+                   {"low_rank_update": float(secs[0]), "compression": float(secs[1])})
+    out._st = getattr(h2, "_st", None) or _structure(h2.tree, h2.partition)
+    return out
+
+
 def export_blocks(h2):
     """The device operator's blocks as the reference's dicts (one D2H copy)."""
     lib = L.lib()
@@ -178,8 +205,6 @@ def build_problem_device(name, n, **overrides):
         raise ValueError(f"unknown problem {name!r}; choose from {sorted(P.PROBLEMS)}")
     prm = dict(P.PROBLEMS[name])
     prm.update({k: v for k, v in overrides.items() if v is not None})
-    if prm.get("lru_rank", 0) > 0:
-        raise ValueError("build_problem_device: the low-rank update row is host-built (problem.absorb_low_rank)")
     t0 = time.perf_counter()
     points, counts = P.generate_uniform_grid(n, prm["dim"])
     h = 1.0 / max(counts)
@@ -191,5 +216,13 @@ def build_problem_device(name, n, **overrides):
     t1 = time.perf_counter()
     h2 = build_h2_device(tree, part, spec, prm["p0"], prm["eps"])
     h2.build_seconds["host_structure"] = t1 - t0
+    if prm.get("lru_rank", 0) > 0:
+        # the low-rank row (harness.py:68-70, 185-189): seeded W, absorbed on the device
+        # (rows in tree order, as problem._build passes it to absorb_low_rank)
+        w = P.make_low_rank_factor(n, prm["lru_rank"], prm.get("seed", 7))
+        h2u = absorb_low_rank_device(h2, w, prm["eps"])
+        h2u.build_seconds = dict(h2.build_seconds, **{"low_rank_update": h2u.build_seconds["low_rank_update"],
+                                                       "compression_after_update": h2u.build_seconds["compression"]})
+        h2 = h2u
     h2.build_seconds["device_total"] = time.perf_counter() - t1
     return tree, part, spec, h2, prm

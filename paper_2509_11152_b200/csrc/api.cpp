@@ -279,6 +279,15 @@ int h2f_matrix_build(const h2f_build_desc* desc, h2f_matrix* out, int64_t* rank,
     });
 }
 
+int h2f_matrix_absorb_low_rank(h2f_matrix m, const double* w, int32_t r, double eps, h2f_matrix* out,
+                               int64_t* rank, double* seconds) {
+    return guard([&] {
+        if (!m || !out || (r > 0 && !w)) throw Error(H2F_E_ARG, "null argument");
+        H2Mat* a = h2mat_absorb_low_rank(*m->m, w, r, eps, rank, seconds);
+        *out = new h2f_matrix_s{a};
+    });
+}
+
 int h2f_matrix_layout(h2f_matrix m, int64_t* leaf_basis_off, int64_t* transfer_off, int64_t* coupling_off,
                       int64_t* dense_off, int64_t* nvals) {
     return guard([&] {

@@ -74,6 +74,8 @@ struct Builder {
         cpl.assign(nlev, {});
     }
 
+    std::vector<double*> dense_buf;         // per dense pair (absorb path); empty: evaluate at pack time
+
     bool leaf(int c) const { return d.child_left[c] < 0; }
     int rows(int c) const { return int(d.end[c] - d.begin[c]); }
     int par(int c) const { return int(d.parent[c]); }
@@ -278,10 +280,304 @@ struct Builder {
         return size_t(std::lower_bound(v.begin(), v.end(), c) - v.begin());
     }
 
+    // contiguous device copy, shaped as rows of 256 (+ one remainder row)
+    static void copy_flat(CopyBuild& cb, double* dst, const double* src, int64_t cnt) {
+        const int64_t full = cnt / 256, rem = cnt % 256;
+        for (int64_t r0 = 0; r0 < full; r0 += int64_t(1) << 24) {
+            const int64_t nr = std::min<int64_t>(full - r0, int64_t(1) << 24);
+            cb.add(dst + r0 * 256, 256, int(nr), 256, src + r0 * 256, 256, 0, COPY_SET);
+        }
+        if (rem) cb.add(dst + full * 256, rem, 1, int(rem), src + full * 256, rem, 0, COPY_SET);
+    }
+
+    // state from an existing operator (copies: the input is not modified)
+    void load(const H2Mat& A) {
+        CopyBuild cb;
+        for (int64_t c = 0; c < N; ++c) {
+            rk[c] = int(A.rank[c]);
+            if (A.leaf_basis_off[c] >= 0) {
+                const int64_t cnt = int64_t(rows(int(c))) * rk[c];
+                LB[c] = R.alloc_n<double>(cnt);
+                copy_flat(cb, LB[c], A.vals + A.leaf_basis_off[c], cnt);
+            }
+        }
+        for (int64_t c = 0; c < N; ++c)
+            if (A.transfer_off[c] >= 0) {
+                const int64_t cnt = int64_t(rk[c]) * A.rank[par(int(c))];
+                T[c] = R.alloc_n<double>(cnt);
+                copy_flat(cb, T[c], A.vals + A.transfer_off[c], cnt);
+            }
+        for (int lv = 0; lv < nlev; ++lv)
+            for (int64_t i = d.adm_ptr[lv]; i < d.adm_ptr[lv + 1]; ++i) {
+                const int s = int(d.adm_pairs[2 * i]), t = int(d.adm_pairs[2 * i + 1]);
+                const int64_t cnt = int64_t(rk[s]) * rk[t];
+                double* p = R.alloc_n<double>(cnt);
+                copy_flat(cb, p, A.vals + A.coupling_list[size_t(i)], cnt);
+                touch[s].push_back({int(cpl[lv].size()), false});
+                if (t != s) touch[t].push_back({int(cpl[lv].size()), true});
+                cpl[lv].push_back({s, t, p});
+            }
+        const int64_t nd = d.dense_ptr[nlev];
+        dense_buf.assign(size_t(nd), nullptr);
+        for (int64_t i = 0; i < nd; ++i) {
+            const int s = int(d.dense_pairs[2 * i]), t = int(d.dense_pairs[2 * i + 1]);
+            const int64_t cnt = int64_t(rows(s)) * rows(t);
+            dense_buf[size_t(i)] = R.alloc_n<double>(cnt);
+            copy_flat(cb, dense_buf[size_t(i)], A.vals + A.dense_list[size_t(i)], cnt);
+        }
+        cb.launch();
+    }
+
+    // h2core.py:342-392 (absorb_low_rank before its recompression): A + W W^T.
+    // Dense blocks take W_s W_t^T; bottom-up, each cluster's basis is widened
+    // by the significant range (sigma > 1e-12 |rows|_F) of its rows of W
+    // outside the basis, so coef[c] = basis^T rows reproduces them exactly;
+    // transfers gain zero rows; couplings take coef[s] coef[t]^T.
+    void widen(const double* Wd, int rw) {
+        GemmBuild gd;
+        const int64_t nd = d.dense_ptr[nlev];
+        for (int64_t i = 0; i < nd; ++i) {
+            const int s = int(d.dense_pairs[2 * i]), t = int(d.dense_pairs[2 * i + 1]);
+            gd.add1(dense_buf[size_t(i)], rows(t), rows(s), rows(t), GEMM_ADD,
+                    contrib(Wd + d.begin[s] * rw, rw, 0, Wd + d.begin[t] * rw, rw, 1, rw));
+        }
+        gd.launch(-1);
+        if (top < 0) return;
+        const std::vector<int> rk0 = rk;
+        std::vector<double*> coef(N, nullptr);
+        for (int lv = depth; lv >= top; --lv) {
+            const auto& cl = levels[lv];
+            const size_t nc = cl.size();
+            std::vector<const double*> rowsp(nc);
+            std::vector<int> m(nc), rc(nc);
+            std::vector<double*> inside(nc), fro(nc);
+            CopyBuild c1;
+            GemmBuild g1;
+            for (size_t i = 0; i < nc; ++i) {
+                const int c = cl[i];
+                rc[i] = rk[c];
+                if (leaf(c)) {
+                    m[i] = rows(c);
+                    rowsp[i] = Wd + d.begin[c] * rw;
+                } else {
+                    const int a = int(d.child_left[c]), b = int(d.child_right[c]);
+                    m[i] = rk[a] + rk[b];
+                    double* st_ = R.alloc_n<double>(int64_t(m[i]) * rw);
+                    copy_flat(c1, st_, coef[a], int64_t(rk[a]) * rw);
+                    copy_flat(c1, st_ + int64_t(rk[a]) * rw, coef[b], int64_t(rk[b]) * rw);
+                    rowsp[i] = st_;
+                }
+                // inside = S^T rows (rk x rw)
+                inside[i] = R.alloc_n<double>(int64_t(rc[i]) * rw);
+                if (rc[i] > 0) {
+                    if (leaf(c)) {
+                        g1.add1(inside[i], rw, rc[i], rw, GEMM_STORE, contrib(LB[c], rc[i], 1, rowsp[i], rw, 0, m[i]));
+                    } else {
+                        const int a = int(d.child_left[c]), b = int(d.child_right[c]);
+                        const GemmContrib cs[2] = {contrib(T[a], rc[i], 1, rowsp[i], rw, 0, rk[a]),
+                                                   contrib(T[b], rc[i], 1, rowsp[i] + int64_t(rk[a]) * rw, rw, 0, rk[b])};
+                        g1.add(inside[i], rw, rc[i], rw, GEMM_STORE, cs, 2);
+                    }
+                }
+            }
+            c1.launch();
+            g1.launch(-1);
+            // resid^T = rows^T - inside^T S^T (rw x m): the SVD input M (r = m rows of
+            // left vectors... as M = resid (m x rw))
+            CopyBuild c2;
+            GemmBuild g2;
+            std::vector<Svd> sv(nc);
+            std::vector<RowNormOut> rn;
+            std::vector<int64_t> rstart{0};
+            for (size_t i = 0; i < nc; ++i) {
+                const int c = cl[i];
+                double* M = R.alloc_n<double>(int64_t(m[i]) * rw);
+                copy_flat(c2, M, rowsp[i], int64_t(m[i]) * rw);
+                if (rc[i] > 0) {
+                    if (leaf(c)) {
+                        g2.add1(M, rw, m[i], rw, GEMM_ADD, contrib(LB[c], rc[i], 0, inside[i], rw, 0, rc[i], -1.0));
+                    } else {
+                        const int a = int(d.child_left[c]), b = int(d.child_right[c]);
+                        g2.add1(M, rw, rk[a], rw, GEMM_ADD, contrib(T[a], rc[i], 0, inside[i], rw, 0, rc[i], -1.0));
+                        g2.add1(M + int64_t(rk[a]) * rw, rw, rk[b], rw, GEMM_ADD,
+                                contrib(T[b], rc[i], 0, inside[i], rw, 0, rc[i], -1.0));
+                    }
+                }
+                fro[i] = R.alloc_n<double>(1);
+                rn.push_back(RowNormOut{rowsp[i], fro[i], 0, m[i] * rw, 0});
+                rstart.push_back(rstart.back() + 1);
+                sv[i].M = M;
+                sv[i].r = m[i];
+                sv[i].W = rw;
+            }
+            c2.launch();
+            launch_row_norms(upload(rn), upload(rstart), int32_t(rn.size()), rstart.back(), st);
+            g2.launch(-1);
+            std::vector<double> fro_h(nc);
+            {
+                double* fd = R.alloc_n<double>(int64_t(nc));
+                CopyBuild c3;
+                for (size_t i = 0; i < nc; ++i) c3.add(fd + i, 1, 1, 1, fro[i], 1, 0, COPY_SET);
+                c3.launch();
+                H2F_CUDA(cudaMemcpyAsync(fro_h.data(), fd, sizeof(double) * nc, cudaMemcpyDeviceToHost, st));
+            }
+            svd_left(sv);  // syncs (fro_h is ready after it)
+            std::vector<int> e(nc, 0);
+            for (size_t i = 0; i < nc; ++i) {
+                const double cut = 1e-12 * std::max(fro_h[i], 1e-300);
+                for (double x : sv[i].sh) e[i] += x > cut;
+            }
+            // widened bases [S | extra], coef = [inside; extra^T rows]
+            CopyBuild c4;
+            GemmBuild g4;
+            for (size_t i = 0; i < nc; ++i) {
+                const int c = cl[i], k2 = rc[i] + e[i];
+                const double* U = sv[i].U;  // rows 0..e-1: extra^T (e x m)
+                auto widen_rows = [&](double*& B, int nrow, int row0) {
+                    double* nb = R.alloc_n<double>(int64_t(nrow) * k2);
+                    if (rc[i] > 0) c4.add(nb, k2, nrow, rc[i], B, rc[i], 0, COPY_SET);
+                    if (e[i] > 0) c4.add(nb + rc[i], k2, nrow, e[i], U + row0, m[i], 1, COPY_SET);
+                    B = nb;
+                };
+                if (leaf(c)) {
+                    widen_rows(LB[c], m[i], 0);
+                } else {
+                    const int a = int(d.child_left[c]), b = int(d.child_right[c]);
+                    widen_rows(T[a], rk[a], 0);
+                    widen_rows(T[b], rk[b], rk[a]);
+                }
+                coef[c] = R.alloc_n<double>(int64_t(k2) * rw);
+                if (rc[i] > 0) copy_flat(c4, coef[c], inside[i], int64_t(rc[i]) * rw);
+                if (e[i] > 0)
+                    g4.add1(coef[c] + int64_t(rc[i]) * rw, rw, e[i], rw, GEMM_STORE,
+                            contrib(U, m[i], 0, rowsp[i], rw, 0, m[i]));
+            }
+            c4.launch();
+            g4.launch(-1);
+            // the cluster's own transfer gains e zero rows
+            CopyBuild c5;
+            for (size_t i = 0; i < nc; ++i) {
+                const int c = cl[i];
+                rk[c] = rc[i] + e[i];
+                if (e[i] > 0 && T[c]) {
+                    const int kp = rk[par(c)];
+                    double* nt = R.alloc_n<double>(int64_t(rk[c]) * kp);
+                    if (rc[i] > 0) copy_flat(c5, nt, T[c], int64_t(rc[i]) * kp);
+                    c5.zero(nt + int64_t(rc[i]) * kp, kp, e[i], kp);
+                    T[c] = nt;
+                }
+            }
+            c5.launch();
+        }
+        // couplings: the old block in the leading corner (widening appends
+        // coordinates), plus coef_s coef_t^T
+        CopyBuild z6, c6;
+        GemmBuild g6;
+        for (int lv = 0; lv < nlev; ++lv)
+            for (auto& C : cpl[lv]) {
+                const int ks = rk[C.s], kt = rk[C.t], os = rk0[C.s], ot = rk0[C.t];
+                double* np = R.alloc_n<double>(int64_t(ks) * kt);
+                z6.zero(np, kt, ks, kt);
+                c6.add(np, kt, os, ot, C.p, ot, 0, COPY_SET);
+                g6.add1(np, kt, ks, kt, GEMM_ADD, contrib(coef[C.s], rw, 0, coef[C.t], rw, 1, rw));
+                C.p = np;
+            }
+        z6.launch();
+        c6.launch();
+        g6.launch(-1);
+    }
+
     // h2core.py:236-268: per cluster, SVD of [couplings | transfer * w_parent],
     // keep sigma > eps sigma_0, project basis, transfer and couplings
-    void recompress(double eps) {
+    // left singular vectors and singular values of a batch of r x W
+    // matrices M (row-major, overwritten): R of the QR of M^T (shared-memory
+    // TSQR for r <= 32, blocked Householder above, as factor.cpp's
+    // augmentation), one-sided Jacobi of R keeping every vector (rows of U,
+    // m = min(r, W), sorted by sigma), sigma_j = |R u_j| (GEMM + row norms).
+    // Returns the host sigmas per item (one stream sync).
+    struct Svd {
+        double* M = nullptr;
+        int r = 0, W = 0, m = 0;
+        double *U = nullptr, *Rm = nullptr, *sig = nullptr;
+        std::vector<double> sh;
+    };
+    void svd_left(std::vector<Svd>& v) {
         Context& X = ctx();
+        std::vector<QrTask> qr_small, qr_big, qr_seg;
+        std::vector<SvdTask> svd_small, svd_big;
+        int max_small = 1;
+        int* kept_d = R.alloc_n<int>(1);
+        for (auto& it : v) {
+            const int r = it.r, W = it.W;
+            it.m = (r > 0 && W > 0) ? std::min(r, W) : 0;
+            if (!it.m) continue;
+            const int m = it.m;
+            it.Rm = R.alloc_n<double>(int64_t(m) * r);
+            it.U = R.alloc_n<double>(int64_t(m) * r);
+            it.sig = R.alloc_n<double>(m);
+            if (r > 32) {
+                qr_big.push_back(QrTask{it.M, it.Rm, W, r, W, 0, W, 0});
+            } else {
+                const int seg = std::max(256, 4 * r);
+                const int nseg = int(cdiv(W, seg));
+                if (nseg > 1) {
+                    double* ST = R.alloc_n<double>(int64_t(r) * nseg * r);
+                    for (int sg = 0; sg < nseg; ++sg)
+                        qr_seg.push_back(QrTask{it.M, ST + int64_t(sg) * r, W, r, W, sg * seg,
+                                                std::min(W, (sg + 1) * seg), int64_t(nseg) * r});
+                    qr_small.push_back(QrTask{ST, it.Rm, int64_t(nseg) * r, r, nseg * r, 0, nseg * r, 0});
+                } else {
+                    qr_small.push_back(QrTask{it.M, it.Rm, W, r, W, 0, W, 0});
+                }
+            }
+            SvdTask sv{it.Rm, it.U, m, r, kept_d, 0};
+            if (r <= 64) {
+                svd_small.push_back(sv);
+                max_small = std::max(max_small, r);
+            } else {
+                svd_big.push_back(sv);
+            }
+        }
+        if (!qr_seg.empty()) launch_qr_r_smem(upload(qr_seg), int32_t(qr_seg.size()), max_small, st);
+        if (!qr_small.empty()) launch_qr_r_smem(upload(qr_small), int32_t(qr_small.size()), max_small, st);
+        if (!qr_big.empty()) qr_r_blocked(qr_big, R);
+        if (!svd_small.empty())
+            launch_jacobi_smem(upload(svd_small), int32_t(svd_small.size()), max_small, 0.0, st);
+        if (!svd_big.empty()) jacobi_multi_cta(svd_big, 0.0, R);
+        GemmBuild gp;
+        std::vector<RowNormOut> rn;
+        std::vector<int64_t> rstart{0};
+        int64_t total = 0;
+        for (auto& it : v) {
+            if (!it.m) continue;
+            double* P = R.alloc_n<double>(int64_t(it.m) * it.m);
+            gp.add1(P, it.m, it.m, it.m, GEMM_STORE, contrib(it.U, it.r, 0, it.Rm, it.r, 1, it.r));
+            rn.push_back(RowNormOut{P, it.sig, it.m, it.m, 0});
+            rstart.push_back(rstart.back() + it.m);
+            total += it.m;
+        }
+        gp.launch(-1);
+        if (!rn.empty()) launch_row_norms(upload(rn), upload(rstart), int32_t(rn.size()), rstart.back(), st);
+        std::vector<double> sh(size_t(std::max<int64_t>(total, 1)));
+        double* sdev = R.alloc_n<double>(std::max<int64_t>(total, 1));
+        CopyBuild sc;
+        int64_t off = 0;
+        for (auto& it : v) {
+            if (!it.m) continue;
+            sc.add(sdev + off, it.m, 1, it.m, it.sig, it.m, 0, COPY_SET);
+            off += it.m;
+        }
+        sc.launch();
+        if (total) H2F_CUDA(cudaMemcpyAsync(sh.data(), sdev, sizeof(double) * total, cudaMemcpyDeviceToHost, st));
+        X.sync();
+        off = 0;
+        for (auto& it : v) {
+            it.sh.assign(sh.begin() + off, sh.begin() + off + it.m);
+            off += it.m;
+        }
+    }
+
+    void recompress(double eps) {
         for (int lv = top; lv <= depth; ++lv) {
             const auto& cl = levels[lv];
             const size_t nc = cl.size();
@@ -297,12 +593,7 @@ struct Builder {
             if (!dt.empty()) launch_set_diag(upload(dt), int32_t(dt.size()), st);
             CopyBuild gather;
             GemmBuild gw;
-            std::vector<QrTask> qr_small, qr_big, qr_seg;
-            std::vector<SvdTask> svd_small, svd_big;
-            std::vector<double*> U(nc, nullptr), Rm(nc, nullptr), sig(nc, nullptr);
-            std::vector<int> mm(nc, 0);
-            int max_small = 1;
-            int* kept_d = R.alloc_n<int>(int64_t(nc) + 1);
+            std::vector<Svd> sv(nc);
             for (size_t i = 0; i < nc; ++i) {
                 const int c = cl[i], r = rk[c];
                 int W = 0;
@@ -329,77 +620,24 @@ struct Builder {
                     const int kp = rk[par(c)];
                     gw.add1(M + off, W, r, kp, GEMM_STORE, contrib(T[c], kp, 0, D[par(c)], kp, 0, kp));
                 }
-                const int m = std::min(r, W);
-                mm[i] = m;
-                Rm[i] = R.alloc_n<double>(int64_t(m) * r);
-                U[i] = R.alloc_n<double>(int64_t(m) * r);
-                sig[i] = R.alloc_n<double>(m);
-                // R of the QR of M^T (r columns): shared-memory TSQR for
-                // small r, blocked Householder above (as factor.cpp augment)
-                if (r > 32) {
-                    qr_big.push_back(QrTask{M, Rm[i], W, r, W, 0, W, 0});
-                } else {
-                    const int seg = std::max(256, 4 * r);
-                    const int nseg = int(cdiv(W, seg));
-                    if (nseg > 1) {
-                        double* ST = R.alloc_n<double>(int64_t(r) * nseg * r);
-                        for (int sg = 0; sg < nseg; ++sg)
-                            qr_seg.push_back(QrTask{M, ST + int64_t(sg) * r, W, r, W, sg * seg,
-                                                    std::min(W, (sg + 1) * seg), int64_t(nseg) * r});
-                        qr_small.push_back(QrTask{ST, Rm[i], int64_t(nseg) * r, r, nseg * r, 0, nseg * r, 0});
-                    } else {
-                        qr_small.push_back(QrTask{M, Rm[i], W, r, W, 0, W, 0});
-                    }
-                }
-                SvdTask sv{Rm[i], U[i], m, r, kept_d + nc, 0};
-                if (r <= 64) {
-                    svd_small.push_back(sv);
-                    max_small = std::max(max_small, r);
-                } else {
-                    svd_big.push_back(sv);
-                }
+                sv[i].M = M;
+                sv[i].r = r;
+                sv[i].W = W;
             }
             gather.launch();
             gw.launch(-1);
-            if (!qr_seg.empty()) launch_qr_r_smem(upload(qr_seg), int32_t(qr_seg.size()), max_small, st);
-            if (!qr_small.empty()) launch_qr_r_smem(upload(qr_small), int32_t(qr_small.size()), max_small, st);
-            if (!qr_big.empty()) qr_r_blocked(qr_big, R);
-            if (!svd_small.empty())
-                launch_jacobi_smem(upload(svd_small), int32_t(svd_small.size()), max_small, 0.0, st);
-            if (!svd_big.empty()) jacobi_multi_cta(svd_big, 0.0, R);
-            // sigma_j = |R u_j|: rows of P = U R^T
-            GemmBuild gp;
-            std::vector<RowNormOut> rn;
-            std::vector<int64_t> rstart{0};
-            for (size_t i = 0; i < nc; ++i) {
-                if (!mm[i]) continue;
-                const int m = mm[i], r = rk[cl[i]];
-                double* P = R.alloc_n<double>(int64_t(m) * m);
-                gp.add1(P, m, m, m, GEMM_STORE, contrib(U[i], r, 0, Rm[i], r, 1, r));
-                rn.push_back(RowNormOut{P, sig[i], m, m, 0});
-                rstart.push_back(rstart.back() + m);
-            }
-            gp.launch(-1);
-            if (!rn.empty()) launch_row_norms(upload(rn), upload(rstart), int32_t(rn.size()), rstart.back(), st);
-            // kept counts on the host
-            std::vector<int64_t> soff(nc + 1, 0);
-            for (size_t i = 0; i < nc; ++i) soff[i + 1] = soff[i] + mm[i];
-            std::vector<double> sh(size_t(std::max<int64_t>(soff[nc], 1)));
-            double* sdev = R.alloc_n<double>(std::max<int64_t>(soff[nc], 1));
-            CopyBuild sc;
-            for (size_t i = 0; i < nc; ++i)
-                if (mm[i]) sc.add(sdev + soff[i], mm[i], 1, mm[i], sig[i], mm[i], 0, COPY_SET);
-            sc.launch();
-            if (soff[nc]) H2F_CUDA(cudaMemcpyAsync(sh.data(), sdev, sizeof(double) * soff[nc], cudaMemcpyDeviceToHost, st));
-            X.sync();
+            svd_left(sv);
             std::vector<int> k(nc, 0);
+            std::vector<double*> U(nc, nullptr), sig(nc, nullptr);
             for (size_t i = 0; i < nc; ++i) {
-                if (!mm[i]) continue;
+                U[i] = sv[i].U;
+                sig[i] = sv[i].sig;
+                if (!sv[i].m) continue;
                 double smax = 0.0;
-                for (int j = 0; j < mm[i]; ++j) smax = std::max(smax, sh[soff[i] + j]);
+                for (double x : sv[i].sh) smax = std::max(smax, x);
                 const double cut = eps * smax;
                 int kk = 0;
-                for (int j = 0; j < mm[i]; ++j) kk += sh[soff[i] + j] > cut;
+                for (double x : sv[i].sh) kk += x > cut;
                 k[i] = kk;
             }
             // projections: basis <- S U_k, transfer <- U_k^T T, C <- U_s^T C U_t
@@ -448,35 +686,17 @@ struct Builder {
     }
 };
 
-}  // namespace
 
-H2Mat* h2mat_build(const h2f_build_desc* dp, int64_t* rank_out, double* seconds) {
-    if (!dp || dp->n <= 0 || dp->num_nodes <= 0) throw Error(H2F_E_ARG, "empty H2 build description");
-    const h2f_build_desc& d = *dp;
-    if (d.dim < 1 || d.dim > 3) throw Error(H2F_E_ARG, "dim must be 1, 2 or 3");
-    if (d.family < 0 || d.family > 2) throw Error(H2F_E_ARG, "unknown kernel family");
-    if (d.top_level >= 0 && (d.p0 < 1 || d.p0 + d.depth / 2 > 32)) throw Error(H2F_E_ARG, "p0 out of range");
-    Context& X = ctx();
-    auto now = [] { return std::chrono::steady_clock::now(); };
-    auto t0 = now();
-    Region R(size_t(256) << 20);
-    Builder B(d, R);
-    B.construct();
-    X.sync();
-    auto t1 = now();
-    if (d.top_level >= 0 && d.eps > 0) {
-        B.qr_sweep();
-        B.recompress(d.eps);
-        B.qr_sweep();
-    }
-    X.sync();
-    auto t2 = now();
-    // final layout: leaf bases, transfers, couplings, dense blocks
+// final layout (leaf bases, transfers, couplings, dense blocks) in one new
+// arena allocation; dense blocks are copied from the builder's buffers or,
+// for a fresh construction, evaluated straight into it
+H2Mat* pack_matrix(Builder& B, std::vector<int64_t>& rank) {
+    const h2f_build_desc& d = B.d;
     const int64_t N = d.num_nodes;
     const int nlev = d.depth + 1;
-    std::vector<int64_t> leaf_off(N, -1), trans_off(N, -1), rank(N, -1), coup_off, dense_off;
+    std::vector<int64_t> leaf_off(N, -1), trans_off(N, -1), coup_off, dense_off;
+    rank.assign(N, -1);
     int64_t pos = 0;
-    CopyBuild pack;
     std::vector<std::pair<int64_t, std::pair<const double*, int64_t>>> pieces;  // (offset, (src, count))
     for (int64_t c = 0; c < N; ++c) {
         rank[c] = B.rk[c] < 0 ? -1 : B.rk[c];
@@ -504,30 +724,24 @@ H2Mat* h2mat_build(const h2f_build_desc* dp, int64_t* rank_out, double* seconds)
     for (int64_t i = 0; i < ndense; ++i) {
         dense_off.push_back(pos);
         const int s = int(d.dense_pairs[2 * i]), t = int(d.dense_pairs[2 * i + 1]);
-        pos += int64_t(B.rows(s)) * B.rows(t);
+        const int64_t cnt = int64_t(B.rows(s)) * B.rows(t);
+        if (!B.dense_buf.empty()) pieces.push_back({pos, {B.dense_buf[size_t(i)], cnt}});
+        pos += cnt;
     }
     double* vals = static_cast<double*>(dalloc(sizeof(double) * std::max<int64_t>(pos, 1)));
-    // contiguous pieces as (cnt / 256) x 256 row blocks plus one remainder row
-    for (auto& pc : pieces) {
-        const int64_t cnt = pc.second.second, full = cnt / 256, rem = cnt % 256;
-        double* dst = vals + pc.first;
-        const double* src = pc.second.first;
-        for (int64_t r0 = 0; r0 < full; r0 += int64_t(1) << 24) {
-            const int64_t nr = std::min<int64_t>(full - r0, int64_t(1) << 24);
-            pack.add(dst + r0 * 256, 256, int(nr), 256, src + r0 * 256, 256, 0, COPY_SET);
-        }
-        if (rem) pack.add(dst + full * 256, rem, 1, int(rem), src + full * 256, rem, 0, COPY_SET);
-    }
+    CopyBuild pack;
+    for (auto& pc : pieces) Builder::copy_flat(pack, vals + pc.first, pc.second.first, pc.second.second);
     pack.launch();
-    Builder::EvalBuild ev;
-    for (int64_t i = 0; i < ndense; ++i) {
-        const int s = int(d.dense_pairs[2 * i]), t = int(d.dense_pairs[2 * i + 1]);
-        ev.add(B.pts + d.begin[s] * d.dim, B.pts + d.begin[t] * d.dim, vals + dense_off[i], B.rows(t), d.begin[s],
-               d.begin[t], B.rows(s), B.rows(t), 1);
+    if (B.dense_buf.empty()) {
+        Builder::EvalBuild ev;
+        for (int64_t i = 0; i < ndense; ++i) {
+            const int s = int(d.dense_pairs[2 * i]), t = int(d.dense_pairs[2 * i + 1]);
+            ev.add(B.pts + d.begin[s] * d.dim, B.pts + d.begin[t] * d.dim, vals + dense_off[i], B.rows(t),
+                   d.begin[s], d.begin[t], B.rows(s), B.rows(t), 1);
+        }
+        ev.launch(B.kparams());
     }
-    ev.launch(B.kparams());
-    X.sync();
-    auto t3 = now();
+    ctx().sync();
     h2f_matrix_desc md{};
     md.n = d.n;
     md.depth = d.depth;
@@ -551,13 +765,101 @@ H2Mat* h2mat_build(const h2f_build_desc* dp, int64_t* rank_out, double* seconds)
     md.coupling_off = coup_off.data();
     md.dense_off = dense_off.data();
     md.nvals = pos;
-    H2Mat* m = h2mat_create_device(&md, vals);
-    if (rank_out) std::memcpy(rank_out, rank.data(), sizeof(int64_t) * N);
+    return h2mat_create_device(&md, vals);
+}
+
+using Clock = std::chrono::steady_clock;
+double secs(Clock::time_point a, Clock::time_point b) { return std::chrono::duration<double>(b - a).count(); }
+
+}  // namespace
+
+H2Mat* h2mat_build(const h2f_build_desc* dp, int64_t* rank_out, double* seconds) {
+    if (!dp || dp->n <= 0 || dp->num_nodes <= 0) throw Error(H2F_E_ARG, "empty H2 build description");
+    const h2f_build_desc& d = *dp;
+    if (d.dim < 1 || d.dim > 3) throw Error(H2F_E_ARG, "dim must be 1, 2 or 3");
+    if (d.family < 0 || d.family > 2) throw Error(H2F_E_ARG, "unknown kernel family");
+    if (d.top_level >= 0 && (d.p0 < 1 || d.p0 + d.depth / 2 > 32)) throw Error(H2F_E_ARG, "p0 out of range");
+    const auto t0 = Clock::now();
+    Region R(size_t(256) << 20);
+    Builder B(d, R);
+    B.construct();
+    ctx().sync();
+    const auto t1 = Clock::now();
+    if (d.top_level >= 0 && d.eps > 0) {
+        B.qr_sweep();
+        B.recompress(d.eps);
+        B.qr_sweep();
+    }
+    ctx().sync();
+    const auto t2 = Clock::now();
+    std::vector<int64_t> rank;
+    H2Mat* m = pack_matrix(B, rank);
+    const auto t3 = Clock::now();
+    if (rank_out) std::memcpy(rank_out, rank.data(), sizeof(int64_t) * d.num_nodes);
     if (seconds) {
         // construction includes the dense near-field evaluation (done last,
         // straight into the operator's storage)
-        seconds[0] = std::chrono::duration<double>(t1 - t0).count() + std::chrono::duration<double>(t3 - t2).count();
-        seconds[1] = std::chrono::duration<double>(t2 - t1).count();
+        seconds[0] = secs(t0, t1) + secs(t2, t3);
+        seconds[1] = secs(t1, t2);
+    }
+    return m;
+}
+
+H2Mat* h2mat_absorb_low_rank(const H2Mat& A, const double* w_host, int rw, double eps, int64_t* rank_out,
+                             double* seconds) {
+    if (rw < 0) throw Error(H2F_E_ARG, "update rank must be >= 0");
+    const auto t0 = Clock::now();
+    // a build description over A's structure (no points: nothing is evaluated)
+    const int nlev = A.depth + 1;
+    std::vector<int64_t> adm, adm_ptr{0}, inner, inner_ptr{0}, dense, dense_ptr{0};
+    for (int l = 0; l < nlev; ++l) {
+        for (auto& p : A.adm[l]) adm.insert(adm.end(), {p.first, p.second});
+        for (auto& p : A.inner[l]) inner.insert(inner.end(), {p.first, p.second});
+        for (auto& p : A.dense[l]) dense.insert(dense.end(), {p.first, p.second});
+        adm_ptr.push_back(int64_t(adm.size() / 2));
+        inner_ptr.push_back(int64_t(inner.size() / 2));
+        dense_ptr.push_back(int64_t(dense.size() / 2));
+    }
+    h2f_build_desc d{};
+    d.n = A.n;
+    d.dim = 1;
+    d.depth = A.depth;
+    d.top_level = A.top;
+    d.num_nodes = A.nnodes;
+    d.parent = A.parent.data();
+    d.child_left = A.left.data();
+    d.child_right = A.right.data();
+    d.level = A.level.data();
+    d.begin = A.begin.data();
+    d.end = A.end.data();
+    d.adm_pairs = adm.data();
+    d.adm_ptr = adm_ptr.data();
+    d.inner_pairs = inner.data();
+    d.inner_ptr = inner_ptr.data();
+    d.dense_pairs = dense.data();
+    d.dense_ptr = dense_ptr.data();
+    Region R(size_t(256) << 20);
+    Builder B(d, R);
+    B.load(A);
+    double* Wd = R.alloc_n<double>(A.n * std::max(rw, 1));
+    if (rw > 0) {
+        H2F_CUDA(cudaMemcpyAsync(Wd, w_host, sizeof(double) * A.n * rw, cudaMemcpyHostToDevice, ctx().stream));
+        B.widen(Wd, rw);
+    }
+    ctx().sync();
+    const auto t1 = Clock::now();
+    if (d.top_level >= 0 && eps > 0) {
+        B.qr_sweep();
+        B.recompress(eps);
+        B.qr_sweep();
+    }
+    std::vector<int64_t> rank;
+    H2Mat* m = pack_matrix(B, rank);
+    const auto t2 = Clock::now();
+    if (rank_out) std::memcpy(rank_out, rank.data(), sizeof(int64_t) * A.nnodes);
+    if (seconds) {
+        seconds[0] = secs(t0, t1);
+        seconds[1] = secs(t1, t2);
     }
     return m;
 }

@@ -71,6 +71,9 @@ H2Mat* h2mat_create(const h2f_matrix_desc* d, const double* host_vals);
 H2Mat* h2mat_create_device(const h2f_matrix_desc* d, double* dev_vals);
 // device construction + recompression from points, tree and partition (build.cpp)
 H2Mat* h2mat_build(const h2f_build_desc* d, int64_t* rank_out, double* seconds);
+// A + W W^T absorbed into a new operator, then recompressed at eps (build.cpp)
+H2Mat* h2mat_absorb_low_rank(const H2Mat& A, const double* w_host, int rw, double eps, int64_t* rank_out,
+                             double* seconds);
 MatvecPlan& matvec_plan(H2Mat& m, int nrhs);
 // y_dev = A x_dev (both n x nrhs row-major device buffers), stream-ordered
 void matvec_device(H2Mat& m, const double* x_dev, double* y_dev, int nrhs);

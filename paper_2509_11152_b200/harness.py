@@ -101,12 +101,14 @@ class ExperimentConfig:
 
 def _operator(config):
     from . import problem as P
-    if config.device_build and not config.lru_rank:
+    if config.device_build:
         from .construct import build_problem_device
         tree, part, spec, h2, prm = build_problem_device(config.problem, config.n, **config.builder_overrides())
         bs = h2.build_seconds
-        return tree, spec, h2, prm, {"construction": bs["host_structure"] + bs["construction"],
-                                     "compression": bs["compression"]}
+        t = {"construction": bs["host_structure"] + bs["construction"], "compression": bs["compression"]}
+        if "low_rank_update" in bs:
+            t["low_rank_update"] = bs["low_rank_update"] + bs["compression_after_update"]
+        return tree, spec, h2, prm, t
     tree, part, spec, h2, prm = build_problem(config.problem, config.n, **config.builder_overrides())
     return tree, spec, h2, prm, dict(P.LAST_BUILD_TIMINGS)
 

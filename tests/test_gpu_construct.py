@@ -26,6 +26,8 @@ CASES = {
     "osc2d_4096": ("helmholtz3d", 4096, {"dim": 2, "p0": 8, "eta": 0.9}),
     "laplace2d_2048": ("laplace2d", 2048, {}),
     "cov3d_e8_4096": ("cov3d", 4096, {"eps_lu": 1e-8}),
+    # + the seeded rank-32 update absorbed on the device (h2core.py:342-405)
+    "lru_cov3d_4096": ("lru_cov3d", 4096, {}),
 }
 _cache = {}
 
@@ -52,6 +54,9 @@ def test_ranks_and_operator_match_host_builder(case):
     assert np.linalg.norm(yd - yh) <= 1e-8 * np.linalg.norm(yh)
     rows = np.random.default_rng(2).choice(hh.n, size=128, replace=False)
     ex = P.entry_block(spec, hh.tree.points, rows, np.arange(hh.n)) @ x
+    if prm.get("lru_rank", 0):
+        w = P.make_low_rank_factor(hh.n, prm["lru_rank"], prm.get("seed", 7))
+        ex = ex + w[rows] @ (w.T @ x)
     err_h = np.linalg.norm(yh[rows] - ex) / np.linalg.norm(ex)
     err_d = np.linalg.norm(yd[rows] - ex) / np.linalg.norm(ex)
     assert err_d <= 1.01 * err_h + 1e-14
@@ -132,3 +137,22 @@ def test_harness_and_cli_device_build(tmp_path):
     assert rep["kmax_construction"] == 43 and rep["h2_bytes"] > 0
     assert cli.main(["run", "--problem", "cov2d", "--n", "4096", "--device-build", "--out", str(tmp_path)]) == 0
     assert json.load(open(tmp_path / "report.json"))["config"]["device_build"] is True
+
+
+def test_absorb_low_rank_on_host_built_operator():
+    # device absorb of a host-built operator = host absorb_low_rank (ranks, operator)
+    import copy
+
+    _, _, _, h0, prm = P.build_problem("cov3d", 2048)
+    w = P.make_low_rank_factor(2048, 16, 3)
+    from paper_2509_11152_b200.construct import absorb_low_rank_device
+
+    hh = P.absorb_low_rank(copy.deepcopy(h0), w, prm["eps"])  # (before h0 caches a device handle)
+    hd = absorb_low_rank_device(h0, w, prm["eps"])
+    assert np.array_equal(ranks(hd), ranks(hh))
+    x = np.random.default_rng(5).standard_normal(2048)
+    yh = H.matvec(hh, x)
+    assert np.linalg.norm(H.matvec(hd, x) - yh) <= 1e-8 * np.linalg.norm(yh)
+    # the input operator is untouched
+    y0 = H.matvec(h0, x)
+    assert np.linalg.norm(y0 - yh) > 1e-6 * np.linalg.norm(yh)
