@@ -22,6 +22,11 @@ pytestmark = pytest.mark.gpu
 ROBUST = ["cov2d_1024", "cov3d_2048", "cov2d_4096", "cov3d_e8_4096", "cov2d_16384", "cov3d_e8_16384"]
 SENSITIVE = ["laplace2d_2048", "helmholtz3d_2048", "laplace3d_4096", "osc2d_4096", "laplace3d_16384",
              "lru_cov3d_4096", "osc2d_65536"]
+# cases whose backward error is chaotic for the reference itself: rounding-
+# level (1e-14) perturbations of the operator move the reference's own e_b by
+# decades (tests/golden/*_draws.json), so one draw is compared as a
+# distribution (test_backward_error_distribution_chaotic), not pointwise
+CHAOTIC = ["osc2d_65536"]
 
 _fac_cache = {}
 
@@ -128,7 +133,7 @@ def test_default_completion_pivots_and_solution(case):
     assert np.linalg.norm(x - g["x"]) <= 1e-8 * np.linalg.norm(g["x"])
 
 
-@pytest.mark.parametrize("case", ROBUST + SENSITIVE)
+@pytest.mark.parametrize("case", ROBUST + [c for c in SENSITIVE if c not in CHAOTIC])
 def test_solution_and_backward_error(case):
     g = load(case)
     h2, prm, fac = gpu_factor(case)
@@ -365,3 +370,56 @@ def test_device_harness_report_matches_reference_schema():
     assert rep["n"] == 1024 and rep["e_b"] <= 1e-10
     assert set(["factorization", "solve"]) <= set(rep["timings"])
     assert "partial_lu" in rep["phases"] and len(rep["levels"]) == len(rep["ranks"])
+
+
+def _perturbed(h2, seed, p=1e-14):
+    # the oracle draws' operator (scripts/oracle_big.py perturb=1e-14 seed=s):
+    # dense blocks * (1 + p z), z ~ N(0,1) per block in sorted key order,
+    # symmetrised on diagonal blocks
+    import copy
+
+    out = copy.copy(h2)
+    object.__setattr__(out, "_h2f_device", None)
+    if seed == 0:
+        return out
+    rng = np.random.default_rng(seed)
+    dense = {}
+    for key in sorted(h2.dense):
+        blk = h2.dense[key]
+        z = rng.standard_normal(blk.shape)
+        if key[0] == key[1]:
+            z = 0.5 * (z + z.T)
+        dense[key] = blk * (1.0 + p * z)
+    out.dense = dense
+    return out
+
+
+@pytest.mark.parametrize("case", CHAOTIC)
+def test_backward_error_distribution_chaotic(case):
+    # paired draws: the unperturbed operator and 23 rounding-level
+    # perturbations, factored + solved on the GPU; the reference algorithm's
+    # e_b on the same 24 operators is committed (tests/golden/<case>_draws.json,
+    # the oracle pinned to the reference).  Contract: the median refined e_b
+    # within 10x of the reference's median, and the two samples not
+    # distinguishable (rank-sum test, p > 0.01)
+    import json
+    import os
+
+    from scipy.stats import mannwhitneyu
+
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", f"{case}_draws.json")))
+    seeds = [d["seed"] for d in ref["draws"]]
+    ref_eb = np.array([d["e_b"] for d in ref["draws"]])
+    _, _, _, h2, prm = problem(case)
+    x_true = np.random.Generator(np.random.Philox(7)).standard_normal(h2.n)
+    got = []
+    for sd in seeds:
+        hp = _perturbed(h2, sd)
+        b = H.matvec(hp, x_true)
+        fac = H.factorize(hp, prm["eps_lu"])
+        x = H.refined_solve(hp, fac, b, steps=1)
+        got.append(np.linalg.norm(H.matvec(hp, x) - b) / np.linalg.norm(b))
+        del fac, hp
+    got = np.array(got)
+    assert np.median(got) <= 10 * np.median(ref_eb), (np.median(got), np.median(ref_eb))
+    assert mannwhitneyu(np.log(got), np.log(ref_eb)).pvalue > 0.01
