@@ -205,6 +205,56 @@ int h2f_matrix_values(h2f_matrix m, double* vals);
 int h2f_factorize(h2f_matrix m, double eps_lu, double norm_estimate, const double* v0,
                   h2f_factor* out, h2f_status* status);
 int h2f_factor_destroy(h2f_factor f);
+
+/* ---- subtree-sharded factorization ---------------------------
+ * The same factorization as h2f_factorize (factorization.py:204-271: same
+ * colouring, batches, kept counts, fill decisions, pivots and bits), with the
+ * work split over `world` processes, one per GPU.  Cluster c is owned by the
+ * rank of its ancestor at the top level (contiguous subtrees); a block (a, b)
+ * lives on the owners of a and of b.  Per batch (factorization.py:433-505):
+ * owners augment / eliminate their clusters; Q~ and the eliminator panels
+ * [G | -W] travel to the ranks that hold a neighbour block (all-to-all);
+ * every holder projects and Schur-updates its own copy; kept counts, pivot
+ * status and fill-candidate norms are max-reduced so every rank's host
+ * scheduler makes the same decisions.  The dense top matrix is sum-reduced
+ * (each block added by one rank) and factored on every rank, and the cluster
+ * factors are broadcast at the end, so the returned factor is complete and
+ * replicated: h2f_solve / h2f_refined_solve work on it unchanged.
+ *
+ * The collectives are callbacks (the host binds them to torch.distributed:
+ * NCCL over NVLink on a GPU box, gloo for tests).  Each is called with the
+ * library stream drained and must return with its output written (device
+ * buffers: complete with respect to the library stream, i.e. synchronised). */
+typedef struct {
+    int32_t rank, world;
+    void* user;
+    /* element-wise max over ranks of n doubles, in place, HOST memory */
+    int (*allreduce_max)(void* user, double* buf, int64_t n);
+    /* element-wise sum over ranks of n doubles, in place, DEVICE memory */
+    int (*allreduce_sum_dev)(void* user, double* buf, int64_t n);
+    /* all-to-all of DEVICE bytes: send holds send_counts[g] bytes for rank g,
+     * packed in rank order; recv receives recv_counts[g] bytes from rank g,
+     * in rank order (counts are known to both sides) */
+    int (*alltoallv_dev)(void* user, const void* send, const int64_t* send_counts, void* recv,
+                         const int64_t* recv_counts);
+    /* broadcast of `bytes` DEVICE bytes from rank root, in place */
+    int (*broadcast_dev)(void* user, void* buf, int64_t bytes, int32_t root);
+} h2f_comm;
+
+/* shard statistics of the last sharded factorization in this process:
+ * stats[0] clusters eliminated here, [1] clusters eliminated by all ranks,
+ * [2] bytes sent by the all-to-alls, [3] collective calls, [4] Schur target
+ * tiles computed here, [5] batches, [6] seconds inside the collectives
+ * (host wall time), [7] factor-broadcast bytes */
+int h2f_factorize_sharded(h2f_matrix m, double eps_lu, double norm_estimate, const double* v0,
+                          const h2f_comm* comm, h2f_factor* out, h2f_status* status);
+int h2f_shard_stats(double* stats);
+/* owner rank of every node under a `world`-way split into contiguous
+ * subtrees of the top level (-1 above it); parent/level as in
+ * h2f_matrix_desc.  Host-only, no device work. */
+int h2f_shard_owners(int64_t num_nodes, const int64_t* parent, const int64_t* level, int32_t top_level,
+                     int32_t world, int32_t* owner);
+
 int h2f_solve(h2f_factor f, const double* b, double* x, int64_t nrhs);
 int h2f_solve_dev(h2f_factor f, const double* b_dev, double* x_dev, int64_t nrhs);
 int h2f_refined_solve(h2f_matrix m, h2f_factor f, const double* b, double* x, int32_t steps);

@@ -81,6 +81,19 @@ class ClusterInfo(C.Structure):
                 ("num_edges", C.c_int32), ("offset", C.c_int64)]
 
 
+# collective callbacks of h2f_comm (include/h2f.h)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, f64p, C.c_int64)
+ALLREDUCE_DEV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, i64p, C.c_void_p, i64p)
+BROADCAST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32)
+
+
+class Comm(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("user", C.c_void_p),
+                ("allreduce_max", ALLREDUCE_FN), ("allreduce_sum_dev", ALLREDUCE_DEV_FN),
+                ("alltoallv_dev", ALLTOALLV_FN), ("broadcast_dev", BROADCAST_FN)]
+
+
 _SIGS = {
     "h2f_init": (C.c_int, [C.c_int, C.c_double]),
     "h2f_last_error": (C.c_char_p, []),
@@ -109,6 +122,10 @@ _SIGS = {
     "h2f_norm2": (C.c_int, [C.c_void_p, f64p, C.c_int32, f64p]),
     "h2f_factorize": (C.c_int, [C.c_void_p, C.c_double, C.c_double, f64p, C.POINTER(C.c_void_p),
                                 C.POINTER(Status)]),
+    "h2f_factorize_sharded": (C.c_int, [C.c_void_p, C.c_double, C.c_double, f64p, C.POINTER(Comm),
+                                        C.POINTER(C.c_void_p), C.POINTER(Status)]),
+    "h2f_shard_stats": (C.c_int, [f64p]),
+    "h2f_shard_owners": (C.c_int, [C.c_int64, i64p, i64p, C.c_int32, C.c_int32, i32p]),
     "h2f_factor_destroy": (C.c_int, [C.c_void_p]),
     "h2f_solve": (C.c_int, [C.c_void_p, f64p, f64p, C.c_int64]),
     "h2f_solve_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),

@@ -338,13 +338,13 @@ int h2f_norm2(h2f_matrix m, const double* v0, int32_t iters, double* est) {
     return guard([&] { *est = norm2_estimate(*m->m, v0, iters); });
 }
 
-int h2f_factorize(h2f_matrix m, double eps_lu, double norm_estimate, const double* v0, h2f_factor* out,
-                  h2f_status* status) {
+static int factorize_entry(h2f_matrix m, double eps_lu, double norm_estimate, const double* v0,
+                           const h2f_comm* comm, h2f_factor* out, h2f_status* status) {
     std::lock_guard<std::recursive_mutex> hold(g_lock);
     if (status) *status = {H2F_OK, -1, -1};
     try {
         bind_device();
-        Factorization* f = factorize(*m->m, eps_lu, norm_estimate, v0);
+        Factorization* f = factorize(*m->m, eps_lu, norm_estimate, v0, comm);
         *out = new h2f_factor_s{f};
         return H2F_OK;
     } catch (const Error& e) {
@@ -359,6 +359,42 @@ int h2f_factorize(h2f_matrix m, double eps_lu, double norm_estimate, const doubl
         g_err = e.what();
         if (status) *status = {H2F_E_INTERNAL, -1, -1};
         return H2F_E_INTERNAL;
+    }
+}
+
+int h2f_factorize(h2f_matrix m, double eps_lu, double norm_estimate, const double* v0, h2f_factor* out,
+                  h2f_status* status) {
+    return factorize_entry(m, eps_lu, norm_estimate, v0, nullptr, out, status);
+}
+
+int h2f_factorize_sharded(h2f_matrix m, double eps_lu, double norm_estimate, const double* v0,
+                          const h2f_comm* comm, h2f_factor* out, h2f_status* status) {
+    if (!comm) {
+        g_err = "h2f_factorize_sharded: null comm";
+        if (status) *status = {H2F_E_ARG, -1, -1};
+        return H2F_E_ARG;
+    }
+    return factorize_entry(m, eps_lu, norm_estimate, v0, comm, out, status);
+}
+
+int h2f_shard_stats(double* stats) {
+    return guard([&] {
+        const ShardStats& s = shard_stats();
+        const double v[8] = {s.local, s.total, s.bytes_sent, s.calls, s.tiles_here, s.batches, s.seconds,
+                             s.gather_bytes};
+        std::memcpy(stats, v, sizeof(v));
+    });
+}
+
+int h2f_shard_owners(int64_t num_nodes, const int64_t* parent, const int64_t* level, int32_t top_level,
+                     int32_t world, int32_t* owner) {
+    try {
+        const std::vector<int> own = shard_owners_tree(num_nodes, parent, level, top_level, world);
+        for (size_t i = 0; i < own.size(); ++i) owner[i] = own[i];
+        return H2F_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
     }
 }
 

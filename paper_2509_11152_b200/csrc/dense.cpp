@@ -75,7 +75,7 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
         maxp = std::max<int>(maxp, int(cdiv(jobs[i].nfac, HH_NB)));
         jobs[i].Vt.clear();
         jobs[i].T.clear();
-        if (!keep && jobs[i].nfac > 0) vbuf[i] = scr.alloc_n<double>(int64_t(HH_NB) * jobs[i].L);
+        if (!keep && jobs[i].nfac > 0 && jobs[i].M) vbuf[i] = scr.alloc_n<double>(int64_t(HH_NB) * jobs[i].L);
     }
     for (int p = 0; p < maxp; ++p) {
         const int j0 = p * HH_NB;
@@ -112,6 +112,13 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
             for (size_t t = 0; t < w.size(); ++t) {
                 const PanelPlan& pp = w[t];
                 HhJob& J = jobs[pp.job];
+                if (!J.M) {
+                    // plan-only job (another rank's cluster in a sharded
+                    // factorization): it shaped the wave, nothing to launch
+                    J.Vt.push_back(nullptr);
+                    J.T.push_back(nullptr);
+                    continue;
+                }
                 HhPanelTask k{};
                 k.M = J.M;
                 k.ldm = J.ldm;
@@ -119,15 +126,15 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
                 k.T = scr.alloc_n<double>(HH_NB * HH_NB);
                 k.part = scr.alloc_n<double>(int64_t(2) * (pp.ncta + 1) * (HH_NB + 2));
                 k.gram = scr.alloc_n<double>(int64_t(pp.ncta) * HH_NB * HH_NB);
-                k.bar = bars + 2 * t;
+                k.bar = bars + 2 * tasks.size();
                 k.L = J.L;
                 k.j0 = pp.j0;
                 k.nbp = pp.nbp;
                 k.chunk = pp.chunk;
                 k.cta0 = cta0;
                 k.ncta = pp.ncta;
+                for (int c = 0; c < pp.ncta; ++c) owner.push_back(int32_t(tasks.size()));
                 tasks.push_back(k);
-                for (int c = 0; c < pp.ncta; ++c) owner.push_back(int32_t(t));
                 cta0 += pp.ncta;
                 max_chunk = std::max(max_chunk, pp.chunk);
                 J.Vt.push_back(k.Vt);
@@ -148,6 +155,7 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
                 max_trail = std::max(max_trail, ntrail);
                 gu.add1(At, J.ldm, ntrail, L, GEMM_ADD, contrib(W2, ntrail, 1, k.Vt, L, 0, pp.nbp, -1.0));
             }
+            if (tasks.empty()) continue;
             cudaError_t e = launch_hh_panel(upload(tasks), upload(owner), int32_t(owner.size()), max_chunk, st);
             if (e != cudaSuccess)
                 throw Error(H2F_E_CUDA, std::string("cooperative Householder panel launch: ") + cudaGetErrorString(e));
@@ -169,7 +177,7 @@ void hh_apply_q(const std::vector<HhJob>& jobs, const std::vector<HhApply>& xs, 
         for (size_t i = 0; i < jobs.size(); ++i) {
             const HhJob& J = jobs[i];
             const HhApply& X = xs[i];
-            if (p >= int(J.Vt.size()) || X.nx <= 0) continue;
+            if (p >= int(J.Vt.size()) || X.nx <= 0 || !J.M) continue;
             const int j0 = p * HH_NB, nbp = std::min(HH_NB, J.nfac - j0), L = J.L - j0;
             double* Xp = X.X + int64_t(j0) * X.ldx;  // L x nx
             double* P = scr.alloc_n<double>(int64_t(nbp) * X.nx);
@@ -216,11 +224,11 @@ void qr_r_blocked(const std::vector<QrTask>& tasks, Region& scr) {
         J.ntot = t.s;
         J.nfac = std::min(t.s, t.wf);
         jobs.push_back(J);
-        ex.push_back(RExtractTask{t.Y, t.R, t.ldy, J.nfac, t.s});
+        if (t.Y) ex.push_back(RExtractTask{t.Y, t.R, t.ldy, J.nfac, t.s});
         maxn = std::max(maxn, t.s);
     }
     hh_factor(jobs, scr, false);
-    launch_r_extract(upload(ex), int32_t(ex.size()), maxn, ctx().stream);
+    if (!ex.empty()) launch_r_extract(upload(ex), int32_t(ex.size()), maxn, ctx().stream);
 }
 
 void complement_blocked(const std::vector<ComplementTask>& tasks, Region& scr) {
@@ -239,6 +247,10 @@ void complement_blocked(const std::vector<ComplementTask>& tasks, Region& scr) {
         J.ntot = kt;
         J.nfac = kt;
         jobs.push_back(J);
+        if (!t.W) {  // plan-only (sharded factorization): shapes the waves only
+            xs.push_back(HhApply{nullptr, s, 0});
+            continue;
+        }
         cp.add(t.W, s, kt, s, t.BT, s, 0, COPY_SET);     // the QR works on a copy of b_aug
         cp.add(t.Q + r, s, s, kt, t.BT, s, 1, COPY_SET);  // trailing columns: b_aug itself
         zero.zero(t.Q, s, s, r);
@@ -248,7 +260,7 @@ void complement_blocked(const std::vector<ComplementTask>& tasks, Region& scr) {
     }
     zero.launch();
     cp.launch();
-    launch_set_eye(upload(eye), int32_t(eye.size()), maxr, st);
+    if (!eye.empty()) launch_set_eye(upload(eye), int32_t(eye.size()), maxr, st);
     hh_factor(jobs, scr, true);
     hh_apply_q(jobs, xs, scr);
 }
@@ -324,11 +336,13 @@ void jacobi_wave(const std::vector<SvdTask>& tasks, const std::vector<size_t>& i
     int cta0 = 0;
     for (size_t w = 0; w < idx.size(); ++w) {
         const SvdTask& t = tasks[idx[w]];
+        if (!t.R) continue;  // plan-only (sharded factorization): sized the wave only
+        for (int c = 0; c < want[w]; ++c) owner.push_back(int32_t(ct.size()));
         ct.push_back(CoopSvdTask{t, cta0, want[w], bars + 2 * w, flags + 64 * w, scr.alloc_n<double>(std::max(t.m, 1))});
-        for (int c = 0; c < want[w]; ++c) owner.push_back(int32_t(w));
         cta0 += want[w];
         if (flags_out) (*flags_out)[idx[w]] = flags + 64 * w;
     }
+    if (ct.empty()) return;
     cudaError_t e = pairwise ? launch_jacobi_coop(upload(ct), int32_t(owner.size()), upload(owner), max_n, max_m,
                                                   thresh, st)
                              : launch_jacobi_block(upload(ct), int32_t(owner.size()), upload(owner), max_n, max_m,

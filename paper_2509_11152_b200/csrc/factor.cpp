@@ -38,7 +38,50 @@ Replay& replay() {
     return r;
 }
 
+ShardStats& shard_stats() {
+    static ShardStats st;
+    return st;
+}
+
+std::vector<int> shard_owners_tree(int64_t nnodes, const int64_t* parent, const int64_t* level, int top,
+                                   int world) {
+    // contiguous subtrees: the top-level clusters (ascending id = left to
+    // right) split into `world` equal runs; every descendant follows its
+    // ancestor, so a parent and its children always share an owner and the
+    // level transition (factorization.py:548-588) needs no exchange
+    if (world < 1) throw Error(H2F_E_ARG, "world size must be >= 1");
+    std::vector<int> own(size_t(nnodes), -1);
+    if (world == 1) {
+        std::fill(own.begin(), own.end(), 0);
+        return own;
+    }
+    if (top < 0) throw Error(H2F_E_ARG, "sharded factorization needs a compressed level (dense-only operator)");
+    std::vector<int> tops;
+    for (int64_t c = 0; c < nnodes; ++c)
+        if (level[c] == top) tops.push_back(int(c));
+    if (int64_t(tops.size()) < world)
+        throw Error(H2F_E_ARG, "sharded factorization: " + std::to_string(tops.size()) +
+                                   " clusters at the top level for " + std::to_string(world) + " ranks");
+    for (size_t i = 0; i < tops.size(); ++i) own[tops[i]] = int(int64_t(i) * world / int64_t(tops.size()));
+    // node ids grow with depth (parents before children)
+    for (int64_t c = 0; c < nnodes; ++c)
+        if (level[c] > top) {
+            if (parent[c] < 0 || parent[c] >= c) throw Error(H2F_E_ARG, "tree: parent after child");
+            own[c] = own[parent[c]];
+        }
+    return own;
+}
+
+std::vector<int> shard_owners(const H2Mat& M, int world) {
+    return shard_owners_tree(M.nnodes, M.parent.data(), M.level.data(), M.top, world);
+}
+
 namespace {
+
+struct Timer {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    double s() const { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
+};
 
 constexpr double PIVOT_RTOL = 1e-14;      // factorization.py:47
 constexpr double FILL_DROP_FACTOR = 1e-2; // factorization.py:55
@@ -203,7 +246,10 @@ void complement(const std::vector<ComplementTask>& tasks, Region& scr) {
     int lim = min_s;
     if (const char* env = std::getenv("H2F_SMALL_N_MAX")) lim = std::min(lim, std::atoi(env));
     std::vector<ComplementTask> small, big;
-    for (auto& t : tasks) (t.s > lim && t.kt > 0 ? big : small).push_back(t);
+    for (auto& t : tasks) {
+        if (t.s > lim && t.kt > 0) big.push_back(t);  // plan-only tasks (Q == null) shape the waves
+        else if (t.Q) small.push_back(t);
+    }
     if (!small.empty()) launch_complement(upload(small), int32_t(small.size()), ctx().stream);
     if (!big.empty()) complement_blocked(big, scr);
 }
@@ -212,10 +258,33 @@ class Factorizer {
   public:
     Factorizer(H2Mat& m, Factorization& f) : M(m), F(f) {}
     void run(double norm_estimate, const double* v0);
+    void shard(const h2f_comm* c);
 
   private:
     H2Mat& M;
     Factorization& F;
+    // ---- subtree sharding (h2f_factorize_sharded).  world
+    // == 1: every predicate below is true and no collective is called.
+    const h2f_comm* comm = nullptr;
+    int rank = 0, world = 1;
+    std::vector<int> owner;  // node -> rank
+    bool sharded() const { return world > 1; }
+    bool mine(int c) const { return world == 1 || owner[c] == rank; }
+    // a block (a, b) lives on the owners of a and of b
+    bool holds(Key k) const { return world == 1 || owner[key_a(k)] == rank || owner[key_b(k)] == rank; }
+    // ranks other than c's owner that hold a block touching c (they need
+    // c's Q~ and eliminator panels)
+    std::vector<int> dests(const Lvl& L, int c) const;
+    void coll_check(int rc, const char* what);
+    void allreduce_max(double* buf, int64_t n);
+    // one all-to-all of per-cluster device payloads: rows of `bytes` from
+    // src[i] (owned here) to each rank of dests; returns the receive buffer
+    // and, per payload received here, its address (recv_at[i], else null)
+    double* exchange(const std::vector<int>& cl, const std::vector<std::vector<int>>& dst,
+                     const std::vector<int64_t>& ndoubles, const std::vector<std::vector<std::pair<const double*, int64_t>>>& parts,
+                     Region& scr, std::vector<double*>& recv_at);
+    void gather_factors();
+    void stats_tiles(const GemmBuild& g);
     double eps_fill = 0, drop = 0;
     PhaseClock clock;
     Region scratch[2] = {Region(size_t(64) << 20), Region(size_t(64) << 20)};
@@ -286,6 +355,10 @@ std::unique_ptr<Lvl> Factorizer::leaf_level(int level) {
             if (M.level[pr.first] != level || M.level[pr.second] != level)
                 throw Error(H2F_E_INTERNAL, "assertion: dense leaf block away from the leaf level");
             const int rs = int(M.rows(pr.first)), cs = int(M.rows(pr.second));
+            if (!holds(mkkey(pr.first, pr.second))) {  // another rank's block: shape only
+                L->D[mkkey(pr.first, pr.second)] = View{nullptr, cs, rs, cs};
+                continue;
+            }
             double* dst = L->mem.alloc_n<double>(int64_t(rs) * cs);
             cp.add(dst, cs, rs, cs, M.vals + M.dense_off.at(mkkey(pr.first, pr.second)), cs, 0, COPY_SET);
             L->D[mkkey(pr.first, pr.second)] = View{dst, cs, rs, cs};
@@ -334,6 +407,10 @@ void Factorizer::level_complements(Lvl& L) {
         const int s = int(L.size[ci]);
         const View& V = L.basis[ci];
         const int k = V.cols;
+        if (!mine(L.clusters[ci])) {  // shapes the blocked waves only (bit-identical plans on every rank)
+            tasks.push_back(ComplementTask{nullptr, nullptr, nullptr, nullptr, s, k});
+            continue;
+        }
         double* bt = L.mem.alloc_n<double>(int64_t(std::max(k, 1)) * s);
         L.qv[ci] = L.mem.alloc_n<double>(int64_t(s) * s);
         gather.add(bt, s, k, s, V.p, V.ld, 1, COPY_SET);
@@ -360,6 +437,12 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         node_bi[batch[bi]] = bi;
     }
     auto in_batch = [&](int c) { return mark_node[c] == stamp; };
+    if (sharded()) {
+        ShardStats& ss = shard_stats();
+        ss.batches += 1;
+        ss.total += nb;
+        for (int c : batch) ss.local += mine(c);
+    }
 
     // ------------------------------------------------------------- augment
     // factorization.py:62-99, 377-407.  The fill row is projected onto the
@@ -416,6 +499,17 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 A.wf += parts.back().w;
             }
             A.skip = (A.wf == 0 || k == s);
+            A.m = std::min(n, A.wf);
+            if (!mine(c)) {
+                // another rank's cluster: its QR / Jacobi shape the waves
+                // (plans identical on every rank), nothing runs here
+                Q[bi] = nullptr;
+                if (A.skip) continue;
+                if (n > hh_min_n) qr_big.push_back(QrTask{nullptr, nullptr, A.wf, n, A.wf, 0, A.wf, 0});
+                if (n <= svd_smem_max) max_n_small = std::max(max_n_small, n);
+                else svd_big.push_back(SvdTask{nullptr, nullptr, A.m, n, nullptr, nb});
+                continue;
+            }
             Q[bi] = F.store.alloc_n<double>(int64_t(s) * s);
             A.QV = L.qv[ci];  // [V_perp | V], level_complements
             if (A.skip) {
@@ -468,6 +562,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         gz.launch(K_GEMM_AUG);
         auto qr_work = [](const std::vector<QrTask>& v, double& f, double& b) {
             for (auto& t : v) {
+                if (!t.Y) continue;
                 const double n = t.s, w = t.wf;
                 f += 2.0 * w * n * n - (w >= n ? 2.0 / 3.0 * n * n * n : 0.0);
                 b += 8.0 * n * w + 8.0 * n * n;
@@ -475,6 +570,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         };
         auto svd_work = [](const std::vector<SvdTask>& v, double& f, double& b) {
             for (auto& t : v) {
+                if (!t.R) continue;
                 f += 22.0 * double(t.m) * t.m * t.n;  // c_svd = 22 convention
                 b += 16.0 * double(t.m) * t.n;
             }
@@ -512,6 +608,14 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     tick(HT_SYNC1);
     std::vector<int> kept(kept_h, kept_h + nb);
     std::vector<int> degenerate(kept_h + nb, kept_h + 2 * nb);
+    if (sharded()) {  // every rank's scheduler needs every cluster's kept count
+        std::vector<double> kb(kept_h, kept_h + 2 * nb);
+        allreduce_max(kb.data(), 2 * nb);
+        for (int bi = 0; bi < nb; ++bi) {
+            kept[bi] = int(kb[bi]);
+            degenerate[bi] = int(kb[nb + bi]);
+        }
+    }
     if (replay().active) {
         Replay& R = replay();
         for (int bi = 0; bi < nb; ++bi) {
@@ -548,6 +652,11 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         for (int bi = 0; bi < nb; ++bi) {
             Aug& A = aug[bi];
             if (A.skip) continue;
+            if (!mine(batch[bi])) {  // plan-only Householder complement (wave shapes)
+                if (kept[bi] && !(fast_ok && A.m == A.n && !degenerate[bi]))
+                    cmp.push_back(ComplementTask{nullptr, nullptr, nullptr, nullptr, A.s, A.k + kept[bi]});
+                continue;
+            }
             if (kept[bi] == 0) {
                 keep.add(Q[bi], A.s, A.s, A.s, A.QV, A.s, 0, COPY_SET);
                 continue;
@@ -570,6 +679,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         double rf = 0, cf = 0, cb = 0;
         for (auto& t : ro) rf += 4.0 * double(t.s) * t.k * t.kept;
         for (auto& t : cmp) {
+            if (!t.Q) continue;
             cf += 4.0 * double(t.s) * t.s * t.s;
             cb += 16.0 * double(t.s) * t.s;
         }
@@ -584,6 +694,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         // development aid: orthogonality of every Q~ of the batch
         X.sync();
         for (int bi = 0; bi < nb; ++bi) {
+            if (!mine(batch[bi])) continue;
             const int sz = aug[bi].s;
             std::vector<double> q(size_t(sz) * sz);
             H2F_CUDA(cudaMemcpy(q.data(), Q[bi], q.size() * 8, cudaMemcpyDeviceToHost));
@@ -620,6 +731,22 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         // zero padding of couplings / transfer is logical: S and T keep their
         // stored extent and every consumer treats the added rows as zeros
     }
+    if (sharded()) {
+        // Q~ of every eliminated cluster to the ranks holding one of its
+        // blocks (they project their copies, factorization.py:410-430)
+        std::vector<std::vector<int>> dst(nb);
+        std::vector<int64_t> nd(nb);
+        std::vector<std::vector<std::pair<const double*, int64_t>>> parts(nb);
+        for (int bi = 0; bi < nb; ++bi) {
+            dst[bi] = dests(L, batch[bi]);
+            nd[bi] = int64_t(aug[bi].s) * aug[bi].s;
+            if (mine(batch[bi])) parts[bi] = {{Q[bi], nd[bi]}};
+        }
+        std::vector<double*> at;
+        exchange(batch, dst, nd, parts, scr, at);
+        for (int bi = 0; bi < nb; ++bi)
+            if (!mine(batch[bi])) Q[bi] = at[bi];
+    }
 
     tick(HT_AUG2);
     // ------------------------------------------------------------- project
@@ -634,6 +761,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         items.erase(std::unique(items.begin(), items.end()), items.end());
         GemmBuild p1, p2;
         for (auto& it : items) {
+            if (!holds(it.second)) continue;  // another rank's block: shape unchanged
             View& B = L.block(it.second, !it.first);
             const int a = key_a(it.second), b = key_b(it.second);
             const bool ra = in_batch(a), rb = in_batch(b);
@@ -699,7 +827,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             cf.s = s;
             cf.r = r;
             cf.offset = L.offset[ci];
-            cf.q = Q[bi];
+            cf.q = mine(c) ? Q[bi] : nullptr;  // others' factors arrive in gather_factors
             if (r == 0) continue;
             Elim e;
             e.c = c;
@@ -718,6 +846,20 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             e.offs.assign(e.np + 1, 0);
             for (int i = 0; i < e.np; ++i) e.offs[i + 1] = e.offs[i] + e.widths[i];
             e.W = e.offs[e.np];
+            const int nc = r >= trsm_dmma_min ? trsm_dmma_cols(r) : 0;
+            if (nc) max_r_dmma[nc == 32 ? 0 : 1] = std::max(max_r_dmma[nc == 32 ? 0 : 1], r);
+            if (!mine(c)) {
+                // another rank eliminates c; its panels arrive below if a
+                // block held here takes one of its Schur updates
+                e.G = e.MW = nullptr;
+                cf.edges.push_back({c, EDGE_SELF, nullptr, e.W, kt});
+                for (int i = 1; i < e.np; ++i) {
+                    const int o = e.ids[i];
+                    cf.edges.push_back({o, L.done[L.at(o)] ? EDGE_SKEL : EDGE_FULL, nullptr, e.W, e.widths[i]});
+                }
+                el.push_back(std::move(e));
+                continue;
+            }
             e.G = scr.alloc_n<double>(int64_t(r) * e.W);
             e.MW = F.store.alloc_n<double>(int64_t(r) * e.W);
             cf.lu = F.store.alloc_n<double>(int64_t(r) * r);
@@ -748,7 +890,6 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 lt.status = status_d + bi;
                 lus.push_back(lt);
             }
-            const int nc = r >= trsm_dmma_min ? trsm_dmma_cols(r) : 0;
             for (int64_t c0 = 0; c0 < e.W; c0 += (nc ? nc : 128)) {
                 TrsmTask tt{};
                 tt.LU = cf.lu;
@@ -762,7 +903,6 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 tt.col0 = int(c0);
                 tt.mode = TRSM_ELIMINATOR;
                 (nc == 32 ? trs32 : nc == 16 ? trs16 : trs).push_back(tt);
-                if (nc) max_r_dmma[nc == 32 ? 0 : 1] = std::max(max_r_dmma[nc == 32 ? 0 : 1], r);
             }
             // edges (factorization.py:453-456)
             cf.edges.push_back({c, EDGE_SELF, e.MW, e.W, kt});
@@ -776,6 +916,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         panels.launch();
         double lf = 0, lb = 0, tf = 0, tb = 0;
         for (auto& e : el) {
+            if (!e.MW) continue;
             const double r = e.r, W = double(e.W);
             lf += 2.0 / 3.0 * r * r * r;
             lb += 16.0 * r * r;
@@ -800,6 +941,28 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         }
     }
 
+    if (sharded()) {
+        // eliminator panels [G | -W] of every eliminated cluster to the ranks
+        // holding a block it updates (factorization.py:122-126, 476-505)
+        std::vector<int> cl(el.size());
+        std::vector<std::vector<int>> dst(el.size());
+        std::vector<int64_t> nd(el.size());
+        std::vector<std::vector<std::pair<const double*, int64_t>>> parts(el.size());
+        for (size_t i = 0; i < el.size(); ++i) {
+            const Elim& e = el[i];
+            cl[i] = e.c;
+            dst[i] = dests(L, e.c);
+            nd[i] = 2 * int64_t(e.r) * e.W;
+            if (e.MW) parts[i] = {{e.G, int64_t(e.r) * e.W}, {e.MW, int64_t(e.r) * e.W}};
+        }
+        std::vector<double*> at;
+        exchange(cl, dst, nd, parts, scr, at);
+        for (size_t i = 0; i < el.size(); ++i)
+            if (!el[i].MW && at[i]) {
+                el[i].G = at[i];
+                el[i].MW = at[i] + int64_t(el[i].r) * el[i].W;
+            }
+    }
     tick(HT_ELIM);
     // Schur updates (factorization.py:122-126) fused with the scatter into the
     // target blocks (factorization.py:476-505).  (target, contribution) pairs
@@ -822,6 +985,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         int M, N;
         GemmContrib g;
         int64_t base, ntiles;
+        bool here;  // this rank holds the would-be block and computes its norm
     };
     std::vector<Cand> cands;
     int64_t npairs = 0;  // updates of the batch
@@ -856,10 +1020,12 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             for (int j = i; j < e.np; ++j) {
                 if (i == 0 && j == 0) {
                     const View& Dcc = *L.diag[e.ci];
+                    if (!Dcc.p) continue;  // held by another rank (sharded)
                     out.push_back({&Dcc, Dcc.p + int64_t(r) * Dcc.ld + r, Dcc.ld, kt, kt, 0, 0});
                 } else if (i == 0) {
                     const Entry& en = e.ents[j - 1];
                     const View* B = en.v;
+                    if (!B->p) continue;
                     if (key_a(en.key) == c) out.push_back({B, B->p + int64_t(r) * B->ld, B->ld, kt, B->cols, 0, j});
                     else out.push_back({B, B->p + r, B->ld, B->rows, kt, 0, -j - 1});
                 } else {
@@ -873,8 +1039,11 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                         while (walk != walk_end && walk->first < e.ids[j]) ++walk;
                         if (walk != walk_end && walk->first == e.ids[j]) B = walk->second.v;
                     }
-                    if (B) out.push_back({B, B->p, B->ld, B->rows, B->cols, i, j});
-                    else out.push_back({nullptr, nullptr, 0, e.widths[i], e.widths[j], i, j});
+                    if (B) {
+                        if (B->p) out.push_back({B, B->p, B->ld, B->rows, B->cols, i, j});
+                    } else {
+                        out.push_back({nullptr, nullptr, 0, e.widths[i], e.widths[j], i, j});
+                    }
                 }
             }
         // stable counting sort of the targeted updates by bucket; candidates
@@ -907,6 +1076,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             cd.g = contrib(e.G + e.offs[u.i], e.W, 1, e.MW + e.offs[u.j], e.W, 0, e.r);
             cd.base = 0;
             cd.ntiles = GemmBuild::tiles(cd.M, cd.N);
+            cd.here = holds(cd.key);
             cands.push_back(cd);
         }
     }
@@ -992,34 +1162,52 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             }
         int64_t pos = ntc;
         for (auto& cd : cands) {
+            if (!cd.here) continue;
             hc[pos] = cd.g;
             cd.base = sch.add_ext(nullptr, 0, cd.M, cd.N, GEMM_NORM, pos, 1, cd.g.K, cdiv(cd.g.K, GEMM_BK));
             ++pos;
         }
     }
     tick(HT_S3);
+    std::vector<size_t> lc;  // candidates whose norm is computed here
+    for (size_t i = 0; i < cands.size(); ++i)
+        if (cands[i].here) lc.push_back(i);
     double* norms_d = sch.norm_tiles ? scr.alloc_n<double>(sch.norm_tiles) : nullptr;
-    double* cand_ss_d = cands.empty() ? nullptr : scr.alloc_n<double>(cands.size());
+    double* cand_ss_d = lc.empty() ? nullptr : scr.alloc_n<double>(lc.size());
     sch.launch(K_GEMM_SCHUR, norms_d, schur_bytes);
-    if (!cands.empty()) {
-        std::vector<int64_t> seg(cands.size() + 1, 0);
-        for (size_t i = 0; i < cands.size(); ++i) seg[i + 1] = cands[i].base + cands[i].ntiles;
-        for (size_t i = 0; i < cands.size(); ++i)
-            if (cands[i].base != seg[i]) throw Error(H2F_E_INTERNAL, "assertion: norm segments");
+    stats_tiles(sch);
+    if (!lc.empty()) {
+        std::vector<int64_t> seg(lc.size() + 1, 0);
+        for (size_t k = 0; k < lc.size(); ++k) seg[k + 1] = cands[lc[k]].base + cands[lc[k]].ntiles;
+        for (size_t k = 0; k < lc.size(); ++k)
+            if (cands[lc[k]].base != seg[k]) throw Error(H2F_E_INTERNAL, "assertion: norm segments");
         ProfScope ps(K_REDUCE, 0.0, 8.0 * double(sch.norm_tiles));
-        launch_sumsq_reduce(norms_d, upload(seg), int32_t(cands.size()), cand_ss_d, st);
+        launch_sumsq_reduce(norms_d, upload(seg), int32_t(lc.size()), cand_ss_d, st);
     }
     tick(HT_SCHUR);
     // one sync: LU status + candidate norms
-    const size_t nbytes_read = sizeof(int) * nb + sizeof(double) * cands.size() + 8;
+    const size_t nbytes_read = sizeof(int) * nb + sizeof(double) * lc.size() + 8;
     char* hbuf = static_cast<char*>(X.pinned_buf(nbytes_read + 64));
     int* status_h = reinterpret_cast<int*>(hbuf);
     double* ss_h = reinterpret_cast<double*>(hbuf + ((sizeof(int) * nb + 15) & ~size_t(15)));
     H2F_CUDA(cudaMemcpyAsync(status_h, status_d, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
-    if (!cands.empty())
-        H2F_CUDA(cudaMemcpyAsync(ss_h, cand_ss_d, sizeof(double) * cands.size(), cudaMemcpyDeviceToHost, st));
+    if (!lc.empty())
+        H2F_CUDA(cudaMemcpyAsync(ss_h, cand_ss_d, sizeof(double) * lc.size(), cudaMemcpyDeviceToHost, st));
     X.sync();
     tick(HT_SYNC2);
+    // candidate norms in reference order; sharded: max-reduced so that every
+    // rank takes the same fill decisions (each candidate is computed, with
+    // identical bits, by the owners of both of its clusters; -1 elsewhere)
+    std::vector<double> cand_ss(cands.size(), -1.0);
+    for (size_t k = 0; k < lc.size(); ++k) cand_ss[lc[k]] = ss_h[k];
+    if (sharded()) {
+        std::vector<double> red(size_t(nb) + cands.size());
+        for (int bi = 0; bi < nb; ++bi) red[bi] = status_h[bi];
+        std::copy(cand_ss.begin(), cand_ss.end(), red.begin() + nb);
+        allreduce_max(red.data(), int64_t(red.size()));
+        for (int bi = 0; bi < nb; ++bi) status_h[bi] = int(red[bi]);
+        std::copy(red.begin() + nb, red.end(), cand_ss.begin());
+    }
     for (int bi = 0; bi < nb; ++bi)
         if (status_h[bi]) {
             Error err(H2F_E_SINGULAR, "cluster " + std::to_string(batch[bi]) + " at level " +
@@ -1045,10 +1233,11 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             const Cand& cd = cands[i];
             auto it = made.find(cd.key);
             if (it != made.end()) {
-                news[it->second].cs.push_back(cd.g);
+                if (it->second >= 0) news[it->second].cs.push_back(cd.g);
                 continue;
             }
-            bool create_it = std::sqrt(ss_h[i]) > drop;
+            if (cand_ss[i] < 0) throw Error(H2F_E_INTERNAL, "assertion: fill candidate norm computed nowhere");
+            bool create_it = std::sqrt(cand_ss[i]) > drop;
             if (replay().active) {
                 Replay& R = replay();
                 auto rt = R.created.find((int64_t(L.level) << 32) | uint32_t(cd.creator));
@@ -1057,17 +1246,23 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 if (want != create_it) {
                     ++R.fill_changed;
                     // how far this run's own norm is from the drop tolerance
-                    const double lr = std::fabs(std::log10(std::max(std::sqrt(ss_h[i]), 1e-300) / drop));
+                    const double lr = std::fabs(std::log10(std::max(std::sqrt(cand_ss[i]), 1e-300) / drop));
                     ++R.fill_margin_hist[lr < 0.01 ? 0 : lr < 0.1 ? 1 : lr < 0.5 ? 2 : lr < 1.0 ? 3 : 4];
                 }
                 create_it = want;
             }
             if (create_it) {
+                L.fill_created.back().push_back(cd.key);
+                if (!cd.here) {  // another rank's block: structure only
+                    L.F[cd.key] = View{nullptr, cd.N, cd.M, cd.N};
+                    L.link(cd.key, false);
+                    made[cd.key] = -1;
+                    continue;
+                }
                 double* blk = L.mem.alloc_n<double>(int64_t(cd.M) * cd.N);
                 L.F[cd.key] = View{blk, cd.N, cd.M, cd.N};
                 L.link(cd.key, false);
                 made[cd.key] = int(news.size());
-                L.fill_created.back().push_back(cd.key);
                 news.push_back({blk, cd.N, cd.M, cd.N, {cd.g}});
             }
         }
@@ -1080,16 +1275,16 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         const int r = L.red[ci];
         if (r) {
             View& Dcc = L.dcc(ci);
-            Dcc.p += int64_t(r) * Dcc.ld + r;
+            if (Dcc.p) Dcc.p += int64_t(r) * Dcc.ld + r;
             Dcc.rows -= r;
             Dcc.cols -= r;
             for (auto& kv : L.touch[ci]) {
                 View& B = *kv.second.v;
                 if (key_a(kv.second.key) == c) {
-                    B.p += int64_t(r) * B.ld;
+                    if (B.p) B.p += int64_t(r) * B.ld;
                     B.rows -= r;
                 } else {
-                    B.p += r;
+                    if (B.p) B.p += r;
                     B.cols -= r;
                 }
             }
@@ -1120,6 +1315,11 @@ std::unique_ptr<Lvl> Factorizer::transition(Lvl& L) {
         N->offset[i] = pos;
         pos += N->size[i];
         const int kp = int(M.rank[p]);
+        N->k[i] = kp;
+        if (!mine(p)) {  // another rank's cluster: shape only
+            N->basis[i] = View{nullptr, kp, int(N->size[i]), kp};
+            continue;
+        }
         double* bas = N->mem.alloc_n<double>(int64_t(N->size[i]) * std::max(kp, 1));
         zero.zero(bas, kp, int(N->size[i]), kp);
         const TransferW& ta = L.T[L.at(a)];
@@ -1133,6 +1333,10 @@ std::unique_ptr<Lvl> Factorizer::transition(Lvl& L) {
     for (auto& pr : dense_pairs(nl)) {
         const int s = pr.first, t = pr.second;
         const int rs = nsize(s), cs = nsize(t);
+        if (!holds(mkkey(s, t))) {
+            N->D[mkkey(s, t)] = View{nullptr, cs, rs, cs};
+            continue;
+        }
         double* blk = N->mem.alloc_n<double>(int64_t(rs) * cs);
         zero.zero(blk, cs, rs, cs);
         N->D[mkkey(s, t)] = View{blk, cs, rs, cs};
@@ -1171,10 +1375,12 @@ std::unique_ptr<Lvl> Factorizer::transition(Lvl& L) {
         auto it = N->F.find(mkkey(p, q));
         if (it == N->F.end()) {
             const int rs = nsize(p), cs = nsize(q);
-            double* blk = N->mem.alloc_n<double>(int64_t(rs) * cs);
-            zero.zero(blk, cs, rs, cs);
+            double* blk = holds(mkkey(p, q)) ? N->mem.alloc_n<double>(int64_t(rs) * cs) : nullptr;
+            if (blk) zero.zero(blk, cs, rs, cs);
             it = N->F.emplace(mkkey(p, q), View{blk, cs, rs, cs}).first;
         }
+        if (!it->second.p) continue;  // held by other ranks
+        if (!kv.second.p) throw Error(H2F_E_INTERNAL, "assertion: held parent fill block from a child held elsewhere");
         const int ro = (a == M.left[p]) ? 0 : live_of(int(M.left[p]));
         const int co = (b == M.left[q]) ? 0 : live_of(int(M.left[q]));
         View& dst = it->second;
@@ -1206,14 +1412,19 @@ void Factorizer::finish_top(Lvl& L) {
     double* A = F.top_lu;
     zero.zero(A, n, int(n), int(n));
     auto live_of = [&](int c) { return L.live[L.at(c)]; };
+    // sharded: each block is added by the owner of its first cluster (who
+    // holds it), the other ranks' entries stay zero, and a sum-reduction
+    // assembles the matrix exactly (x + 0 = x)
     for (auto& pr : dense_pairs(L.level)) {
         const int s = pr.first, t = pr.second;
+        if (!mine(s)) continue;
         const View& V = L.D.at(mkkey(s, t));
         set.add(A + offs[s] * n + offs[t], n, V.rows, V.cols, V.p, V.ld, 0, COPY_SET);
         if (s != t) set.add(A + offs[t] * n + offs[s], n, V.cols, V.rows, V.p, V.ld, 1, COPY_SET);
     }
     for (auto& pr : M.adm[L.level]) {
         const int s = pr.first, t = pr.second;
+        if (!mine(s)) continue;
         const Key key = mkkey(s, t);
         const CouplingW& S = L.S.at(key);
         set.add(A + offs[s] * n + offs[t], n, S.rows, S.cols, S.p, S.ld, 0, COPY_SET);
@@ -1228,6 +1439,13 @@ void Factorizer::finish_top(Lvl& L) {
     zero.launch();
     set.launch();
     add.launch();
+    if (sharded()) {
+        ctx().sync();
+        Timer t;
+        coll_check(comm->allreduce_sum_dev(comm->user, A, n * n), "allreduce_sum_dev");
+        shard_stats().calls += 1;
+        shard_stats().seconds += t.s();
+    }
 }
 
 void Factorizer::dense_only_top() {
@@ -1300,7 +1518,207 @@ void Factorizer::dump_level_profile(int level) {
     std::fprintf(stderr, "\n");
 }
 
+
+// ---------------------------------------------------------------- sharding
+
+void Factorizer::shard(const h2f_comm* c) {
+    comm = c;
+    rank = c ? c->rank : 0;
+    world = c ? c->world : 1;
+    if (world < 1 || rank < 0 || rank >= world) throw Error(H2F_E_ARG, "comm: rank/world out of range");
+    if (world > 1 && (!c->allreduce_max || !c->allreduce_sum_dev || !c->alltoallv_dev || !c->broadcast_dev))
+        throw Error(H2F_E_ARG, "comm: missing collective callback");
+    owner = shard_owners(M, world);
+}
+
+std::vector<int> Factorizer::dests(const Lvl& L, int c) const {
+    std::vector<int> d;
+    const int oc = owner[c];
+    for (auto& kv : L.touch[L.at(c)]) {
+        const int g = owner[kv.first];
+        if (g != oc) d.push_back(g);
+    }
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+    return d;
+}
+
+void Factorizer::coll_check(int rc, const char* what) {
+    if (rc != 0) throw Error(H2F_E_INTERNAL, std::string("sharded factorization: collective ") + what +
+                                                 " failed with " + std::to_string(rc));
+}
+
+void Factorizer::allreduce_max(double* buf, int64_t n) {
+    Timer t;
+    coll_check(comm->allreduce_max(comm->user, buf, n), "allreduce_max");
+    shard_stats().calls += 1;
+    shard_stats().seconds += t.s();
+}
+
+void Factorizer::stats_tiles(const GemmBuild& g) {
+    // Schur target tiles computed here vs the batch schedule's total
+    // (identical on every rank: the host resolves all targets)
+    shard_stats().tiles_here += double(g.tile_start.back());
+}
+
+// Per-cluster payloads (cl[i], payload of nd[i] doubles made of parts[i])
+// from their owner to every rank in dst[i], as ONE all-to-all.  The send
+// buffer is packed by destination rank then payload order; receivers see
+// the payloads of each source rank in payload order, so recv_at[i] is the
+// payload's address here (null where this rank is not a destination).
+double* Factorizer::exchange(const std::vector<int>& cl, const std::vector<std::vector<int>>& dst,
+                             const std::vector<int64_t>& nd,
+                             const std::vector<std::vector<std::pair<const double*, int64_t>>>& parts, Region& scr,
+                             std::vector<double*>& recv_at) {
+    const size_t np = cl.size();
+    std::vector<int64_t> sendc(world, 0), recvc(world, 0);
+    for (size_t i = 0; i < np; ++i) {
+        const int src = owner[cl[i]];
+        for (int g : dst[i]) {
+            if (src == rank) sendc[g] += nd[i];
+            if (g == rank) recvc[src] += nd[i];
+        }
+    }
+    int64_t stot = 0, rtot = 0;
+    for (int g = 0; g < world; ++g) {
+        stot += sendc[g];
+        rtot += recvc[g];
+    }
+    double* sbuf = scr.alloc_n<double>(std::max<int64_t>(stot, 1));
+    double* rbuf = scr.alloc_n<double>(std::max<int64_t>(rtot, 1));
+    recv_at.assign(np, nullptr);
+    // pack: contiguous ranges copied as rows of PACK_W doubles
+    constexpr int PACK_W = 512;
+    CopyBuild pack;
+    auto copy_range = [&](double* d, const double* sp, int64_t cnt) {
+        const int64_t rows = cnt / PACK_W, rest = cnt - rows * PACK_W;
+        if (rows) pack.add(d, PACK_W, int(rows), PACK_W, sp, PACK_W, 0, COPY_SET);
+        if (rest) pack.add(d + rows * PACK_W, rest, 1, int(rest), sp + rows * PACK_W, rest, 0, COPY_SET);
+    };
+    int64_t so = 0, ro = 0;
+    for (int g = 0; g < world; ++g)
+        for (size_t i = 0; i < np; ++i) {
+            if (!std::binary_search(dst[i].begin(), dst[i].end(), g)) continue;
+            const int src = owner[cl[i]];
+            if (src == rank) {
+                int64_t o = 0;
+                for (auto& pt : parts[i]) {
+                    copy_range(sbuf + so + o, pt.first, pt.second);
+                    o += pt.second;
+                }
+                if (o != nd[i]) throw Error(H2F_E_INTERNAL, "assertion: exchange payload size");
+                so += nd[i];
+            }
+        }
+    // receive offsets: per source rank, payloads in order
+    for (int g = 0; g < world; ++g)
+        for (size_t i = 0; i < np; ++i)
+            if (owner[cl[i]] == g && std::binary_search(dst[i].begin(), dst[i].end(), rank)) {
+                recv_at[i] = rbuf + ro;
+                ro += nd[i];
+            }
+    pack.launch();
+    ctx().sync();
+    std::vector<int64_t> sb(world), rb(world);
+    for (int g = 0; g < world; ++g) {
+        sb[g] = sendc[g] * 8;
+        rb[g] = recvc[g] * 8;
+    }
+    Timer t;
+    coll_check(comm->alltoallv_dev(comm->user, sbuf, sb.data(), rbuf, rb.data()), "alltoallv_dev");
+    ShardStats& st = shard_stats();
+    st.calls += 1;
+    st.seconds += t.s();
+    st.bytes_sent += 8.0 * double(stot);
+    return rbuf;
+}
+
+// Every rank ends with every cluster's factor (q, lu, piv, eliminator): the
+// owner packs its clusters of a record into one staging buffer, broadcasts
+// it, and the others keep the broadcast buffer as their storage of those
+// clusters (no unpack copy).  Layout per cluster: q (s*s), lu (r*r), the
+// r x W eliminator, piv (r int32, padded to whole doubles).
+void Factorizer::gather_factors() {
+    Region stage(size_t(256) << 20);
+    for (auto& rec : F.recs) {
+        const size_t nc = rec.factors.size();
+        std::vector<int64_t> W(nc, 0), sz(nc, 0);
+        for (size_t i = 0; i < nc; ++i) {
+            const ClusterFactor& cf = rec.factors[i];
+            for (auto& e : cf.edges) W[i] += e.w;
+            const int64_t r = cf.r;
+            sz[i] = int64_t(cf.s) * cf.s + (r ? r * r + r * W[i] + (r + 1) / 2 : 0);
+        }
+        for (int g = 0; g < world; ++g) {
+            int64_t tot = 0;
+            for (size_t i = 0; i < nc; ++i)
+                if (owner[rec.factors[i].cluster] == g) tot += sz[i];
+            if (!tot) continue;
+            stage.reset();
+            double* buf = g == rank ? stage.alloc_n<double>(tot) : F.store.alloc_n<double>(tot);
+            if (g == rank) {
+                CopyBuild pack;
+                int64_t o = 0;
+                auto put = [&](const double* src, int64_t cnt) {
+                    constexpr int PACK_W = 512;
+                    const int64_t rows = cnt / PACK_W, rest = cnt - rows * PACK_W;
+                    if (rows) pack.add(buf + o, PACK_W, int(rows), PACK_W, src, PACK_W, 0, COPY_SET);
+                    if (rest) pack.add(buf + o + rows * PACK_W, rest, 1, int(rest), src + rows * PACK_W, rest, 0, COPY_SET);
+                    o += cnt;
+                };
+                for (size_t i = 0; i < nc; ++i) {
+                    const ClusterFactor& cf = rec.factors[i];
+                    if (owner[cf.cluster] != g) continue;
+                    const int64_t r = cf.r;
+                    put(cf.q, int64_t(cf.s) * cf.s);
+                    if (r) {
+                        put(cf.lu, r * r);
+                        put(cf.edges[0].mat, r * W[i]);
+                        // int32 pivots read as whole doubles: the arena
+                        // rounds every allocation up, so the pad is ours
+                        put(reinterpret_cast<const double*>(cf.piv), (r + 1) / 2);
+                    }
+                }
+                pack.launch();
+            }
+            ctx().sync();
+            Timer t;
+            coll_check(comm->broadcast_dev(comm->user, buf, tot * 8, g), "broadcast_dev");
+            ShardStats& st = shard_stats();
+            st.calls += 1;
+            st.seconds += t.s();
+            st.gather_bytes += 8.0 * double(tot);
+            if (g == rank) continue;
+            int64_t o = 0;
+            for (size_t i = 0; i < nc; ++i) {
+                ClusterFactor& cf = rec.factors[i];
+                if (owner[cf.cluster] != g) continue;
+                const int64_t r = cf.r;
+                cf.q = buf + o;
+                o += int64_t(cf.s) * cf.s;
+                if (r) {
+                    cf.lu = buf + o;
+                    o += r * r;
+                    double* mw = buf + o;
+                    int64_t eo = 0;
+                    for (auto& e : cf.edges) {
+                        e.mat = mw + eo;
+                        e.ld = W[i];
+                        eo += e.w;
+                    }
+                    o += r * W[i];
+                    cf.piv = reinterpret_cast<int32_t*>(buf + o);
+                    o += (r + 1) / 2;
+                }
+            }
+        }
+    }
+    ctx().sync();
+}
+
 void Factorizer::run(double norm_estimate, const double* v0) {
+    if (owner.empty()) owner = shard_owners(M, 1);
+    if (sharded()) shard_stats() = ShardStats{};
     level_prof = std::getenv("H2F_LEVEL_PROF") != nullptr && ctx().prof.on;
     if (level_prof) {
         ctx().prof.collect();
@@ -1411,6 +1829,7 @@ void Factorizer::run(double norm_estimate, const double* v0) {
             if (level_prof) dump_level_profile(level);
         }
     }
+    if (sharded()) gather_factors();
     clock.mark(PH_TOP);
     top_factor(F.top_lu, F.top_size);
     clock.mark(-1);
@@ -1436,12 +1855,14 @@ void Factorizer::run(double norm_estimate, const double* v0) {
 
 }  // namespace
 
-Factorization* factorize(H2Mat& m, double eps_lu, double norm_estimate, const double* v0_host) {
+Factorization* factorize(H2Mat& m, double eps_lu, double norm_estimate, const double* v0_host,
+                         const h2f_comm* comm) {
     auto f = std::make_unique<Factorization>();
     f->mat = &m;
     f->n = m.n;
     f->eps_lu = eps_lu;
     Factorizer fz(m, *f);
+    if (comm) fz.shard(comm);
     fz.run(norm_estimate, v0_host);
     return f.release();
 }

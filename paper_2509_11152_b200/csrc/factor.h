@@ -88,8 +88,25 @@ struct Replay {
 };
 Replay& replay();
 
-// throws Error(H2F_E_SINGULAR) with cluster/level set on a vanishing pivot
-Factorization* factorize(H2Mat& m, double eps_lu, double norm_estimate, const double* v0_host);
+// subtree sharding (h2f_factorize_sharded): counters of the last run
+struct ShardStats {
+    double local = 0, total = 0;   // clusters eliminated here / in all
+    double bytes_sent = 0, calls = 0;
+    double tiles_here = 0, batches = 0;
+    double seconds = 0;            // host wall time inside the collectives
+    double gather_bytes = 0;       // factor broadcast at the end
+};
+ShardStats& shard_stats();
+// node -> owner rank for a world-way split into contiguous subtrees of the
+// top level (-1 above the top level)
+std::vector<int> shard_owners(const H2Mat& m, int world);
+std::vector<int> shard_owners_tree(int64_t nnodes, const int64_t* parent, const int64_t* level, int top,
+                                   int world);
+
+// throws Error(H2F_E_SINGULAR) with cluster/level set on a vanishing pivot;
+// comm (world > 1): the subtree-sharded factorization, same result
+Factorization* factorize(H2Mat& m, double eps_lu, double norm_estimate, const double* v0_host,
+                         const h2f_comm* comm = nullptr);
 
 void solve_device(Factorization& f, const double* b_dev, double* x_dev, int nrhs);
 void refined_solve_device(H2Mat& m, Factorization& f, const double* b_dev, double* x_dev, int steps,

@@ -221,6 +221,12 @@ def factorize(h2, eps_lu, threads=1, norm_estimate=None):
     Raises FactorizationError when a redundant diagonal block is singular.
     """
     del threads  # API parity: clusters of a batch run as one device launch
+    return factorize_with(h2, eps_lu, norm_estimate)
+
+
+def factorize_with(h2, eps_lu, norm_estimate=None, comm=None):
+    """factorize() through h2f_factorize, or -- with `comm` (an h2f_comm,
+    see multigpu.TorchComm) -- through h2f_factorize_sharded."""
     dev = device_matrix(h2)
     v0 = None
     if norm_estimate is None:
@@ -230,10 +236,14 @@ def factorize(h2, eps_lu, threads=1, norm_estimate=None):
         est = float(norm_estimate)
     handle = C.c_void_p()
     st = L.Status()
-    code = L.lib().h2f_factorize(dev.handle, float(eps_lu), est,
-                                 L.ptr(v0) if v0 is not None else None,
-                                 C.byref(handle), C.byref(st))
+    v0p = L.ptr(v0) if v0 is not None else None
+    if comm is None:
+        code = L.lib().h2f_factorize(dev.handle, float(eps_lu), est, v0p, C.byref(handle), C.byref(st))
+    else:
+        code = L.lib().h2f_factorize_sharded(dev.handle, float(eps_lu), est, v0p, C.byref(comm.struct),
+                                             C.byref(handle), C.byref(st))
+        comm.reraise()
     if code == L.H2F_E_SINGULAR:
         raise FactorizationError(L.last_error())
-    L.check(code, "h2f_factorize")
+    L.check(code, "h2f_factorize" if comm is None else "h2f_factorize_sharded")
     return H2Factorization(h2.tree, _Handle(handle, dev))

@@ -13,6 +13,9 @@ if HERE not in sys.path:
 # LAPACK bits depend on the BLAS thread count
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 os.environ.setdefault("OMP_NUM_THREADS", "1")
+# the library context of the pytest process takes a bounded arena, so that
+# the multi-process tests (tests/test_gpu_sharded.py) find device memory
+os.environ.setdefault("H2F_ARENA_GB", "100")
 
 
 def pytest_configure(config):

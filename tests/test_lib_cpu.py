@@ -84,7 +84,7 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
 
     structs = {"h2f_matrix_desc": L.MatrixDesc, "h2f_build_desc": L.BuildDesc, "h2f_factor_info": L.FactorInfo,
-               "h2f_status": L.Status}
+               "h2f_status": L.Status, "h2f_comm": L.Comm}
     lines = ["#include <stddef.h>", "#include <stdio.h>", '#include "h2f.h"', "int main(void) {"]
     for cname, py in structs.items():
         lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
