@@ -7,9 +7,13 @@ reference) + refined_solve(h2, fac, b, steps=1), the pair the reference's
 harness times (harness.py:203-213).  `value` is measured with the operator
 and b already resident in HBM, with CUDA events on the library's stream;
 `e2e` goes through the public Python API with host buffers (operator upload,
-b H2D, x D2H inside the timed region).  Multi-GPU (torchrun): every rank
-factors its own replica (weak scaling, "replicas only" for now, see
-DESIGN.md), max over ranks.
+b H2D, x D2H inside the timed region).  Multi-GPU (torchrun, NCCL): the
+factorization is split by cluster-tree subtree over the ranks
+(h2f_factorize_sharded: per-batch all-to-all of Q~ and
+eliminator panels, reduced decisions, factor broadcast; bit-identical to
+the single-GPU factor), then every rank runs the refined solve on the
+replicated factor; strong scaling (the same N on every rank count), max
+over ranks.
 
 --impl reference times the CPU oracle (the reference algorithm restated and
 pinned bit-for-bit to it, oracle/h2_oracle.py) on this host: config 1 in
@@ -245,7 +249,7 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": "H2 factor+solve time (s)", "value": v, "unit": "s",
         "n_gpus": args.gpus, "steps": len(vals), "warmup": args.warmup, "higher_is_better": False,
-        "dtype": "f64", "data": "synthetic", "scaling": "weak",
+        "dtype": "f64", "data": "synthetic", "scaling": "strong",
         "config": {"workload": cfg["desc"], "n": cfg["n"], "problem": cfg["problem"], **cfg["over"]},
         "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "port", "sample": s["sample"],
                          "host": host_cpu(), "sample_seconds": samples,
@@ -312,11 +316,23 @@ def run_b200(args, cfg):
 
     import ctypes as C
 
+    comm = None
+    if world > 1:
+        from paper_2509_11152_b200.multigpu import TorchComm
+
+        comm = TorchComm()
+
     def step():
         fh = C.c_void_p()
         st = L.Status()
-        L.check(lib.h2f_factorize(dm.handle, float(prm["eps_lu"]), -1.0, L.ptr(v0), C.byref(fh),
-                                  C.byref(st)), "factorize")
+        if comm is None:
+            L.check(lib.h2f_factorize(dm.handle, float(prm["eps_lu"]), -1.0, L.ptr(v0), C.byref(fh),
+                                      C.byref(st)), "factorize")
+        else:
+            code = lib.h2f_factorize_sharded(dm.handle, float(prm["eps_lu"]), -1.0, L.ptr(v0),
+                                             C.byref(comm.struct), C.byref(fh), C.byref(st))
+            comm.reraise()
+            L.check(code, "factorize_sharded")
         L.check(lib.h2f_refined_solve_dev(dm.handle, fh, C.c_void_p(b_dev.data_ptr()),
                                           C.c_void_p(x_dev.data_ptr()), 1), "refined_solve")
         return fh
@@ -357,6 +373,11 @@ def run_b200(args, cfg):
     fh = step()
     prof = L.profile_get()
     L.profile_enable(False)
+    shard = None
+    if comm is not None:
+        from paper_2509_11152_b200.multigpu import shard_stats
+
+        shard = shard_stats()
     torch.cuda.synchronize()
     lib.h2f_factor_destroy(fh)
     prof_steps = 1
@@ -373,7 +394,12 @@ def run_b200(args, cfg):
             object.__setattr__(h2, "_h2f_device", None)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        fac = H.factorize(h2, prm["eps_lu"])
+        if comm is None:
+            fac = H.factorize(h2, prm["eps_lu"])
+        else:
+            from paper_2509_11152_b200.multigpu import factorize_sharded
+
+            fac = factorize_sharded(h2, prm["eps_lu"])
         xh = H.refined_solve(h2, fac, b_host, steps=1)
         e2e_times.append(time.perf_counter() - t0)
         h2d = h2_bytes(h2) + b_host.nbytes
@@ -387,11 +413,11 @@ def run_b200(args, cfg):
     line = {
         "metric": "H2 factor+solve time (s)", "value": t_step, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": cfg["desc"], "n": n, "problem": cfg["problem"], **cfg["over"],
                    "eps_lu": prm["eps_lu"], "eps": prm["eps"], "leaf": prm["m"],
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": f"subtree shards x{world}" if world > 1 else "single",
                    "l2": "flushed between timed steps (256 MB write)"},
         "e2e": {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(round(launches)),
@@ -407,6 +433,7 @@ def run_b200(args, cfg):
         "input_build_s": t_build,
         "device_construction": dcons,
         "phase_seconds_last": None,
+        "shard_stats_rank0": shard,
         "kernels": {k: {"ms": v["seconds"] * 1e3 / prof_steps, "launches": v["launches"] // prof_steps,
                         "gflop": v["flops"] / 1e9 / prof_steps, "gbytes": v["bytes"] / 1e9 / prof_steps}
                     for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["seconds"])},

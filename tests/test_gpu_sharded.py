@@ -55,3 +55,49 @@ def test_sharded_factor_is_the_single_gpu_factor(tmp_path, name, n, over, world)
         here += st["clusters_here"]
     # every cluster is eliminated by exactly one rank
     assert here == r["ranks"][0]["stats"]["clusters_total"]
+
+
+def test_torchcomm_device_collectives_nccl_single_rank():
+    """The NCCL side of TorchComm (what bench.py --gpus N uses over NVLink):
+    zero-copy views of library-style device buffers through every callback,
+    at world size 1 on this one-GPU box; plus the degenerate sharded
+    factorization (world 1) equal to factorize()."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_11152_b200 as H
+    from paper_2509_11152_b200 import _lib as L
+    from paper_2509_11152_b200 import problem as P
+    from paper_2509_11152_b200.multigpu import TorchComm, factorize_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        comm = TorchComm()
+        assert comm.nccl and comm.world == 1
+        a = torch.arange(10, dtype=torch.float64, device="cuda")
+        assert comm.struct.allreduce_sum_dev(None, C.c_void_p(a.data_ptr()), 10) == 0
+        assert torch.equal(a.cpu(), torch.arange(10, dtype=torch.float64))
+        send = torch.arange(40, dtype=torch.uint8, device="cuda")
+        recv = torch.zeros(40, dtype=torch.uint8, device="cuda")
+        cnt = (C.c_int64 * 1)(40)
+        assert comm.struct.alltoallv_dev(None, C.c_void_p(send.data_ptr()), cnt, C.c_void_p(recv.data_ptr()),
+                                         cnt) == 0
+        assert torch.equal(recv, send)
+        assert comm.struct.broadcast_dev(None, C.c_void_p(recv.data_ptr()), 40, 0) == 0
+        assert torch.equal(recv, send)
+        v = np.array([1.0, -2.0])
+        assert comm.struct.allreduce_max(None, v.ctypes.data_as(L.f64p), 2) == 0
+        assert list(v) == [1.0, -2.0]
+        comm.reraise()
+        _, _, _, h2, prm = P.build_problem("cov2d", 4096)
+        f1 = factorize_sharded(h2, prm["eps_lu"])
+        f0 = H.factorize(h2, prm["eps_lu"])
+        assert [r.batches for r in f1.records] == [r.batches for r in f0.records]
+        assert np.array_equal(f1.top_lu, f0.top_lu)
+    finally:
+        dist.destroy_process_group()

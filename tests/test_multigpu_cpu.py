@@ -121,3 +121,85 @@ def test_broadcast_arrays_gloo_world2(tmp_path):
             assert str(z["meta"]) == '{"format": "x"}'
             assert z["piv"].dtype == np.int32 and np.array_equal(z["piv"], np.arange(9))
             assert z["empty"].shape == (0,) and np.array_equal(z["ids"], np.arange(4))
+
+
+# ---------------------------------------------------------------- subtree sharding
+# (h2f_factorize_sharded): the host-side pieces -- the owner
+# map and the host collectives of TorchComm -- on CPU with gloo.  The device
+# collectives and the sharded factorization itself: tests/test_gpu_sharded.py.
+
+def test_shard_owners_are_contiguous_subtrees():
+    import paper_2509_11152_b200 as H
+    from paper_2509_11152_b200.multigpu import shard_owners
+
+    for name, n, over in [("cov2d", 4096, {}), ("helmholtz3d", 16384, {"kappa": 0.0})]:
+        pts, _ = H.generate_uniform_grid(n, 2 if name == "cov2d" else 3)
+        tree = H.build_cluster_tree(pts, 64)
+        part = H.dual_tree_traversal(tree, 0.9 if name == "cov2d" else 0.7)
+        top = part.top_level
+        for world in [1, 2, 4, 8]:
+            own = shard_owners(tree, top, world)
+            lv = np.asarray(tree.level)
+            assert (own[lv < top] == -1).all() if world > 1 else (own == 0).all()
+            if world == 1:
+                continue
+            tops = np.flatnonzero(lv == top)
+            # contiguous, balanced runs of the top-level clusters
+            assert list(own[tops]) == sorted(own[tops])
+            assert np.bincount(own[tops], minlength=world).min() == len(tops) // world
+            # every deeper cluster follows its parent
+            deep = np.flatnonzero(lv > top)
+            assert (own[deep] == own[np.asarray(tree.parent)[deep]]).all()
+            # the leaves split evenly
+            leaves = np.flatnonzero(lv == tree.depth)
+            cnt = np.bincount(own[leaves], minlength=world)
+            assert cnt.max() - cnt.min() <= 1 + len(leaves) // len(tops)
+
+
+def test_shard_owners_rejects_too_many_ranks():
+    import paper_2509_11152_b200 as H
+    from paper_2509_11152_b200.multigpu import shard_owners
+
+    pts, _ = H.generate_uniform_grid(4096, 2)
+    tree = H.build_cluster_tree(pts, 64)
+    part = H.dual_tree_traversal(tree, 0.9)
+    ntop = int(np.count_nonzero(np.asarray(tree.level) == part.top_level))
+    with pytest.raises(ValueError, match="top level"):
+        shard_owners(tree, part.top_level, ntop + 1)
+    with pytest.raises(ValueError, match="compressed level"):
+        shard_owners(tree, None, 2)
+
+
+def _comm_worker(rank, world, port, out_dir):
+    import ctypes as C
+
+    import torch.distributed as dist
+
+    from paper_2509_11152_b200 import _lib as L
+    from paper_2509_11152_b200.multigpu import TorchComm
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = TorchComm()
+        assert (comm.rank, comm.world, comm.nccl) == (rank, world, False)
+        # the kept / pivot-status / fill-norm reduction: element-wise max,
+        # -1 where a rank did not compute the candidate
+        v = np.array([-1.0, 3.0 * rank, 0.5, -1.0 if rank else 7.25])
+        rc = comm.struct.allreduce_max(None, v.ctypes.data_as(L.f64p), len(v))
+        assert rc == 0
+        np.save(os.path.join(out_dir, f"max{rank}.npy"), v)
+        # a failing collective returns nonzero and re-raises after the call
+        rc = comm.struct.allreduce_max(None, C.cast(None, L.f64p), 3)
+        assert rc != 0
+        with pytest.raises(Exception):
+            comm.reraise()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_torchcomm_host_reduction_gloo(tmp_path):
+    port = _free_port()
+    mp.spawn(_comm_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        assert np.array_equal(np.load(tmp_path / f"max{r}.npy"), [-1.0, 3.0, 0.5, 7.25])
