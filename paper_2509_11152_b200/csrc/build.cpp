@@ -23,6 +23,7 @@
 // on both sides afterwards (C <- U_s^T C U_t).  The two differ by the
 // truncated part, O(eps) relative.
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -512,7 +513,8 @@ struct Builder {
             it.m = (r > 0 && W > 0) ? std::min(r, W) : 0;
             if (!it.m) continue;
             const int m = it.m;
-            it.Rm = R.alloc_n<double>(int64_t(m) * r);
+            // both QR paths write a full r x r R (rows >= m zero), also when W < r
+            it.Rm = R.alloc_n<double>(int64_t(r) * r);
             it.U = R.alloc_n<double>(int64_t(m) * r);
             it.sig = R.alloc_n<double>(m);
             if (r > 32) {

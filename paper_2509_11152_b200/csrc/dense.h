@@ -30,8 +30,9 @@ struct HhApply {
 };
 void hh_apply_q(const std::vector<HhJob>& jobs, const std::vector<HhApply>& xs, Region& scr);
 
-// R (min(n,wf) x n, row-major ld n) of the QR of Y^T for the QrTasks (Y is n x wf,
-// row-major; overwritten)
+// R of the QR of Y^T for the QrTasks (Y is n x wf, row-major; overwritten):
+// written as a full n x n row-major block, rows >= min(n, wf) zero -- callers
+// allocate n x n even when wf < n (as does the shared-memory TSQR)
 void qr_r_blocked(const std::vector<QrTask>& tasks, Region& scr);
 
 // Q~ = [complement | b_aug] for each task (factorization.py:88-99), blocked
