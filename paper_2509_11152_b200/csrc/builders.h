@@ -9,7 +9,19 @@
 #include "kernels.h"
 #include "runtime.h"
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
 namespace h2f {
+
+#ifdef _OPENMP
+inline int max_threads() { return omp_get_max_threads(); }
+inline int thread_id() { return omp_get_thread_num(); }
+#else
+inline int max_threads() { return 1; }
+inline int thread_id() { return 0; }
+#endif
 
 struct GemmBuild {
     std::vector<GemmTask> tasks;
@@ -82,6 +94,87 @@ struct GemmBuild {
         tile_start.push_back(tile_start.back() + nt);
         tile_cost.push_back(chunks + (mode == GEMM_ADD ? 2 : 1));
         return t.norm_base;
+    }
+    // n external-contribution tasks at once (all with M, N > 0), e.g. the
+    // ~1e5 Schur targets / fill candidates of a leaf-level batch: get(i)
+    // describes task i (called in parallel); tile offsets, norm bases and the
+    // work sums are formed serially in task order, exactly as n add_ext calls
+    // would, and the task records are written in parallel.
+    struct BulkItem {
+        double* C;
+        int64_t ldc;
+        int M, N;
+        int64_t begin, nc;
+        double ksum;
+        int64_t chunks;
+    };
+    template <class F> void add_ext_bulk(int64_t n, int mode, F&& get, int64_t* norm_base_out) {
+        if (n <= 0) return;
+        const size_t t0 = tasks.size();
+        std::vector<BulkItem> it(static_cast<size_t>(n));
+        tasks.resize(t0 + size_t(n));
+        tile_start.resize(t0 + 1 + size_t(n));
+        tile_cost.resize(t0 + size_t(n));
+        // two-pass parallel scan over contiguous thread ranges: items and
+        // per-range sums, range offsets, then tile offsets / norm bases /
+        // task records (the work sums feed the profiler and the kernel-variant
+        // choice only, whose variants are bit-identical)
+        const int nth = n > 4096 ? max_threads() : 1;
+        std::vector<int64_t> tsum(size_t(nth) + 1, 0);
+        std::vector<double> fsum(size_t(nth), 0.0), bsum(size_t(nth), 0.0);
+        bool bad = false;
+        const int64_t ts0 = tile_start[t0], nb0 = norm_tiles;
+#pragma omp parallel num_threads(nth) if (nth > 1) reduction(|| : bad)
+        {
+            const int tid = thread_id();
+            const int64_t lo = n * tid / nth, hi = n * (tid + 1) / nth;
+            int64_t acc = 0;
+            double f = 0, by = 0;
+            for (int64_t i = lo; i < hi; ++i) {
+                BulkItem& b = it[size_t(i)];
+                b = get(i);
+                if (b.M <= 0 || b.N <= 0) bad = true;
+                acc += tiles(b.M, b.N);
+                f += 2.0 * b.M * b.N * b.ksum;
+                by += 8.0 * b.ksum * (double(b.M) + b.N) +
+                      (mode == GEMM_ADD ? 16.0 * b.M * b.N : (mode == GEMM_STORE ? 8.0 * b.M * b.N : 0.0));
+            }
+            tsum[size_t(tid) + 1] = acc;
+            fsum[size_t(tid)] = f;
+            bsum[size_t(tid)] = by;
+#pragma omp barrier
+#pragma omp single
+            for (int q = 0; q < nth; ++q) tsum[size_t(q) + 1] += tsum[size_t(q)];
+            int64_t run = tsum[size_t(tid)];
+            for (int64_t i = lo; i < hi; ++i) {
+                const BulkItem& b = it[size_t(i)];
+                const int64_t nt = tiles(b.M, b.N);
+                GemmTask t{};
+                t.C = b.C;
+                t.ldc = b.ldc;
+                t.M = b.M;
+                t.N = b.N;
+                t.mode = mode;
+                t.tiles_n = int(cdiv(b.N, GEMM_TILE));
+                t.contrib_begin = b.begin;
+                t.contrib_end = b.begin + b.nc;
+                t.norm_base = -1;
+                if (mode == GEMM_NORM) {
+                    t.norm_base = nb0 + run;
+                    norm_base_out[i] = t.norm_base;
+                }
+                run += nt;
+                tile_start[t0 + 1 + size_t(i)] = ts0 + run;
+                tasks[t0 + size_t(i)] = t;
+                tile_cost[t0 + size_t(i)] = b.chunks + (mode == GEMM_ADD ? 2 : 1);
+            }
+        }
+        if (bad) throw Error(H2F_E_INTERNAL, "assertion: empty bulk GEMM task");
+        for (int q = 0; q < nth; ++q) {
+            flops += fsum[size_t(q)];
+            bytes += bsum[size_t(q)];
+        }
+        if (mode == GEMM_NORM) norm_tiles += tsum[size_t(nth)];
     }
     int64_t add1(double* C, int64_t ldc, int M, int N, int mode, const GemmContrib& c) {
         return add(C, ldc, M, N, mode, &c, 1);

@@ -292,6 +292,7 @@ class Factorizer {
     std::vector<size_t> level_marks;
     std::vector<int> mark_node;  // node-indexed batch membership stamp
     std::vector<int> node_bi;    // node -> position in the current batch (valid where stamped)
+    std::vector<int64_t> made_mark;  // node -> batch in which a fill key (node, .) was created
     int stamp = 0;
     bool level_prof = false;
     FILE* aug_log = nullptr;  // H2F_AUG_LOG=path: per-cluster augmentation shapes (development aid)
@@ -299,7 +300,8 @@ class Factorizer {
     std::chrono::steady_clock::time_point level_t0;
     // host wall time per section of process_batch (H2F_LEVEL_PROF); the two
     // sync entries are the host blocked on the device
-    enum { HT_PICK, HT_AUG, HT_SYNC1, HT_AUG2, HT_PROJ, HT_ELIM, HT_S1, HT_S2, HT_S3, HT_SCHUR, HT_SYNC2, HT_CREATE, HT_TRANS, HT_N };
+    enum { HT_PICK, HT_AUG, HT_SYNC1, HT_AUG2, HT_PROJ, HT_ELIM, HT_S1, HT_S2A, HT_S2, HT_S3, HT_SCHUR, HT_SYNC2, HT_CREATE, HT_TRANS, HT_N };
+    int64_t n_upd = 0, n_cand = 0, n_batches_lvl = 0;
     double ht[HT_N] = {};
     std::chrono::steady_clock::time_point ht_last = std::chrono::steady_clock::now();
     void tick(int i) {
@@ -988,6 +990,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         bool here;  // this rank holds the would-be block and computes its norm
     };
     std::vector<Cand> cands;
+    std::vector<size_t> lc;  // candidates whose norm is computed here (sharded: held here)
     int64_t npairs = 0;  // updates of the batch
     for (auto& e : el) npairs += int64_t(e.np) * (e.np + 1) / 2;
     // Target resolution in two passes: (1) per eliminated cluster, in
@@ -1063,22 +1066,45 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     // its own targets, so the contributions of every target stay in
     // reference order (the only order the numerics depend on); the task order
     // is bucket-major, deterministic for a given arena layout.
-    for (size_t ei = 0; ei < el.size(); ++ei) {  // fill candidates, serial, reference order
-        const Elim& e = el[ei];
-        for (int64_t k = boff[ei][NBK]; k < boff[ei][NBK + 1]; ++k) {
-            const Upd& u = upd[ei][k];
-            if (u.M <= 0 || u.N <= 0) continue;
-            Cand cd;
-            cd.key = mkkey(e.ids[u.i], e.ids[u.j]);
-            cd.creator = e.c;
-            cd.M = u.M;
-            cd.N = u.N;
-            cd.g = contrib(e.G + e.offs[u.i], e.W, 1, e.MW + e.offs[u.j], e.W, 0, e.r);
-            cd.base = 0;
-            cd.ntiles = GemmBuild::tiles(cd.M, cd.N);
-            cd.here = holds(cd.key);
-            cands.push_back(cd);
+    {
+        // fill candidates in reference order (cluster, then pair order),
+        // built per eliminated cluster in parallel at precomputed offsets
+        std::vector<int64_t> cstart(el.size() + 1, 0);
+#pragma omp parallel for schedule(dynamic, 4) if (npairs > 20000)
+        for (size_t ei = 0; ei < el.size(); ++ei) {
+            int64_t n = 0;
+            for (int64_t k = boff[ei][NBK]; k < boff[ei][NBK + 1]; ++k) {
+                const Upd& u = upd[ei][k];
+                n += (u.M > 0 && u.N > 0);
+            }
+            cstart[ei + 1] = n;
         }
+        for (size_t ei = 0; ei < el.size(); ++ei) cstart[ei + 1] += cstart[ei];
+        cands.resize(size_t(cstart.back()));
+#pragma omp parallel for schedule(dynamic, 4) if (npairs > 20000)
+        for (size_t ei = 0; ei < el.size(); ++ei) {
+            const Elim& e = el[ei];
+            int64_t q = cstart[ei];
+            for (int64_t k = boff[ei][NBK]; k < boff[ei][NBK + 1]; ++k) {
+                const Upd& u = upd[ei][k];
+                if (u.M <= 0 || u.N <= 0) continue;
+                Cand& cd = cands[size_t(q++)];
+                cd.key = mkkey(e.ids[u.i], e.ids[u.j]);
+                cd.creator = e.c;
+                cd.M = u.M;
+                cd.N = u.N;
+                cd.g = contrib(e.G + e.offs[u.i], e.W, 1, e.MW + e.offs[u.j], e.W, 0, e.r);
+                cd.base = 0;
+                cd.ntiles = GemmBuild::tiles(cd.M, cd.N);
+                cd.here = holds(cd.key);
+            }
+        }
+    }
+    tick(HT_S2A);
+    if (level_prof) {
+        n_batches_lvl += 1;
+        n_cand += int64_t(cands.size());
+        for (auto& u : upd) n_upd += int64_t(u.size());
     }
     struct Bucket {
         std::vector<THdr> th;
@@ -1138,10 +1164,18 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         const size_t ncon = size_t(ntc) + cands.size();
         GemmContrib* hc = nullptr;
         sch.ext = X.up.reserve<GemmContrib>(std::max<size_t>(ncon, 1), &hc);
+        // contribution offsets per slot: a bucket's slots are contiguous and
+        // its contributions start at con0
         std::vector<int64_t> tstart(size_t(nslots) + 1, 0);
-        for (auto& B : bk)
-            for (size_t t = 0; t < B.th.size(); ++t) tstart[B.slot0 + t + 1] = B.th[t].count;
-        for (int64_t t = 0; t < nslots; ++t) tstart[t + 1] += tstart[t];
+        tstart[size_t(nslots)] = ntc;
+#pragma omp parallel for schedule(static, 1) if (NBK > 1)
+        for (int b = 0; b < NBK; ++b) {
+            int64_t run = bk[b].con0;
+            for (size_t t = 0; t < bk[b].th.size(); ++t) {
+                tstart[size_t(bk[b].slot0) + t] = run;
+                run += bk[b].th[t].count;
+            }
+        }
 #pragma omp parallel for schedule(static, 1) if (NBK > 1)
         for (int b = 0; b < NBK; ++b) {
             Bucket& B = bk[b];
@@ -1153,34 +1187,50 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 else g = contrib(E.MW + E.offs[-tc.j - 1], E.W, 1, E.G + E.offs[0], E.W, 0, E.r);
             }
         }
+        // target tasks (slot order = bucket-major), then the candidates'
+        // norm tasks (reference order), built in bulk
         sch.tasks.reserve(size_t(nslots) + cands.size());
+        std::vector<int64_t> slot0(NBK + 1, 0);
+        for (int b = 0; b < NBK; ++b) slot0[b + 1] = slot0[b] + int64_t(bk[b].th.size());
         for (auto& B : bk)
-            for (size_t t = 0; t < B.th.size(); ++t) {
-                const THdr& h = B.th[t];
-                schur_bytes += 16.0 * h.M * double(h.N);
-                sch.add_ext(h.C, h.ldc, h.M, h.N, GEMM_ADD, tstart[B.slot0 + t], h.count, B.ksum[t], B.chunks[t]);
-            }
-        int64_t pos = ntc;
-        for (auto& cd : cands) {
-            if (!cd.here) continue;
-            hc[pos] = cd.g;
-            cd.base = sch.add_ext(nullptr, 0, cd.M, cd.N, GEMM_NORM, pos, 1, cd.g.K, cdiv(cd.g.K, GEMM_BK));
-            ++pos;
+            for (size_t t = 0; t < B.th.size(); ++t) schur_bytes += 16.0 * B.th[t].M * double(B.th[t].N);
+        sch.add_ext_bulk(nslots, GEMM_ADD, [&](int64_t sl) {
+            const int b = int(std::upper_bound(slot0.begin(), slot0.end(), sl) - slot0.begin()) - 1;
+            const Bucket& B = bk[b];
+            const size_t t = size_t(sl - slot0[b]);
+            const THdr& h = B.th[t];
+            return GemmBuild::BulkItem{h.C, h.ldc, h.M, h.N, tstart[size_t(sl)], h.count, B.ksum[t], B.chunks[t]};
+        }, nullptr);
+        if (sharded()) {
+            for (size_t i = 0; i < cands.size(); ++i)
+                if (cands[i].here) lc.push_back(i);
+        } else {
+            lc.resize(cands.size());
+            std::iota(lc.begin(), lc.end(), size_t(0));
         }
+        std::vector<int64_t> nbase(lc.size());
+        sch.add_ext_bulk(int64_t(lc.size()), GEMM_NORM, [&](int64_t q) {
+            const Cand& cd = cands[lc[size_t(q)]];
+            hc[ntc + q] = cd.g;
+            return GemmBuild::BulkItem{nullptr, 0, cd.M, cd.N, ntc + q, 1, double(cd.g.K), cdiv(cd.g.K, GEMM_BK)};
+        }, nbase.data());
+#pragma omp parallel for schedule(static) if (lc.size() > 4096)
+        for (size_t q = 0; q < lc.size(); ++q) cands[lc[q]].base = nbase[q];
     }
     tick(HT_S3);
-    std::vector<size_t> lc;  // candidates whose norm is computed here
-    for (size_t i = 0; i < cands.size(); ++i)
-        if (cands[i].here) lc.push_back(i);
     double* norms_d = sch.norm_tiles ? scr.alloc_n<double>(sch.norm_tiles) : nullptr;
     double* cand_ss_d = lc.empty() ? nullptr : scr.alloc_n<double>(lc.size());
     sch.launch(K_GEMM_SCHUR, norms_d, schur_bytes);
     stats_tiles(sch);
     if (!lc.empty()) {
+        // the candidates are the launch's only NORM tasks, their tiles
+        // contiguous in candidate order: segment k = [base_k, base_k+1)
         std::vector<int64_t> seg(lc.size() + 1, 0);
-        for (size_t k = 0; k < lc.size(); ++k) seg[k + 1] = cands[lc[k]].base + cands[lc[k]].ntiles;
-        for (size_t k = 0; k < lc.size(); ++k)
-            if (cands[lc[k]].base != seg[k]) throw Error(H2F_E_INTERNAL, "assertion: norm segments");
+#pragma omp parallel for schedule(static) if (lc.size() > 4096)
+        for (size_t k = 0; k < lc.size(); ++k) seg[k] = cands[lc[k]].base;
+        seg[lc.size()] = sch.norm_tiles;
+        if (seg[0] != 0 || cands[lc.back()].base + cands[lc.back()].ntiles != sch.norm_tiles)
+            throw Error(H2F_E_INTERNAL, "assertion: norm segments");
         ProfScope ps(K_REDUCE, 0.0, 8.0 * double(sch.norm_tiles));
         launch_sumsq_reduce(norms_d, upload(seg), int32_t(lc.size()), cand_ss_d, st);
     }
@@ -1229,12 +1279,17 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             std::vector<GemmContrib> cs;
         };
         std::vector<Target> news;
+        // made_mark[a] == this batch: some key (a, .) was created in it (a
+        // cheap filter in front of the hash lookup)
+        const int64_t mstamp = batch_counter;
         for (size_t i = 0; i < cands.size(); ++i) {
             const Cand& cd = cands[i];
-            auto it = made.find(cd.key);
-            if (it != made.end()) {
-                if (it->second >= 0) news[it->second].cs.push_back(cd.g);
-                continue;
+            if (made_mark[key_a(cd.key)] == mstamp) {
+                auto it = made.find(cd.key);
+                if (it != made.end()) {
+                    if (it->second >= 0) news[it->second].cs.push_back(cd.g);
+                    continue;
+                }
             }
             if (cand_ss[i] < 0) throw Error(H2F_E_INTERNAL, "assertion: fill candidate norm computed nowhere");
             bool create_it = std::sqrt(cand_ss[i]) > drop;
@@ -1252,6 +1307,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 create_it = want;
             }
             if (create_it) {
+                made_mark[key_a(cd.key)] = mstamp;
                 L.fill_created.back().push_back(cd.key);
                 if (!cd.here) {  // another rank's block: structure only
                     L.F[cd.key] = View{nullptr, cd.N, cd.M, cd.N};
@@ -1509,13 +1565,15 @@ void Factorizer::dump_level_profile(int level) {
         if (d > 1e-4) std::fprintf(stderr, " %s=%.4f", kernel_name(k), d);
     }
     std::fprintf(stderr, " | kernels %.4f\n", dev);
-    static const char* names[HT_N] = {"pick", "aug", "sync1", "aug2", "proj", "elim", "s.resolve", "s.slots", "s.fill", "s.launch", "sync2", "create", "trans"};
+    static const char* names[HT_N] = {"pick", "aug", "sync1", "aug2", "proj", "elim", "s.resolve", "s.cands", "s.slots", "s.fill", "s.launch", "sync2", "create", "trans"};
     std::fprintf(stderr, "[level %d host]", level);
     for (int i = 0; i < HT_N; ++i) {
         std::fprintf(stderr, " %s=%.4f", names[i], ht[i]);
         ht[i] = 0;
     }
-    std::fprintf(stderr, "\n");
+    std::fprintf(stderr, " | updates %lld candidates %lld batches %lld\n", (long long)n_upd, (long long)n_cand,
+                 (long long)n_batches_lvl);
+    n_upd = n_cand = n_batches_lvl = 0;
 }
 
 
@@ -1727,6 +1785,7 @@ void Factorizer::run(double norm_estimate, const double* v0) {
     }
     mark_node.assign(M.nnodes, 0);
     node_bi.assign(M.nnodes, -1);
+    made_mark.assign(M.nnodes, -1);
     if (const char* p = std::getenv("H2F_AUG_LOG")) aug_log = std::fopen(p, "a");
     clock.mark(PH_NORM);
     if (norm_estimate < 0) {

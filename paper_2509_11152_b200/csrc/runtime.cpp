@@ -129,7 +129,18 @@ void Region::reset() {
 void* Uploader::put_bytes(const void* src, size_t bytes) {
     void* host = nullptr;
     void* d = reserve_bytes(bytes, &host);
-    if (bytes) std::memcpy(host, src, bytes);
+    if (bytes >= (size_t(2) << 20)) {
+        // large task arrays (a leaf-level Schur launch carries ~1e5 tasks):
+        // the staging copy into pinned memory in parallel slices
+        const int64_t nsl = int64_t(std::min<size_t>(16, bytes >> 19));
+#pragma omp parallel for schedule(static)
+        for (int64_t q = 0; q < nsl; ++q) {
+            const size_t lo = bytes * size_t(q) / size_t(nsl), hi = bytes * size_t(q + 1) / size_t(nsl);
+            std::memcpy(static_cast<char*>(host) + lo, static_cast<const char*>(src) + lo, hi - lo);
+        }
+    } else if (bytes) {
+        std::memcpy(host, src, bytes);
+    }
     return d;
 }
 
