@@ -8,12 +8,18 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
 
 #include "builders.h"
 
 namespace h2f {
 
 namespace {
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
 
 int sm_count() {
     static int sms = 0;
@@ -86,6 +92,83 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
             all.push_back({int(i), j0, std::min(HH_NB, J.nfac - j0), J.L - j0, 0, 0});
         }
         if (all.empty()) break;
+        GemmBuild gk, gu;
+        std::vector<HhTmulTask> tm;
+        int max_trail = 0;
+        // trailing update of the panel's job: columns [j0 + nbp, ntot), rows [j0, L)
+        auto add_trailing = [&](const PanelPlan& pp, const HhPanelTask& k) {
+            HhJob& J = jobs[pp.job];
+            // trailing update of columns [j0 + nbp, ntot), rows [j0, L)
+            const int ntrail = J.ntot - (pp.j0 + pp.nbp);
+            if (ntrail <= 0) return;
+            const int L = pp.Lp, nch = int(cdiv(L, KCH));
+            double* At = J.M + int64_t(pp.j0 + pp.nbp) * J.ldm + pp.j0;  // ntrail x L, ld ldm
+            double* P = scr.alloc_n<double>(int64_t(nch) * pp.nbp * ntrail);
+            double* W2 = scr.alloc_n<double>(int64_t(pp.nbp) * ntrail);
+            for (int c = 0; c < nch; ++c) {
+                const int kk = std::min(KCH, L - c * KCH);
+                gk.add1(P + int64_t(c) * pp.nbp * ntrail, ntrail, pp.nbp, ntrail, GEMM_STORE,
+                        contrib(k.Vt + int64_t(c) * KCH, L, 0, At + int64_t(c) * KCH, J.ldm, 1, kk));
+            }
+            tm.push_back(HhTmulTask{P, k.T, W2, nch, pp.nbp, ntrail, 1});
+            max_trail = std::max(max_trail, ntrail);
+            gu.add1(At, J.ldm, ntrail, L, GEMM_ADD, contrib(W2, ntrail, 1, k.Vt, L, 0, pp.nbp, -1.0));
+
+        };
+        // H2F_HH_CLUSTER=1: panels of HH_CHUNK_MAX < Lp <= 16 * HH_CLUSTER_CHUNK
+        // rows as one thread-block cluster each (DSMEM exchange, cluster
+        // barrier).  Measured on config 2: no gain over the
+        // cooperative panel -- the per-column time is the slice's own
+        // dot/update/syncthreads chain, not the inter-CTA barrier -- so the
+        // cooperative panel stays the default.
+        static const bool no_cluster = env_int("H2F_HH_CLUSTER", 0) == 0;
+        {
+            std::vector<PanelPlan> rest;
+            std::map<int, std::vector<HhPanelTask>> by_cl;
+            std::map<int, int> cl_chunk;
+            for (auto& pp : all) {
+                if (no_cluster || pp.Lp <= HH_CHUNK_MAX || pp.Lp > 16 * HH_CLUSTER_CHUNK) {
+                    rest.push_back(pp);
+                    continue;
+                }
+                HhJob& J = jobs[pp.job];
+                if (!J.M) {  // plan-only (sharded): nothing to launch
+                    J.Vt.push_back(nullptr);
+                    J.T.push_back(nullptr);
+                    continue;
+                }
+                // cluster size: ~rows_per_cta rows per CTA (the per-column
+                // dot products and updates of a slice are the work between
+                // two cluster barriers), 2..16 CTAs
+                static const int rows_per_cta = env_int("H2F_HH_CLUSTER_ROWS", 256);
+                int cl = 2;
+                while (cl < 16 && int64_t(cl) * rows_per_cta < pp.Lp) cl *= 2;
+                int ch = int(cdiv(pp.Lp, cl));
+                ch = std::max(HH_NB, (ch + 3) & ~3);
+                HhPanelTask k{};
+                k.M = J.M;
+                k.ldm = J.ldm;
+                k.Vt = keep ? scr.alloc_n<double>(int64_t(HH_NB) * pp.Lp) : vbuf[pp.job];
+                k.T = scr.alloc_n<double>(HH_NB * HH_NB);
+                k.L = J.L;
+                k.j0 = pp.j0;
+                k.nbp = pp.nbp;
+                k.chunk = ch;
+                k.ncta = cl;
+                by_cl[cl].push_back(k);
+                cl_chunk[cl] = std::max(cl_chunk[cl], ch);
+                J.Vt.push_back(k.Vt);
+                J.T.push_back(k.T);
+                add_trailing(pp, k);
+            }
+            for (auto& kv : by_cl) {
+                cudaError_t e = launch_hh_panel_cluster(upload(kv.second), int32_t(kv.second.size()), kv.first,
+                                                        cl_chunk[kv.first], st);
+                if (e != cudaSuccess)
+                    throw Error(H2F_E_CUDA, std::string("cluster Householder panel launch: ") + cudaGetErrorString(e));
+            }
+            all.swap(rest);
+        }
         // waves of co-resident CTA groups
         std::vector<std::vector<PanelPlan>> waves(1);
         int used = 0;
@@ -99,9 +182,6 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
             waves.back().push_back(pp);
             used += need;
         }
-        GemmBuild gk, gu;
-        std::vector<HhTmulTask> tm;
-        int max_trail = 0;
         for (auto& w : waves) {
             size_wave(w, cap);
             std::vector<HhPanelTask> tasks;
@@ -139,21 +219,7 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
                 max_chunk = std::max(max_chunk, pp.chunk);
                 J.Vt.push_back(k.Vt);
                 J.T.push_back(k.T);
-                // trailing update of columns [j0 + nbp, ntot), rows [j0, L)
-                const int ntrail = J.ntot - (pp.j0 + pp.nbp);
-                if (ntrail <= 0) continue;
-                const int L = pp.Lp, nch = int(cdiv(L, KCH));
-                double* At = J.M + int64_t(pp.j0 + pp.nbp) * J.ldm + pp.j0;  // ntrail x L, ld ldm
-                double* P = scr.alloc_n<double>(int64_t(nch) * pp.nbp * ntrail);
-                double* W2 = scr.alloc_n<double>(int64_t(pp.nbp) * ntrail);
-                for (int c = 0; c < nch; ++c) {
-                    const int kk = std::min(KCH, L - c * KCH);
-                    gk.add1(P + int64_t(c) * pp.nbp * ntrail, ntrail, pp.nbp, ntrail, GEMM_STORE,
-                            contrib(k.Vt + int64_t(c) * KCH, L, 0, At + int64_t(c) * KCH, J.ldm, 1, kk));
-                }
-                tm.push_back(HhTmulTask{P, k.T, W2, nch, pp.nbp, ntrail, 1});
-                max_trail = std::max(max_trail, ntrail);
-                gu.add1(At, J.ldm, ntrail, L, GEMM_ADD, contrib(W2, ntrail, 1, k.Vt, L, 0, pp.nbp, -1.0));
+                add_trailing(pp, k);
             }
             if (tasks.empty()) continue;
             cudaError_t e = launch_hh_panel(upload(tasks), upload(owner), int32_t(owner.size()), max_chunk, st);

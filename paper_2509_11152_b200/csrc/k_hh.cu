@@ -10,8 +10,12 @@
 // partial sums are reduced in a fixed order, so the factor is bitwise
 // reproducible.  The trailing update A -= V T^T (V^T A) runs on the DMMA tile
 // GEMM (k_gemm.cu) between panels.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace h2f {
 
@@ -194,6 +198,142 @@ hh_panel_kernel(const HhPanelTask* __restrict__ tasks, const int32_t* __restrict
     }
 }
 
+
+// ---- thread-block-cluster panel ----------------------------------------------
+// The same panel factorization with the panel's CTAs forming ONE thread-block
+// cluster (2..16 CTAs, one per SM): the per-column exchange of partial sums
+// goes through distributed shared memory and the per-column barrier is the
+// cluster barrier (barrier.cluster), instead of global-memory partials and a
+// global atomic barrier -- the panel is latency bound (one exchange per
+// column), so this is where its time goes.  Rows per CTA <= HH_CLUSTER_CHUNK
+// (the slice stays in shared memory).  Clusters are independent, so a launch
+// needs no co-residency of all its tasks (no cooperative launch, no waves),
+// and a task's result depends only on its own (L, cluster size).
+__global__ void __launch_bounds__(HT, 1) hh_panel_cluster_kernel(const HhPanelTask* __restrict__ tasks) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int G = int(cluster.num_blocks()), g = int(cluster.block_rank());
+    const HhPanelTask T = tasks[blockIdx.x / G];
+    const int nbp = T.nbp, lds = T.chunk + 4;
+    const int64_t Lp = (int64_t)T.L - T.j0;
+    const int64_t r0 = (int64_t)g * T.chunk;
+    const int rows = (int)max((int64_t)0, min((int64_t)T.chunk, Lp - r0));
+    const int rows4 = (rows + 3) & ~3;
+    extern __shared__ double S[];  // column jj of the slice at S[jj * lds]
+    __shared__ double taus[HH_NB];
+    __shared__ double dsh[HH_NB + 2];
+    __shared__ double wsh[HH_NB];
+    __shared__ double Tm[HH_NB][HH_NB + 1];
+    // this CTA's partials (column parity double buffer): slot 0 = |x|^2,
+    // slot c = x . a_c; CTA 0 also publishes alpha (slot 0) and the head row
+    __shared__ double cpart[2][HH_NB + 2];
+    __shared__ double chead[2][HH_NB + 2];
+    __shared__ double cgram[HH_NB * HH_NB];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* M0 = T.M + (int64_t)T.j0 * T.ldm + T.j0 + r0;
+
+    for (int jj = 0; jj < HH_NB; ++jj)
+        for (int i = threadIdx.x; i < lds; i += HT)
+            S[jj * lds + i] = (jj < nbp && i < rows) ? M0[(int64_t)jj * T.ldm + i] : 0.0;
+    __syncthreads();
+
+    for (int jj = 0; jj < nbp; ++jj) {
+        const int par = jj & 1;
+        const int lo = (int)max((int64_t)0, (int64_t)(jj + 1) - r0);  // local rows strictly below the diagonal
+        for (int c = jj + warp; c < nbp; c += HW) {
+            double d = 0.0;
+            if (c == jj)
+                for (int i = lo + lane; i < rows; i += 32) d += S[jj * lds + i] * S[jj * lds + i];
+            else
+                for (int i = lo + lane; i < rows; i += 32) d += S[jj * lds + i] * S[c * lds + i];
+            d = warp_sum(d);
+            if (lane == 0) cpart[par][c == jj ? 0 : c] = d;
+        }
+        if (g == 0)
+            for (int c = jj + threadIdx.x; c < nbp; c += HT) chead[par][c == jj ? 0 : c] = S[c * lds + jj];
+        cluster.sync();
+        // fixed-order sums over the cluster's CTAs (identical in every CTA)
+        for (int c = jj + warp; c < nbp; c += HW) {
+            double v = 0.0;
+            for (int q = lane; q < G; q += 32) v += cluster.map_shared_rank(&cpart[par][0], q)[c == jj ? 0 : c];
+            v = warp_sum(v);
+            if (lane == 0) dsh[c] = v;
+        }
+        const double* head = cluster.map_shared_rank(&chead[par][0], 0);
+        if (threadIdx.x == 0) dsh[HH_NB] = head[0];  // alpha
+        __syncthreads();
+        double beta, tau, scal;
+        hh_reflector(dsh[HH_NB], dsh[jj], beta, tau, scal);
+        if (tau != 0.0) {
+            for (int c = jj + 1 + threadIdx.x; c < nbp; c += HT) wsh[c] = tau * (head[c] + scal * dsh[c]);
+            __syncthreads();
+            const int w = nbp - jj - 1;
+            for (int e = threadIdx.x; e < w * rows; e += HT) {
+                const int c = jj + 1 + e / rows, i = e % rows;
+                if (i >= lo) S[c * lds + i] -= wsh[c] * (scal * S[jj * lds + i]);
+            }
+            if (g == 0)
+                for (int c = jj + 1 + threadIdx.x; c < nbp; c += HT) S[c * lds + jj] -= wsh[c];
+            __syncthreads();
+            for (int i = lo + threadIdx.x; i < rows; i += HT) S[jj * lds + i] *= scal;
+        }
+        if (threadIdx.x == 0) {
+            taus[jj] = tau;
+            if (g == 0) S[jj * lds + jj] = beta;
+        }
+        __syncthreads();
+    }
+
+    // write back (R on/above the diagonal, reflectors below) and the explicit
+    // unit-lower V^T (HH_NB x Lp); S becomes the explicit V for the Gram
+    for (int jj = 0; jj < nbp; ++jj)
+        for (int i = threadIdx.x; i < rows; i += HT) {
+            const double x = S[jj * lds + i];
+            M0[(int64_t)jj * T.ldm + i] = x;
+            const int64_t gi = r0 + i;
+            const double v = gi < jj ? 0.0 : (gi == jj ? 1.0 : x);
+            T.Vt[(int64_t)jj * Lp + gi] = v;
+            S[jj * lds + i] = v;
+        }
+    __syncthreads();
+    {
+        const int gq = lane >> 2, t = lane & 3;
+        for (int tile = warp; tile < 16; tile += HW) {
+            const int ti = tile >> 2, tj = tile & 3;
+            double c0 = 0.0, c1 = 0.0;
+            const double* A = S + (ti * 8 + gq) * lds;
+            const double* B = S + (tj * 8 + gq) * lds;
+            for (int k0 = 0; k0 < rows4; k0 += 4) dmma_8x8x4(c0, c1, A[k0 + t], B[k0 + t]);
+            cgram[(ti * 8 + gq) * HH_NB + tj * 8 + 2 * t] = c0;
+            cgram[(ti * 8 + gq) * HH_NB + tj * 8 + 2 * t + 1] = c1;
+        }
+    }
+    cluster.sync();
+    if (g == 0) {
+        double* Gm = S;  // HH_NB x HH_NB, reuses the slice buffer
+        for (int e = threadIdx.x; e < HH_NB * HH_NB; e += HT) {
+            const int a = e / HH_NB, b = e % HH_NB;
+            double v = 0.0;
+            if (a < b && b < nbp)
+                for (int q = 0; q < G; ++q) v += cluster.map_shared_rank(cgram, q)[e];
+            Gm[e] = v;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            for (int j = 0; j < HH_NB; ++j) {
+                const double tj = j < nbp ? taus[j] : 0.0;
+                double acc = 0.0;
+                if (lane < j)
+                    for (int k = lane; k < j; ++k) acc += Tm[lane][k] * (-tj * Gm[k * HH_NB + j]);
+                __syncwarp();
+                Tm[lane][j] = lane < j ? acc : (lane == j ? tj : 0.0);
+                __syncwarp();
+            }
+            for (int j = 0; j < HH_NB; ++j) T.T[lane * HH_NB + j] = Tm[lane][j];
+        }
+    }
+    cluster.sync();  // the other CTAs' shared memory stays live until CTA 0 has read it
+}
+
 // out[a][c] = sum_b op(T)[a][b] * (sum_ch P[ch][b][c]),  op(T) = T^T (trans) or T
 // 32 columns per CTA, 8 row-threads: the split-K partial sums of the 32 x 32
 // block S are formed with independent loads (4 rows per thread), then T (or
@@ -267,6 +407,29 @@ cudaError_t launch_hh_panel(const HhPanelTask* d_tasks, const int32_t* d_cta_tas
                                                 smem, st);
     count_launch();
     return e;  // never falls back to a plain launch: the group barriers need co-residency
+}
+
+cudaError_t launch_hh_panel_cluster(const HhPanelTask* d_tasks, int32_t ntasks, int32_t cluster, int32_t chunk,
+                                    cudaStream_t st) {
+    if (ntasks <= 0) return cudaSuccess;
+    const size_t smem = hh_panel_smem(chunk);
+    cudaFuncSetAttribute(hh_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(hh_panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(ntasks) * unsigned(cluster));
+    cfg.blockDim = dim3(HT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(cluster);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, hh_panel_cluster_kernel, d_tasks);
+    count_launch();
+    return e;
 }
 
 void launch_hh_tmul(const HhTmulTask* d_tasks, int32_t ntasks, int32_t max_cols, cudaStream_t st) {

@@ -289,6 +289,12 @@ void launch_sumsq_reduce(const double* d_parts, const int64_t* d_seg, int32_t ns
 
 size_t hh_panel_smem(int chunk);
 int hh_panel_capacity(int chunk);  // co-resident CTAs of the panel kernel at this chunk
+// panels of ntasks tasks, each one thread-block cluster of `cluster` CTAs
+// (2..16) holding `chunk` rows each (<= HH_CLUSTER_CHUNK); task.cta0/ncta,
+// part, gram and bar are unused
+constexpr int HH_CLUSTER_CHUNK = 800;
+cudaError_t launch_hh_panel_cluster(const HhPanelTask* d_tasks, int32_t ntasks, int32_t cluster, int32_t chunk,
+                                    cudaStream_t st);
 cudaError_t launch_hh_panel(const HhPanelTask* d_tasks, const int32_t* d_cta_task, int32_t total_ctas,
                             int32_t max_chunk, cudaStream_t st);
 void launch_hh_tmul(const HhTmulTask* d_tasks, int32_t ntasks, int32_t max_cols, cudaStream_t st);

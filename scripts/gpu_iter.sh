@@ -1,3 +1,2 @@
-# development iteration: parity + sharded tests, then the per-level profile of config 2
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_sharded.py -x -q > gpurun_out/it_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/it_pytest.log
-timeout 800 python scripts/level_profile.py > gpurun_out/it_lp.log 2>&1
+for r in 256 128; do echo "rows $r"; H2F_HH_CLUSTER_ROWS=$r timeout 800 python scripts/level_profile.py 2>&1 | grep -oE "factorize.*|qr_r_blocked=[0-9.]+" | tr '\n' ' '; echo; done
+echo "no cluster"; H2F_HH_NO_CLUSTER=1 timeout 800 python scripts/level_profile.py 2>&1 | grep -oE "factorize.*|qr_r_blocked=[0-9.]+" | tr '\n' ' '; echo
