@@ -170,6 +170,8 @@ struct ChunkMeta {
     int64_t local;  // tile index within the task
     int first;    // first chunk of its tile
     int kv;       // k slots of the chunk that carry data
+    int var;      // transA * 2 + transB of the chunk's contribution (the consumer
+                  // selects its fragment layout without a descriptor load)
 };
 
 // NS pipeline stages; PREC: the C tile of a GEMM_ADD task is prefetched into
@@ -214,6 +216,10 @@ __device__ __forceinline__ void gemm_tasks_body(const GemmTask* __restrict__ tas
     int p_pk = 0, p_m0 = 0, p_n0 = 0, p_M = 0, p_N = 0;
     int64_t p_local = 0;
     int p_first = 1;
+    // the producer's current contribution, kept in registers across its
+    // chunks (one descriptor load per contribution, not per chunk)
+    GemmContrib p_P{};
+    int64_t p_P_idx = -1;
     auto open_tile = [&]() {
         p_first = 1;
         while (p_ti + 1 < ntasks && p_tile >= tile_start[p_ti + 1]) ++p_ti;
@@ -244,7 +250,11 @@ __device__ __forceinline__ void gemm_tasks_body(const GemmTask* __restrict__ tas
             ++p_tile;
             if (p_tile < t_end) open_tile();
         } else {
-            const GemmContrib P = contribs[p_pc];
+            if (p_P_idx != p_pc) {
+                p_P = contribs[p_pc];
+                p_P_idx = p_pc;
+            }
+            const GemmContrib& P = p_P;
             double* As = gsm + (2 * stage) * STAGE_ELEMS;
             m.contrib = (int)p_pc;
             m.k0 = p_pk;
@@ -264,6 +274,7 @@ __device__ __forceinline__ void gemm_tasks_body(const GemmTask* __restrict__ tas
                 while (p_pc < p_end && contribs[p_pc].K <= 0) ++p_pc;
             }
             m.kv = total;
+            m.var = P.transA * 2 + P.transB;
             m.last = p_pc >= p_end;
             if (m.last) {
                 ++p_tile;
@@ -322,12 +333,11 @@ __device__ __forceinline__ void gemm_tasks_body(const GemmTask* __restrict__ tas
             }
         }
         if (m.contrib >= 0) {
-            const GemmContrib P = contribs[m.contrib];
             const double* As = gsm + (2 * cur) * STAGE_ELEMS;
             const double* Bs = As + STAGE_ELEMS;
             // k slots past the chunk's data hold zeros: skip them
             const int kv = m.kv;
-            switch (P.transA * 2 + P.transB) {
+            switch (m.var) {
             case 0: mma_chunk<false, false, NJ>(As, Bs, acc, wm, wn, g, t, kv); break;
             case 1: mma_chunk<false, true, NJ>(As, Bs, acc, wm, wn, g, t, kv); break;
             case 2: mma_chunk<true, false, NJ>(As, Bs, acc, wm, wn, g, t, kv); break;
