@@ -696,8 +696,17 @@ void launch_gemm_warp(const GemmTask* d_tasks, const GemmContrib* d_contribs, co
     if (ntiles <= 0) return;
     // 3 resident CTAs per SM (168 registers; measured: forcing 4 or 5 CTAs
     // costs spills and is 5-40 % slower on every kbench shape)
-    auto fn = role == 1 ? gemm_schur_warp_kernel<3> : gemm_warp_kernel<3>;
-    fn<<<grid_for(ntiles, 12), GEMM_THREADS, 0, st>>>(d_tasks, d_contribs, d_tile_start, ntasks, ntiles, d_norms);
+    // H2F_GEMM_WARP_MINB: CTAs per SM the register budget is sized for (3 default)
+    static const int minb = [] {
+        const char* e = std::getenv("H2F_GEMM_WARP_MINB");
+        const int v = e ? std::atoi(e) : 3;
+        return v == 4 || v == 6 ? v : 3;
+    }();
+    auto fn = role == 1 ? (minb == 4 ? gemm_schur_warp_kernel<4> : minb == 6 ? gemm_schur_warp_kernel<6>
+                                                                             : gemm_schur_warp_kernel<3>)
+                        : (minb == 4 ? gemm_warp_kernel<4> : minb == 6 ? gemm_warp_kernel<6> : gemm_warp_kernel<3>);
+    fn<<<grid_for(ntiles, 4 * minb), GEMM_THREADS, 0, st>>>(d_tasks, d_contribs, d_tile_start, ntasks, ntiles,
+                                                            d_norms);
     count_launch();
 }
 
