@@ -1,1 +1,6 @@
-for mb in 3 4 6; do echo "minb $mb"; H2F_GEMM_WARP_MINB=$mb timeout 800 python scripts/level_profile.py 2>&1 | grep -oE "factorize \(profiler off\).*|gemm_schur=[0-9.]+" | tr '\n' ' '; echo; done
+run() { echo "$1"; env $1 timeout 800 python scripts/level_profile.py 2>&1 | grep -oE "factorize \(profiler off\).*|gemm_schur=[0-9.]+" | tr '\n' ' '; echo; }
+run "H2F_X=0"
+run "H2F_GEMM_WARP_KMAX=32"
+run "H2F_GEMM_WARP_KMAX=56"
+run "H2F_GEMM_PREC_KMAX=64"
+run "H2F_GEMM_PREC_KMAX=160"
