@@ -270,17 +270,33 @@ gemv1_tasks_kernel(const GemvTask* __restrict__ tasks, const GemvContrib* __rest
             for (int i = threadIdx.x; i < T.rows; i += GV_T) {
                 const double* a = P.A + i;
                 double part = 0.0;
-#pragma unroll 4
+#pragma unroll 8
                 for (int j = 0; j < P.cols; ++j) part += __ldg(a + (int64_t)j * P.lda) * __ldg(P.x + j);
                 acc[i] += P.alpha * part;
             }
         } else {
-            for (int i = warp; i < T.rows; i += GV_T / 32) {
-                const double* ai = P.A + (int64_t)i * P.lda;
-                double part = 0.0;
-                for (int j = lane; j < P.cols; j += 32) part += __ldg(ai + j) * __ldg(P.x + j);
-                part = warp_sum(part);
-                if (lane == 0) acc[i] += P.alpha * part;
+            // GV_R rows per warp and step, their loads issued together (the
+            // per-row sums -- lane-strided, then the warp butterfly -- are
+            // the one-row form's, bit for bit; only more of them are in
+            // flight before the reductions)
+            constexpr int GV_R = 4;
+            for (int i0 = warp * GV_R; i0 < T.rows; i0 += GV_R * (GV_T / 32)) {
+                double part[GV_R];
+#pragma unroll
+                for (int r = 0; r < GV_R; ++r) part[r] = 0.0;
+                const double* a0 = P.A + (int64_t)i0 * P.lda;
+#pragma unroll 2
+                for (int j = lane; j < P.cols; j += 32) {
+                    const double xj = __ldg(P.x + j);
+#pragma unroll
+                    for (int r = 0; r < GV_R; ++r)
+                        if (i0 + r < T.rows) part[r] += __ldg(a0 + (int64_t)r * P.lda + j) * xj;
+                }
+#pragma unroll
+                for (int r = 0; r < GV_R; ++r) {
+                    const double v = warp_sum(part[r]);
+                    if (lane == 0 && i0 + r < T.rows) acc[i0 + r] += P.alpha * v;
+                }
             }
         }
         __syncthreads();
