@@ -31,12 +31,23 @@ __device__ void cta_trsv(const double* __restrict__ A, int r, double* v) {
         // rows of block b minus the already solved part
         const int c0 = LOWER ? 0 : r0 + rb, c1 = LOWER ? r0 : r;
         if (c1 > c0) {
-            for (int i = warp; i < rb; i += STW) {
-                const double* ai = A + (int64_t)(r0 + i) * r;
-                double acc = 0.0;
-                for (int j = c0 + lane; j < c1; j += 32) acc += ai[j] * v[j];
-                acc = warp_sum(acc);
-                if (lane == 0) v[r0 + i] -= acc;
+            // 4 rows per warp step, their loads in flight together (each
+            // row's lane-strided sum and butterfly are the one-row form's)
+            for (int i0 = warp * 4; i0 < rb; i0 += 4 * STW) {
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                const double* a0 = A + (int64_t)(r0 + i0) * r;
+#pragma unroll 2
+                for (int j = c0 + lane; j < c1; j += 32) {
+                    const double vj = v[j];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (i0 + q < rb) acc[q] += a0[(int64_t)q * r + j] * vj;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double t = warp_sum(acc[q]);
+                    if (lane == 0 && i0 + q < rb) v[r0 + i0 + q] -= t;
+                }
             }
             __syncthreads();
         }
@@ -175,12 +186,21 @@ solve_tasks_kernel(const SolveTask* __restrict__ tasks, const SolveCluster* __re
                 sv[j] = wk[(int64_t)j * nrhs + rh] + t;
             }
             __syncthreads();
-            for (int i = T.begin + warp; i < T.end; i += STW) {
-                const double* qi = C.q + (int64_t)i * s;
-                double acc = 0.0;
-                for (int j = lane; j < s; j += 32) acc += qi[j] * sv[j];
-                acc = warp_sum(acc);
-                if (lane == 0) yc[(int64_t)i * nrhs + rh] = acc;
+            for (int i0 = T.begin + 4 * warp; i0 < T.end; i0 += 4 * STW) {
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                const double* q0 = C.q + (int64_t)i0 * s;
+#pragma unroll 2
+                for (int j = lane; j < s; j += 32) {
+                    const double vj = sv[j];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (i0 + q < T.end) acc[q] += q0[(int64_t)q * s + j] * vj;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double t = warp_sum(acc[q]);
+                    if (lane == 0 && i0 + q < T.end) yc[(int64_t)(i0 + q) * nrhs + rh] = t;
+                }
             }
             __syncthreads();
         }
