@@ -83,8 +83,31 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
         jobs[i].T.clear();
         if (!keep && jobs[i].nfac > 0 && jobs[i].M) vbuf[i] = scr.alloc_n<double>(int64_t(HH_NB) * jobs[i].L);
     }
+    // block column pivoting: per job scratch, identity permutation
+    struct PivScratch { double* norms; int32_t* order; int32_t* perm_tmp; double* tmp; };
+    std::vector<PivScratch> piv(jobs.size(), PivScratch{nullptr, nullptr, nullptr, nullptr});
+    for (size_t i = 0; i < jobs.size(); ++i) {
+        HhJob& J = jobs[i];
+        if (!J.perm || !J.M) continue;
+        piv[i] = PivScratch{scr.alloc_n<double>(J.ntot), scr.alloc_n<int32_t>(J.ntot), scr.alloc_n<int32_t>(J.ntot),
+                            scr.alloc_n<double>(int64_t(J.ntot) * J.L)};
+        launch_iota(J.perm, J.ntot, st);
+    }
     for (int p = 0; p < maxp; ++p) {
         const int j0 = p * HH_NB;
+        {
+            std::vector<PivotTask> pt;
+            int max_cols = 0, max_l = 0;
+            for (size_t i = 0; i < jobs.size(); ++i) {
+                const HhJob& J = jobs[i];
+                if (!J.perm || !J.M || j0 >= J.nfac || J.ntot - j0 < 2) continue;
+                pt.push_back(PivotTask{J.M, J.ldm, J.L, j0, J.ntot, piv[i].norms, piv[i].order, J.perm, piv[i].perm_tmp,
+                                       piv[i].tmp});
+                max_cols = std::max(max_cols, J.ntot - j0);
+                max_l = std::max(max_l, J.L);
+            }
+            if (!pt.empty()) launch_pivot_panel(upload(pt), int32_t(pt.size()), max_cols, max_l, st);
+        }
         std::vector<PanelPlan> all;
         for (size_t i = 0; i < jobs.size(); ++i) {
             const HhJob& J = jobs[i];
@@ -278,12 +301,14 @@ void reorth_batched(const std::vector<ReorthTask>& tasks, Region& scr) {
     launch_normalize_rows(upload(rows), int32_t(rows.size()), ctx().stream);
 }
 
-void qr_r_blocked(const std::vector<QrTask>& tasks, Region& scr) {
+void qr_r_blocked(const std::vector<QrTask>& tasks, Region& scr, const std::vector<int32_t*>* perms) {
     std::vector<HhJob> jobs;
     std::vector<RExtractTask> ex;
     int maxn = 0;
-    for (auto& t : tasks) {
+    for (size_t ti = 0; ti < tasks.size(); ++ti) {
+        const QrTask& t = tasks[ti];
         HhJob J;
+        if (perms) J.perm = (*perms)[ti];
         J.M = t.Y;
         J.ldm = t.ldy;
         J.L = t.wf;

@@ -18,6 +18,10 @@ struct HhJob {
     int64_t ldm = 0;
     int L = 0, ntot = 0, nfac = 0;
     std::vector<double*> Vt, T;  // per panel (keep=true)
+    // non-null: block column pivoting -- before each panel the trailing
+    // columns are reordered by their remaining norms; perm[c] = original
+    // column now at position c (device, ntot entries)
+    int32_t* perm = nullptr;
 };
 
 void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep);
@@ -33,7 +37,7 @@ void hh_apply_q(const std::vector<HhJob>& jobs, const std::vector<HhApply>& xs, 
 // R of the QR of Y^T for the QrTasks (Y is n x wf, row-major; overwritten):
 // written as a full n x n row-major block, rows >= min(n, wf) zero -- callers
 // allocate n x n even when wf < n (as does the shared-memory TSQR)
-void qr_r_blocked(const std::vector<QrTask>& tasks, Region& scr);
+void qr_r_blocked(const std::vector<QrTask>& tasks, Region& scr, const std::vector<int32_t*>* perms = nullptr);
 
 // Q~ = [complement | b_aug] for each task (factorization.py:88-99), blocked
 void complement_blocked(const std::vector<ComplementTask>& tasks, Region& scr);

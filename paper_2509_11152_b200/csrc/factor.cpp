@@ -465,6 +465,13 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
         CopyBuild gather;
         GemmBuild gz;
         std::vector<QrTask> qr_small, qr_big, qr_seg;
+        // block column pivoting of the blocked QR where the multi-CTA Jacobi
+        // follows (fewer sweeps on a graded R): per qr_big task
+        // its permutation, and the un-permutation of the Jacobi's vectors
+        static const bool qr_pivot = env_int("H2F_QR_PIVOT", 1) != 0;
+        std::vector<int32_t*> qr_big_perm;
+        std::vector<UnpermTask> unperm;
+        int max_unperm = 0;
         std::vector<SvdTask> svd_small, svd_big;
         int max_n_small = 1;
         // the Jacobi writes every singular vector (sorted); under a structure
@@ -507,7 +514,10 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 // (plans identical on every rank), nothing runs here
                 Q[bi] = nullptr;
                 if (A.skip) continue;
-                if (n > hh_min_n) qr_big.push_back(QrTask{nullptr, nullptr, A.wf, n, A.wf, 0, A.wf, 0});
+                if (n > hh_min_n) {
+                    qr_big.push_back(QrTask{nullptr, nullptr, A.wf, n, A.wf, 0, A.wf, 0});
+                    qr_big_perm.push_back(nullptr);
+                }
                 if (n <= svd_smem_max) max_n_small = std::max(max_n_small, n);
                 else svd_big.push_back(SvdTask{nullptr, nullptr, A.m, n, nullptr, nb});
                 continue;
@@ -537,6 +547,13 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             SvdTask sv{R, A.U, m, n, kept_d + bi, nb};
             if (n > hh_min_n) {
                 qr_big.push_back(QrTask{Z, R, wf, n, wf, 0, wf, 0});
+                int32_t* pv = nullptr;
+                if (qr_pivot && n > svd_smem_max) {
+                    pv = scr.alloc_n<int32_t>(n);
+                    unperm.push_back(UnpermTask{A.U, scr.alloc_n<double>(int64_t(m) * n), pv, m, n});
+                    max_unperm = std::max(max_unperm, m * n);
+                }
+                qr_big_perm.push_back(pv);
             } else {
                 // two-level TSQR: segments of <= seg columns fold into
                 // their own R (written transposed side by side), then one
@@ -588,7 +605,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             double f = 0, b = 0;
             qr_work(qr_big, f, b);
             ProfScope ps(K_QR_BIG, f, b);
-            qr_r_blocked(qr_big, scr);
+            qr_r_blocked(qr_big, scr, &qr_big_perm);
         }
         if (!svd_small.empty()) {
             double f = 0, b = 0;
@@ -601,6 +618,9 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
             svd_work(svd_big, f, b);
             ProfScope ps(K_JACOBI_BIG, f, b);
             jacobi_multi_cta(svd_big, svd_thresh, scr);
+            // the Jacobi worked on R of the column-pivoted Z^T: its vectors
+            // are in pivoted coordinates, u[perm[i]] = w[i]
+            if (!unperm.empty()) launch_unpermute_rows(upload(unperm), int32_t(unperm.size()), max_unperm, st);
         }
     }
     int* kept_h = static_cast<int*>(X.pinned_buf(sizeof(int) * 2 * nb));

@@ -10,6 +10,7 @@
 // partial sums are reduced in a fixed order, so the factor is bitwise
 // reproducible.  The trailing update A -= V T^T (V^T A) runs on the DMMA tile
 // GEMM (k_gemm.cu) between panels.
+#include <algorithm>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -334,6 +335,75 @@ __global__ void __launch_bounds__(HT, 1) hh_panel_cluster_kernel(const HhPanelTa
     cluster.sync();  // the other CTAs' shared memory stays live until CTA 0 has read it
 }
 
+
+// ---- block column pivoting -------------------------------------------------
+// (1) remaining squared norms of the trailing columns, one warp per column
+__global__ void pivot_norms_kernel(const PivotTask* __restrict__ tasks) {
+    const PivotTask P = tasks[blockIdx.y];
+    const int lane = threadIdx.x & 31;
+    const int c = P.j0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (c >= P.ntot) return;
+    const double* col = P.M + (int64_t)c * P.ldm;
+    double s = 0.0;
+    for (int i = P.j0 + lane; i < P.L; i += 32) s += col[i] * col[i];
+    s = warp_sum(s);
+    if (lane == 0) P.norms[c] = s;
+}
+// (2) rank sort (descending norm, ties by index): order[rank] = column;
+// the permutation composes into perm
+__global__ void pivot_rank_kernel(const PivotTask* __restrict__ tasks) {
+    const PivotTask P = tasks[blockIdx.x];
+    const int nc = P.ntot - P.j0;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+        const double v = P.norms[P.j0 + i];
+        int r = 0;
+        for (int j = 0; j < nc; ++j) {
+            const double w = P.norms[P.j0 + j];
+            r += (w > v) || (w == v && j < i);
+        }
+        P.order[r] = i;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) P.perm_tmp[i] = P.perm[P.j0 + P.order[i]];
+    __syncthreads();
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) P.perm[P.j0 + i] = P.perm_tmp[i];
+}
+// (3) gather the columns into tmp in their new order, (4) copy back
+__global__ void pivot_gather_kernel(const PivotTask* __restrict__ tasks) {
+    const PivotTask P = tasks[blockIdx.z];
+    const int nc = P.ntot - P.j0;
+    const int c = blockIdx.y;
+    if (c >= nc) return;
+    const double* src = P.M + (int64_t)(P.j0 + P.order[c]) * P.ldm;
+    double* dst = P.tmp + (int64_t)c * P.L;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.L; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+__global__ void pivot_scatter_kernel(const PivotTask* __restrict__ tasks) {
+    const PivotTask P = tasks[blockIdx.z];
+    const int nc = P.ntot - P.j0;
+    const int c = blockIdx.y;
+    if (c >= nc) return;
+    const double* src = P.tmp + (int64_t)c * P.L;
+    double* dst = P.M + (int64_t)(P.j0 + c) * P.ldm;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.L; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+__global__ void iota_kernel(int32_t* p, int32_t n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = i;
+}
+__global__ void unpermute_rows_kernel(const UnpermTask* __restrict__ tasks, int phase) {
+    const UnpermTask T = tasks[blockIdx.y];
+    const int64_t tot = (int64_t)T.m * T.n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        if (phase == 0) {
+            T.tmp[e] = T.U[e];
+        } else {
+            const int64_t j = e / T.n, i = e % T.n;
+            T.U[j * T.n + T.perm[i]] = T.tmp[e];
+        }
+    }
+}
+
 // out[a][c] = sum_b op(T)[a][b] * (sum_ch P[ch][b][c]),  op(T) = T^T (trans) or T
 // 32 columns per CTA, 8 row-threads: the split-K partial sums of the 32 x 32
 // block S are formed with independent loads (4 rows per thread), then T (or
@@ -430,6 +500,32 @@ cudaError_t launch_hh_panel_cluster(const HhPanelTask* d_tasks, int32_t ntasks, 
     cudaError_t e = cudaLaunchKernelEx(&cfg, hh_panel_cluster_kernel, d_tasks);
     count_launch();
     return e;
+}
+
+void launch_pivot_panel(const PivotTask* d_tasks, int32_t ntasks, int32_t max_cols, int32_t max_l,
+                        cudaStream_t st) {
+    if (ntasks <= 0 || max_cols <= 0) return;
+    pivot_norms_kernel<<<dim3((max_cols + 7) / 8, ntasks), 256, 0, st>>>(d_tasks);
+    pivot_rank_kernel<<<ntasks, 512, 0, st>>>(d_tasks);
+    const int gx = (max_l + 255) / 256;
+    pivot_gather_kernel<<<dim3(gx, max_cols, ntasks), 256, 0, st>>>(d_tasks);
+    pivot_scatter_kernel<<<dim3(gx, max_cols, ntasks), 256, 0, st>>>(d_tasks);
+    for (int i = 0; i < 4; ++i) count_launch();
+}
+
+void launch_iota(int32_t* p, int32_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    iota_kernel<<<(n + 255) / 256, 256, 0, st>>>(p, n);
+    count_launch();
+}
+
+void launch_unpermute_rows(const UnpermTask* d_tasks, int32_t ntasks, int32_t max_mn, cudaStream_t st) {
+    if (ntasks <= 0 || max_mn <= 0) return;
+    const dim3 grid(std::min(1024, (max_mn + 255) / 256), ntasks);
+    unpermute_rows_kernel<<<grid, 256, 0, st>>>(d_tasks, 0);
+    unpermute_rows_kernel<<<grid, 256, 0, st>>>(d_tasks, 1);
+    count_launch();
+    count_launch();
 }
 
 void launch_hh_tmul(const HhTmulTask* d_tasks, int32_t ntasks, int32_t max_cols, cudaStream_t st) {

@@ -289,6 +289,32 @@ void launch_sumsq_reduce(const double* d_parts, const int64_t* d_seg, int32_t ns
 
 size_t hh_panel_smem(int chunk);
 int hh_panel_capacity(int chunk);  // co-resident CTAs of the panel kernel at this chunk
+// ---- block column pivoting of the blocked Householder QR (augmentation):
+// before each panel, the trailing columns [j0, ntot) of a job are reordered
+// by their remaining norms (rows [j0, L)), descending (ties: lower index
+// first).  Columns live at M + c*ldm with L contiguous rows.
+struct PivotTask {
+    double* M;
+    int64_t ldm;
+    int32_t L, j0, ntot;
+    double* norms;       // ntot scratch
+    int32_t* order;      // ntot scratch: new position -> old column (local, from j0)
+    int32_t* perm;       // ntot: current column -> original column (updated)
+    int32_t* perm_tmp;   // ntot scratch
+    double* tmp;         // (ntot - j0) * L scratch
+};
+void launch_pivot_panel(const PivotTask* d_tasks, int32_t ntasks, int32_t max_cols, int32_t max_l,
+                        cudaStream_t st);
+void launch_iota(int32_t* p, int32_t n, cudaStream_t st);
+// U[j][perm[i]] = W[j][i] for the first m rows of the n x n U (in place
+// through scratch): un-permutes the Jacobi's vectors of a pivoted R
+struct UnpermTask {
+    double* U;
+    double* tmp;         // m * n scratch
+    const int32_t* perm;
+    int32_t m, n;
+};
+void launch_unpermute_rows(const UnpermTask* d_tasks, int32_t ntasks, int32_t max_mn, cudaStream_t st);
 // panels of ntasks tasks, each one thread-block cluster of `cluster` CTAs
 // (2..16) holding `chunk` rows each (<= HH_CLUSTER_CHUNK); task.cta0/ncta,
 // part, gram and bar are unused

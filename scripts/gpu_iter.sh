@@ -1,2 +1,3 @@
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_boundary.py -x -q > gpurun_out/it_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/it_pytest.log
-timeout 1500 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/it_bench.json 2> gpurun_out/it_bench.err
+timeout 1500 python -m pytest tests/test_gpu_dense.py tests/test_gpu_parity.py tests/test_gpu_sharded.py -x -q > gpurun_out/it_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/it_pytest.log
+echo pivot; timeout 800 python scripts/level_profile.py 2>&1 | grep -oE "factorize \(profiler off\).*|jacobi_svd_coop=[0-9.]+|qr_r_blocked=[0-9.]+" | tr '\n' ' '; echo
+echo nopivot; H2F_QR_PIVOT=0 timeout 800 python scripts/level_profile.py 2>&1 | grep -oE "factorize \(profiler off\).*|jacobi_svd_coop=[0-9.]+|qr_r_blocked=[0-9.]+" | tr '\n' ' '; echo
