@@ -93,9 +93,14 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
                             scr.alloc_n<double>(int64_t(J.ntot) * J.L)};
         launch_iota(J.perm, J.ntot, st);
     }
+    // pivoting at the first panels only: the sweep saving of the Jacobi
+    // comes from moving the large-norm columns to the front (numpy study:
+    // the same sweep counts as pivoting before every panel), while each
+    // pivot step copies the whole trailing matrix
+    static const int piv_panels = env_int("H2F_QR_PIVOT_PANELS", 6);
     for (int p = 0; p < maxp; ++p) {
         const int j0 = p * HH_NB;
-        {
+        if (p < piv_panels) {
             std::vector<PivotTask> pt;
             int max_cols = 0, max_l = 0;
             for (size_t i = 0; i < jobs.size(); ++i) {
