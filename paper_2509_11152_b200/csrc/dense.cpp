@@ -90,7 +90,7 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
         HhJob& J = jobs[i];
         if (!J.perm || !J.M) continue;
         piv[i] = PivScratch{scr.alloc_n<double>(J.ntot), scr.alloc_n<int32_t>(J.ntot), scr.alloc_n<int32_t>(J.ntot),
-                            scr.alloc_n<double>(int64_t(J.ntot) * J.L)};
+                            scr.alloc_n<double>(int64_t(J.ntot) * J.ldm)};
         launch_iota(J.perm, J.ntot, st);
     }
     // pivoting at the first panels only: the sweep saving of the Jacobi
@@ -108,10 +108,16 @@ void hh_factor(std::vector<HhJob>& jobs, Region& scr, bool keep) {
                 if (!J.perm || !J.M || j0 >= J.nfac || J.ntot - j0 < 2) continue;
                 pt.push_back(PivotTask{J.M, J.ldm, J.L, j0, J.ntot, piv[i].norms, piv[i].order, J.perm, piv[i].perm_tmp,
                                        piv[i].tmp});
-                max_cols = std::max(max_cols, J.ntot - j0);
+                max_cols = std::max(max_cols, J.ntot);
                 max_l = std::max(max_l, J.L);
             }
             if (!pt.empty()) launch_pivot_panel(upload(pt), int32_t(pt.size()), max_cols, max_l, st);
+            // the reordered matrix lives in the other buffer from now on
+            for (size_t i = 0; i < jobs.size(); ++i) {
+                HhJob& J = jobs[i];
+                if (!J.perm || !J.M || j0 >= J.nfac || J.ntot - j0 < 2) continue;
+                std::swap(J.M, piv[i].tmp);
+            }
         }
         std::vector<PanelPlan> all;
         for (size_t i = 0; i < jobs.size(); ++i) {
@@ -320,10 +326,12 @@ void qr_r_blocked(const std::vector<QrTask>& tasks, Region& scr, const std::vect
         J.ntot = t.s;
         J.nfac = std::min(t.s, t.wf);
         jobs.push_back(J);
-        if (t.Y) ex.push_back(RExtractTask{t.Y, t.R, t.ldy, J.nfac, t.s});
         maxn = std::max(maxn, t.s);
     }
     hh_factor(jobs, scr, false);
+    // R from each job's final buffer (pivoted jobs alternate between two)
+    for (size_t ti = 0; ti < tasks.size(); ++ti)
+        if (tasks[ti].Y) ex.push_back(RExtractTask{jobs[ti].M, tasks[ti].R, tasks[ti].ldy, jobs[ti].nfac, tasks[ti].s});
     if (!ex.empty()) launch_r_extract(upload(ex), int32_t(ex.size()), maxn, ctx().stream);
 }
 

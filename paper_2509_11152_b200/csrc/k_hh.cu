@@ -368,24 +368,19 @@ __global__ void pivot_rank_kernel(const PivotTask* __restrict__ tasks) {
     __syncthreads();
     for (int i = threadIdx.x; i < nc; i += blockDim.x) P.perm[P.j0 + i] = P.perm_tmp[i];
 }
-// (3) gather the columns into tmp in their new order, (4) copy back
+// (3) the job's matrix in its new column order into the other buffer (tmp,
+// same ldm): trailing columns whole, in the new order; the factored columns
+// [0, j0) only their R rows [0, j0) (their reflectors live in Vt) -- the
+// caller then swaps the two buffers
 __global__ void pivot_gather_kernel(const PivotTask* __restrict__ tasks) {
     const PivotTask P = tasks[blockIdx.z];
-    const int nc = P.ntot - P.j0;
     const int c = blockIdx.y;
-    if (c >= nc) return;
-    const double* src = P.M + (int64_t)(P.j0 + P.order[c]) * P.ldm;
-    double* dst = P.tmp + (int64_t)c * P.L;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.L; i += gridDim.x * blockDim.x) dst[i] = src[i];
-}
-__global__ void pivot_scatter_kernel(const PivotTask* __restrict__ tasks) {
-    const PivotTask P = tasks[blockIdx.z];
-    const int nc = P.ntot - P.j0;
-    const int c = blockIdx.y;
-    if (c >= nc) return;
-    const double* src = P.tmp + (int64_t)c * P.L;
-    double* dst = P.M + (int64_t)(P.j0 + c) * P.ldm;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.L; i += gridDim.x * blockDim.x) dst[i] = src[i];
+    if (c >= P.ntot) return;
+    const bool done = c < P.j0;
+    const double* src = P.M + (int64_t)(done ? c : P.j0 + P.order[c - P.j0]) * P.ldm;
+    double* dst = P.tmp + (int64_t)c * P.ldm;
+    const int rows = done ? P.j0 : P.L;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 __global__ void iota_kernel(int32_t* p, int32_t n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -509,8 +504,7 @@ void launch_pivot_panel(const PivotTask* d_tasks, int32_t ntasks, int32_t max_co
     pivot_rank_kernel<<<ntasks, 512, 0, st>>>(d_tasks);
     const int gx = (max_l + 255) / 256;
     pivot_gather_kernel<<<dim3(gx, max_cols, ntasks), 256, 0, st>>>(d_tasks);
-    pivot_scatter_kernel<<<dim3(gx, max_cols, ntasks), 256, 0, st>>>(d_tasks);
-    for (int i = 0; i < 4; ++i) count_launch();
+    for (int i = 0; i < 3; ++i) count_launch();
 }
 
 void launch_iota(int32_t* p, int32_t n, cudaStream_t st) {

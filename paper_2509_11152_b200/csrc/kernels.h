@@ -301,8 +301,9 @@ struct PivotTask {
     int32_t* order;      // ntot scratch: new position -> old column (local, from j0)
     int32_t* perm;       // ntot: current column -> original column (updated)
     int32_t* perm_tmp;   // ntot scratch
-    double* tmp;         // (ntot - j0) * L scratch
+    double* tmp;         // ntot * ldm: receives the reordered matrix (buffers swap)
 };
+// max_cols: the largest ntot of the launch (all columns are visited)
 void launch_pivot_panel(const PivotTask* d_tasks, int32_t ntasks, int32_t max_cols, int32_t max_l,
                         cudaStream_t st);
 void launch_iota(int32_t* p, int32_t n, cudaStream_t st);
