@@ -345,6 +345,7 @@ __global__ void pivot_norms_kernel(const PivotTask* __restrict__ tasks) {
     if (c >= P.ntot) return;
     const double* col = P.M + (int64_t)c * P.ldm;
     double s = 0.0;
+#pragma unroll 8
     for (int i = P.j0 + lane; i < P.L; i += 32) s += col[i] * col[i];
     s = warp_sum(s);
     if (lane == 0) P.norms[c] = s;
