@@ -8,6 +8,7 @@ the reference's H2Matrix and paper_2509_11152_b200.problem.H2Matrix work.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -27,6 +28,31 @@ def _fingerprint(h2):
     return hash(tuple(ids)), id(h2.tree), id(h2.partition)
 
 
+def _pack(blocks, total):
+    """The blocks at their offsets in one float64 array: slices copied by a
+    thread pool (NumPy releases the GIL for the copies; a config-2 operator
+    is ~1e5 blocks, 4.5 GB, which one thread copies in about a second)."""
+    vals = np.empty(max(total, 1))
+    if not blocks:
+        return vals
+    nthreads = max(1, min(16, os.cpu_count() or 1))
+    if total < (1 << 24) or nthreads == 1:
+        for a, off in blocks:
+            vals[off:off + a.size] = a
+        return vals
+    from concurrent.futures import ThreadPoolExecutor
+
+    step = (len(blocks) + 4 * nthreads - 1) // (4 * nthreads)
+
+    def run(i0):
+        for a, off in blocks[i0:i0 + step]:
+            vals[off:off + a.size] = a
+
+    with ThreadPoolExecutor(nthreads) as ex:
+        list(ex.map(run, range(0, len(blocks), step)))
+    return vals
+
+
 class DeviceMatrix:
     """An H2 operator uploaded to the B200 (h2f_matrix)."""
 
@@ -40,13 +66,13 @@ class DeviceMatrix:
         rank = np.full(nnodes, -1, dtype=np.int64)
         for c, k in h2.rank.items():
             rank[int(c)] = int(k)
-        blocks = []
+        blocks = []  # (flat block, offset): packed into one array below
         pos = 0
 
         def place(arr):
             nonlocal pos
             a = np.ascontiguousarray(arr, dtype=np.float64)
-            blocks.append(a.ravel())
+            blocks.append((a.ravel(), pos))
             off = pos
             pos += a.size
             return off
@@ -77,7 +103,7 @@ class DeviceMatrix:
         adm_pairs, adm_ptr, coup_off = level_lists(adm, h2.coupling)
         inner_pairs, inner_ptr, _ = level_lists(inner, None)
         dense_pairs, dense_ptr, dense_off = level_lists(dense_lv, h2.dense)
-        vals = np.concatenate(blocks) if blocks else np.zeros(1)
+        vals = _pack(blocks, pos)
         keep = dict(parent=as_i64(tree.parent), left=as_i64(tree.child_left),
                     right=as_i64(tree.child_right), level=as_i64(tree.level),
                     begin=as_i64(tree.begin), end=as_i64(tree.end), rank=rank,
