@@ -426,6 +426,9 @@ def run_b200(args, cfg):
         "clocks": clk,
         "backward_error": e_b,
         "backward_error_reference": REF_EB.get(next(k for k, v in CONFIGS.items() if v is cfg)),
+        # north_star's contract: within 10x of the reference's on the same operator
+        "backward_error_within_10x": (None if REF_EB.get(next(k for k, v in CONFIGS.items() if v is cfg)) is None
+                                      else bool(e_b <= 10 * REF_EB[next(k for k, v in CONFIGS.items() if v is cfg)])),
         "backward_error_note": ("refined e_b = ||A x - b|| / ||b|| of the last timed step (harness.py:215); at "
                                 "N=131072 it is chaotic for both implementations under 1e-14 operator "
                                 "perturbations (DESIGN.md §5, profiles/r02_draws_config2*.jsonl)"),
