@@ -105,7 +105,10 @@ __global__ void __launch_bounds__(DT) qr_r_smem_kernel(const QrTask* __restrict_
 // iteration instead of a final sweep that would rotate nothing.  The rotate
 // helpers return 0 (no rotation), 1 (settling rotation) or 2 (rotation with
 // |cos| > 1e-7, another sweep is needed).
-constexpr double JAC_SETTLE2 = 1e-14;
+#ifndef H2F_JAC_SETTLE2
+#define H2F_JAC_SETTLE2 1e-14
+#endif
+constexpr double JAC_SETTLE2 = H2F_JAC_SETTLE2;
 
 // Jacobi rotation annihilating the (p, q) inner product: a = |x_p|^2,
 // b = |x_q|^2, g = x_p.x_q.  Rotate iff |g| > tol sqrt(a b) (tested

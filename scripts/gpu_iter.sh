@@ -1,2 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_boundary.py -x -q > gpurun_out/it_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/it_pytest.log
-timeout 1500 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/it_bench.json 2> gpurun_out/it_bench.err
+run() { echo "$1"; env $1 timeout 800 python scripts/level_profile.py 2>&1 | grep -oE "factorize \(profiler off\).*|jacobi_svd_coop +[0-9.]+|jacobi_svd +[0-9.]+" | tr '\n' ' '; echo; }
+run "H2F_X=0"
+run "H2F_LIB=paper_2509_11152_b200/libh2f_s12.so"
+H2F_LIB=paper_2509_11152_b200/libh2f_s12.so timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_dense.py -x -q 2>&1 | tail -3
