@@ -1,5 +1,6 @@
-# development iteration on the GPU box (edited per experiment): the
-# reference's own tests/test_solve.py (copied by the caller into the
-# git-ignored work/ref_tests/, it never enters the repository) through the
-# h2factor alias package
-cd work/ref_tests && PYTHONPATH=$GRAFT_REPO_ROOT/tests/h2factor_shim:$GRAFT_REPO_ROOT timeout 900 python -m pytest test_solve.py -q -p no:cacheprovider > $GRAFT_REPO_ROOT/gpurun_out/ref_test_solve.log 2>&1; echo "rc=$?" >> $GRAFT_REPO_ROOT/gpurun_out/ref_test_solve.log
+# development iteration on the GPU box (edited per experiment)
+run() { echo "$1"; env $1 timeout 800 python scripts/level_profile.py 2>&1 | grep -oE "factorize \(profiler off\).*|jacobi_svd_coop +[0-9.]+|jacobi_svd +[0-9.]+|qr_r_blocked +[0-9.]+|qr_r +[0-9.]+" | tr '\n' ' '; echo; }
+run "H2F_X=0"
+run "H2F_SVD_SMEM_MAX=96"
+run "H2F_SVD_SMEM_MAX=48"
+run "H2F_GEMM_PREC_KMAX=160"
