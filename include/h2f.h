@@ -153,6 +153,13 @@ int h2f_dense_complement(const double* BT, int32_t s, int32_t kt, int32_t path, 
 
 /* ---- H2 matrix ----------------------------------------------------------- */
 int h2f_matrix_create(const h2f_matrix_desc* desc, const double* vals, h2f_matrix* out);
+/* the same operator with its values given block by block (HOST pointers,
+ * element counts, offsets into the value array, offsets ascending): no
+ * packed host copy is needed -- the library packs pinned chunks in parallel
+ * and overlaps them with the upload (what a binding of the reference's
+ * dict-of-blocks H2Matrix passes) */
+int h2f_matrix_create_blocks(const h2f_matrix_desc* desc, int64_t num_blocks, const double* const* block_ptrs,
+                             const int64_t* block_counts, const int64_t* block_offsets, h2f_matrix* out);
 int h2f_matrix_destroy(h2f_matrix m);
 int h2f_matrix_nbytes(h2f_matrix m, int64_t* bytes);
 int h2f_matvec(h2f_matrix m, const double* x, double* y, int64_t nrhs);

@@ -110,6 +110,8 @@ _SIGS = {
     "h2f_dense_qr_r": (C.c_int, [f64p, C.c_int32, C.c_int32, C.c_int32, f64p, f64p]),
     "h2f_dense_complement": (C.c_int, [f64p, C.c_int32, C.c_int32, C.c_int32, f64p, f64p]),
     "h2f_matrix_create": (C.c_int, [C.POINTER(MatrixDesc), f64p, C.POINTER(C.c_void_p)]),
+    "h2f_matrix_create_blocks": (C.c_int, [C.POINTER(MatrixDesc), C.c_int64, C.POINTER(C.c_void_p), i64p, i64p,
+                                           C.POINTER(C.c_void_p)]),
     "h2f_matrix_destroy": (C.c_int, [C.c_void_p]),
     "h2f_matrix_nbytes": (C.c_int, [C.c_void_p, i64p]),
     "h2f_matrix_build": (C.c_int, [C.POINTER(BuildDesc), C.POINTER(C.c_void_p), i64p, f64p]),

@@ -262,6 +262,16 @@ int h2f_matrix_create(const h2f_matrix_desc* desc, const double* vals, h2f_matri
     });
 }
 
+int h2f_matrix_create_blocks(const h2f_matrix_desc* desc, int64_t num_blocks, const double* const* block_ptrs,
+                             const int64_t* block_counts, const int64_t* block_offsets, h2f_matrix* out) {
+    return guard([&] {
+        if (!desc || !out || (num_blocks && (!block_ptrs || !block_counts || !block_offsets)))
+            throw Error(H2F_E_ARG, "null argument");
+        H2Mat* m = h2mat_create_blocks(desc, num_blocks, block_ptrs, block_counts, block_offsets);
+        *out = new h2f_matrix_s{m};
+    });
+}
+
 int h2f_matrix_destroy(h2f_matrix m) {
     return guard([&] {
         if (!m) return;

@@ -6,6 +6,7 @@
 // final per-leaf gather of dense blocks (both orientations) plus V yhat.  Each
 // output segment is owned by one CTA that sums its contributions in a fixed
 // order, so there are no write conflicts and no atomics.
+#include <cstring>
 #include "h2mat.h"
 
 #include <algorithm>
@@ -81,6 +82,62 @@ H2Mat* h2mat_create(const h2f_matrix_desc* d, const double* host_vals) {
         H2F_CUDA(cudaMemcpyAsync(m->vals, host_vals, sizeof(double) * d->nvals, cudaMemcpyHostToDevice,
                                  ctx().stream));
     ctx().sync();
+    return m.release();
+}
+
+H2Mat* h2mat_create_blocks(const h2f_matrix_desc* d, int64_t nblk, const double* const* ptrs, const int64_t* counts,
+                           const int64_t* offs) {
+    // the value array is assembled chunk by chunk in pinned staging memory
+    // (OpenMP copies of the blocks overlapping the chunk) and shipped with
+    // async copies, two staging buffers alternating: packing overlaps the
+    // transfer, and no host-side copy of the whole operator is made
+    for (int64_t i = 0; i < nblk; ++i)
+        if (counts[i] < 0 || offs[i] < 0 || offs[i] + counts[i] > d->nvals || (i && offs[i] < offs[i - 1]))
+            throw Error(H2F_E_ARG, "block list: offsets must be ascending and inside nvals");
+    auto m = h2mat_structure(d);
+    m->vals = static_cast<double*>(dalloc(sizeof(double) * std::max<int64_t>(d->nvals, 1)));
+    cudaStream_t st = ctx().stream;
+    constexpr int64_t CH = int64_t(32) << 20;  // doubles per chunk (256 MB)
+    double* stage[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    const int64_t nchunk = (d->nvals + CH - 1) / CH;
+    const int nbuf = nchunk > 1 ? 2 : 1;
+    try {
+        for (int b = 0; b < nbuf; ++b) {
+            H2F_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&stage[b]), sizeof(double) * std::min(CH, std::max<int64_t>(d->nvals, 1)),
+                                   cudaHostAllocDefault));
+            H2F_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+        }
+        int64_t first = 0;  // first block that may overlap the chunk
+        for (int64_t k = 0; k < nchunk; ++k) {
+            const int b = int(k % nbuf);
+            const int64_t lo = k * CH, hi = std::min(d->nvals, lo + CH);
+            if (k >= nbuf) H2F_CUDA(cudaEventSynchronize(done[b]));  // its previous transfer is complete
+            while (first < nblk && offs[first] + counts[first] <= lo) ++first;
+            int64_t last = first;
+            while (last < nblk && offs[last] < hi) ++last;
+            double* dst = stage[b];
+            std::memset(dst, 0, sizeof(double) * size_t(hi - lo));  // gaps between blocks (none in practice)
+#pragma omp parallel for schedule(dynamic, 64)
+            for (int64_t i = first; i < last; ++i) {
+                const int64_t a = std::max(lo, offs[i]), e = std::min(hi, offs[i] + counts[i]);
+                if (e > a) std::memcpy(dst + (a - lo), ptrs[i] + (a - offs[i]), sizeof(double) * size_t(e - a));
+            }
+            H2F_CUDA(cudaMemcpyAsync(m->vals + lo, dst, sizeof(double) * size_t(hi - lo), cudaMemcpyHostToDevice, st));
+            H2F_CUDA(cudaEventRecord(done[b], st));
+        }
+        ctx().sync();
+    } catch (...) {
+        for (int b = 0; b < 2; ++b) {
+            if (done[b]) cudaEventDestroy(done[b]);
+            if (stage[b]) cudaFreeHost(stage[b]);
+        }
+        throw;
+    }
+    for (int b = 0; b < 2; ++b) {
+        if (done[b]) cudaEventDestroy(done[b]);
+        if (stage[b]) cudaFreeHost(stage[b]);
+    }
     return m.release();
 }
 

@@ -67,6 +67,10 @@ struct H2Mat {
 };
 
 H2Mat* h2mat_create(const h2f_matrix_desc* d, const double* host_vals);
+// values given as blocks (pointer, count, offset in the value array;
+// offsets ascending): packed in pinned chunks overlapped with the upload
+H2Mat* h2mat_create_blocks(const h2f_matrix_desc* d, int64_t nblk, const double* const* ptrs, const int64_t* counts,
+                           const int64_t* offs);
 // takes ownership of dev_vals (an arena allocation of d->nvals doubles)
 H2Mat* h2mat_create_device(const h2f_matrix_desc* d, double* dev_vals);
 // device construction + recompression from points, tree and partition (build.cpp)

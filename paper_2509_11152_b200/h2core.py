@@ -8,7 +8,6 @@ the reference's H2Matrix and paper_2509_11152_b200.problem.H2Matrix work.
 from __future__ import annotations
 
 import ctypes as C
-import os
 
 import numpy as np
 
@@ -28,31 +27,6 @@ def _fingerprint(h2):
     return hash(tuple(ids)), id(h2.tree), id(h2.partition)
 
 
-def _pack(blocks, total):
-    """The blocks at their offsets in one float64 array: slices copied by a
-    thread pool (NumPy releases the GIL for the copies; a config-2 operator
-    is ~1e5 blocks, 4.5 GB, which one thread copies in about a second)."""
-    vals = np.empty(max(total, 1))
-    if not blocks:
-        return vals
-    nthreads = max(1, min(16, os.cpu_count() or 1))
-    if total < (1 << 24) or nthreads == 1:
-        for a, off in blocks:
-            vals[off:off + a.size] = a
-        return vals
-    from concurrent.futures import ThreadPoolExecutor
-
-    step = (len(blocks) + 4 * nthreads - 1) // (4 * nthreads)
-
-    def run(i0):
-        for a, off in blocks[i0:i0 + step]:
-            vals[off:off + a.size] = a
-
-    with ThreadPoolExecutor(nthreads) as ex:
-        list(ex.map(run, range(0, len(blocks), step)))
-    return vals
-
-
 class DeviceMatrix:
     """An H2 operator uploaded to the B200 (h2f_matrix)."""
 
@@ -66,7 +40,7 @@ class DeviceMatrix:
         rank = np.full(nnodes, -1, dtype=np.int64)
         for c, k in h2.rank.items():
             rank[int(c)] = int(k)
-        blocks = []  # (flat block, offset): packed into one array below
+        blocks = []  # (flat block, offset in the value array)
         pos = 0
 
         def place(arr):
@@ -103,7 +77,7 @@ class DeviceMatrix:
         adm_pairs, adm_ptr, coup_off = level_lists(adm, h2.coupling)
         inner_pairs, inner_ptr, _ = level_lists(inner, None)
         dense_pairs, dense_ptr, dense_off = level_lists(dense_lv, h2.dense)
-        vals = _pack(blocks, pos)
+        nvals = max(pos, 1)
         keep = dict(parent=as_i64(tree.parent), left=as_i64(tree.child_left),
                     right=as_i64(tree.child_right), level=as_i64(tree.level),
                     begin=as_i64(tree.begin), end=as_i64(tree.end), rank=rank,
@@ -118,13 +92,21 @@ class DeviceMatrix:
             adm_pairs=p["adm_pairs"], adm_ptr=p["adm_ptr"], inner_pairs=p["inner_pairs"],
             inner_ptr=p["inner_ptr"], dense_pairs=p["dense_pairs"], dense_ptr=p["dense_ptr"],
             leaf_basis_off=p["leaf_off"], transfer_off=p["trans_off"], coupling_off=p["coup_off"],
-            dense_off=p["dense_off"], nvals=int(vals.size))
+            dense_off=p["dense_off"], nvals=int(nvals))
         lib = L.ensure_init()
         handle = C.c_void_p()
-        L.check(lib.h2f_matrix_create(C.byref(desc), L.ptr(vals), C.byref(handle)), "h2f_matrix_create")
+        # the blocks as they are (no packed host copy): the library packs
+        # pinned chunks in parallel, overlapped with the upload
+        nb = len(blocks)
+        ptrs = (C.c_void_p * max(nb, 1))(*[a.ctypes.data for a, _ in blocks])
+        counts = np.fromiter((a.size for a, _ in blocks), dtype=np.int64, count=nb)
+        offs = np.fromiter((o for _, o in blocks), dtype=np.int64, count=nb)
+        L.check(lib.h2f_matrix_create_blocks(C.byref(desc), nb, ptrs, L.ptr(counts, L.i64p), L.ptr(offs, L.i64p),
+                                             C.byref(handle)), "h2f_matrix_create_blocks")
+        del blocks
         self.handle = handle
         self.n = n
-        self.nbytes = int(vals.size) * 8
+        self.nbytes = int(nvals) * 8
         self.key = _fingerprint(h2)
 
     def __del__(self):
