@@ -212,8 +212,11 @@ struct GemmBuild {
         // short average K per tile: the C read-modify-write dominates, use
         // the variant that prefetches C during the tile's math
         static const double kmax = [] {
+            // measured on config 2 (round 2): the C-prefetch variant is as
+            // fast or faster at every K (Schur 5.43 -> 5.35 s), so it is used
+            // throughout unless this caps it
             const char* e = std::getenv("H2F_GEMM_PREC_KMAX");
-            return e ? std::atof(e) : 96.0;
+            return e ? std::atof(e) : 1e30;
         }();
         const double keff = flops / (double(ntiles) * 2.0 * GEMM_TILE * GEMM_TILE);
         // K_eff below this: the register-direct short-K kernel (one tile per
