@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <iterator>
 #include <numeric>
 #include <set>
 
@@ -128,6 +129,18 @@ class Nbrs {
     const Entry* find(int o) const {
         auto it = std::lower_bound(v_.begin(), v_.end(), o, [](const Item& a, int b) { return a.first < b; });
         return (it != v_.end() && it->first == o) ? &it->second : nullptr;
+    }
+    // many new partners at once (none present yet): one sorted merge instead
+    // of an O(size) vector insert each -- the same final list as set() calls
+    void merge_new(std::vector<Item>& add) {
+        auto lt = [](const Item& a, const Item& b) { return a.first < b.first; };
+        std::sort(add.begin(), add.end(), lt);
+        std::vector<Item> out;
+        out.reserve(v_.size() + add.size());
+        std::merge(v_.begin(), v_.end(), add.begin(), add.end(), std::back_inserter(out), lt);
+        for (size_t i = 1; i < out.size(); ++i)
+            if (out[i].first == out[i - 1].first) throw Error(H2F_E_INTERNAL, "assertion: fill partner linked twice");
+        v_.swap(out);
     }
     std::vector<Item>::const_iterator begin() const { return v_.begin(); }
     std::vector<Item>::const_iterator end() const { return v_.end(); }
@@ -1297,6 +1310,7 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
     {
         GemmBuild create;
         std::unordered_map<Key, int> made;
+        std::vector<Key> linked;  // created fill keys, linked into the neighbour lists after the loop
         struct Target {
             double* C;
             int64_t ldc;
@@ -1336,16 +1350,27 @@ void Factorizer::process_batch(Lvl& L, const std::vector<int>& batch) {
                 L.fill_created.back().push_back(cd.key);
                 if (!cd.here) {  // another rank's block: structure only
                     L.F[cd.key] = View{nullptr, cd.N, cd.M, cd.N};
-                    L.link(cd.key, false);
+                    linked.push_back(cd.key);
                     made[cd.key] = -1;
                     continue;
                 }
                 double* blk = L.mem.alloc_n<double>(int64_t(cd.M) * cd.N);
                 L.F[cd.key] = View{blk, cd.N, cd.M, cd.N};
-                L.link(cd.key, false);
+                linked.push_back(cd.key);
                 made[cd.key] = int(news.size());
                 news.push_back({blk, cd.N, cd.M, cd.N, {cd.g}});
             }
+        }
+        if (!linked.empty()) {
+            // (nothing in the loop reads the neighbour lists, and no created
+            // block touches a batch cluster, so linking afterwards is the same)
+            std::unordered_map<int, std::vector<Nbrs::Item>> add;
+            for (Key k : linked) {
+                const Entry e{k, false, &L.F.at(k)};
+                add[L.at(key_a(k))].push_back({key_b(k), e});
+                add[L.at(key_b(k))].push_back({key_a(k), e});
+            }
+            for (auto& kv : add) L.touch[kv.first].merge_new(kv.second);
         }
         for (auto& t : news) create.add(t.C, t.ldc, t.M, t.N, GEMM_STORE, t.cs.data(), t.cs.size());
         create.launch(K_GEMM_CREATE);
